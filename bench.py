@@ -1,0 +1,335 @@
+"""Benchmark of the B200-native Seven-League online path generator (BASELINE.json metric:
+"7L path-steps/sec (device-timed) at 1/2/4/8 B200; % of tensor/FP32/HBM roofline").
+
+Workload (BASELINE.json configs[1], the config the metric is quoted on):
+  GBM mu=0.05 sigma=0.2 Y0=1, T=1, m=7 Gauss-Hermite nodes, [2,50,50,50,7] tanh MLP (oracle-fitted
+  weights), 10^7 paths per GPU, dt in {1, 1/2, ..., 1/64} (n = 1..64 steps: 127 path-steps per
+  path per sweep), TERMINAL output + fused statistics (moments, 4096-bin histogram) + strong error
+  against exact GBM on the same normals.  One bench "step" = one full dt sweep in ANN mode =
+  1.27e9 path-steps per GPU.  The exact-collocation sweep (the config's second mode) is timed
+  alongside and reported under "modes".
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--prec fp32|bf16]
+Under torchrun each rank takes paths [rank*N_P, (rank+1)*N_P) (weak scaling, Philox path offset)
+and the fp64 statistics vectors are summed with one NCCL all_reduce.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "7L path-steps/sec (device-timed)"
+UNIT = "path-steps/s"
+N_SWEEP = (1, 2, 4, 8, 16, 32, 64)
+N_BINS = 4096
+HIST = (0.0, 4.0)
+L2_FLUSH_BYTES = 512 << 20   # > 126 MB L2
+
+
+def ann_flops_per_path_step(dims):
+    """Algorithmic FLOPs of one MLP evaluation with layer 1 folded to rank 1 (2 FLOP per MAC)."""
+    f = 2 * dims[1]                       # layer 1: l1w*Y + l1b
+    for l in range(1, len(dims) - 1):
+        f += 2 * dims[l] * dims[l + 1]
+    return f
+
+
+class ClockSampler(threading.Thread):
+    """Samples SM clock and throttle reasons via NVML every 100 ms during the timed region."""
+
+    def __init__(self, index):
+        super().__init__(daemon=True)
+        self.index = index
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._halt = threading.Event()
+        self.ok = True
+
+    def run(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            names = {getattr(N, k): k for k in dir(N) if k.startswith("nvmlClocksThrottleReason") and
+                     isinstance(getattr(N, k), int)}
+            while not self._halt.is_set():
+                self.samples.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                for bit, name in names.items():
+                    if bit and bit != 0xFFFFFFFFFFFFFFFF and (r & bit) == bit and "All" not in name and "None" not in name:
+                        self.reasons.add(name.replace("nvmlClocksThrottleReason", ""))
+                time.sleep(0.1)
+        except Exception as e:  # NVML missing: report, do not fake
+            self.ok = False
+            self.reasons.add("nvml_error:%s" % type(e).__name__)
+
+    def stop(self):
+        self._halt.set()
+        self.join(timeout=2)
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------------------------------------ oracle
+
+def _oracle_chunk(args):
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)                      # one BLAS thread per pool worker
+    from oracle import sl7_oracle as O
+    from sl7_inputs import load_golden_blob
+    (blob_name, lo, n, seed, sweep) = args
+    net = O.parse_blob(load_golden_blob(blob_name))
+    paths = np.arange(lo, lo + n, dtype=np.uint64)
+    for ns in sweep:
+        spec = O.Spec(7, "ann", (), 1.0, 1.0 / ns, ns, net=net)
+        O.simulate(spec, seed, paths)
+    return n * sum(sweep)
+
+
+def oracle_throughput(n_paths, seed, blob_name, sweep=N_SWEEP):
+    """Time the float64 oracle (as it stands) over a bounded path sample on all host cores."""
+    import multiprocessing as mp
+    cores = len(os.sched_getaffinity(0))
+    chunk = max(1, -(-n_paths // cores))
+    jobs = [(blob_name, lo, min(chunk, n_paths - lo), seed, sweep) for lo in range(0, n_paths, chunk)]
+    for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[k] = "1"
+    ctx = mp.get_context("fork")
+    with ctx.Pool(min(cores, len(jobs))) as pool:
+        pool.map(_oracle_chunk, jobs[:1])              # warm the workers (imports)
+        t0 = time.perf_counter()
+        done = sum(pool.map(_oracle_chunk, jobs))
+        el = time.perf_counter() - t0
+    return done / el, cores, el, done
+
+
+# -------------------------------------------------------------------------------------------- main
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="sl7", choices=["sl7", "reference"])
+    ap.add_argument("--prec", default="auto", choices=["auto", "fp32", "bf16"])
+    ap.add_argument("--paths", type=int, default=10_000_000, help="paths per GPU")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    a = ap.parse_args()
+
+    from sl7_inputs import load_golden_blob, workloads
+    W = workloads()["cfg1"]
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    config = {"workload": "cfg1: GBM m=7 [2,50,50,50,7] tanh, 1e7 paths/GPU, dt sweep 1..1/64 (127 path-steps/path), "
+                          "TERMINAL + 4096-bin stats + strong error",
+              "paths_per_gpu": a.paths, "n_sweep": list(N_SWEEP), "m": W.m, "dims": list(W.dims),
+              "process": "gbm", "theta": list(W.theta), "l2": "flushed (512 MiB write) before every timed step"}
+
+    if a.impl == "reference":
+        if rank != 0:
+            return
+        sample = 32768
+        v, cores, el, done = 0.0, 0, 0.0, 0
+        t_all = []
+        for s in range(a.warmup + a.steps):
+            v, cores, el, done = oracle_throughput(sample, W.seed, W.blob)
+            if s >= a.warmup:
+                t_all.append(el)
+        val = done / statistics.mean(t_all)
+        line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": a.gpus,
+                "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * statistics.mean(t_all),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": dict(config, paths_per_step=sample),
+                "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                 "sample": "%d paths x 127 path-steps (full dt sweep), float64 numpy oracle, "
+                                           "multiprocessing pool" % sample},
+                "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import numpy as np
+    import torch
+    import paper_2302_05170_b200 as sl7
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    sl7.load_library()
+    blob = load_golden_blob(W.blob)
+    ctx = sl7.Context(W.m, list(W.dims), W.act, device=local)
+    ctx.load_weights(blob)
+    prec = {"auto": sl7.PREC_FP32, "fp32": sl7.PREC_FP32, "bf16": sl7.PREC_BF16}[a.prec]
+    if a.prec == "auto" and getattr(sl7, "HAS_TC", False):
+        prec = sl7.PREC_BF16
+    N = a.paths
+    offset = rank * N
+    stream = torch.cuda.current_stream()
+    dev = torch.device("cuda", local)
+    out = torch.empty(N, dtype=torch.float32, device=dev)
+    stats = {ns: torch.zeros(sl7.stats_elems(N_BINS), dtype=torch.float64, device=dev) for ns in N_SWEEP}
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    def opts_for(colloc, p=prec):
+        return sl7.make_opts(prec=p, colloc=colloc, path_offset=offset, stream=stream, hist_lo=HIST[0],
+                             hist_hi=HIST[1], shift=1.0, n_bins=N_BINS, ref=sl7.REF_GBM,
+                             ref_theta=(W.theta[0], W.theta[1], 0.0))
+
+    ann_opts = opts_for(sl7.COLLOC_ANN)
+    ex_opts = opts_for(sl7.COLLOC_EXACT_GBM, sl7.PREC_FP32)
+
+    def sweep(opts, colloc, evs=None):
+        th = () if colloc == sl7.COLLOC_ANN else W.theta
+        for k, ns in enumerate(N_SWEEP):
+            if evs is not None:
+                evs[k][0].record(stream)
+            ctx.simulate(W.y0, 1.0 / ns, ns, th, N, W.seed, sl7.OUT_TERMINAL, opts, out=out, stats=stats[ns])
+            if evs is not None:
+                evs[k][1].record(stream)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    for _ in range(a.warmup):
+        sweep(ann_opts, sl7.COLLOC_ANN)
+    barrier()
+
+    # ---------------- timed region: K ANN sweeps (device-timed with CUDA events on the launch stream)
+    clk = ClockSampler(local)
+    clk.start()
+    per_step_ms, kernel_ms = [], []
+    barrier()
+    for _ in range(a.steps):
+        flush.fill_(1.0)                                     # L2 flush (untimed)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in N_SWEEP]
+        sweep(ann_opts, sl7.COLLOC_ANN, evs)
+        torch.cuda.synchronize()
+        ks = [e0.elapsed_time(e1) for e0, e1 in evs]
+        kernel_ms.append(ks)
+        per_step_ms.append(sum(ks))
+    barrier()
+    clk.stop()
+    step_ms = statistics.mean(per_step_ms)
+    path_steps = N * sum(N_SWEEP)
+    if dist:
+        t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_ms = float(t.item())
+    value = world * path_steps / (step_ms * 1e-3)
+
+    # all-reduce of the statistics (the only collective of the path)
+    if dist:
+        for ns in N_SWEEP:
+            dist.all_reduce(stats[ns])
+    summ = {}
+    for ns in N_SWEEP:
+        s = sl7.stats_summary(stats[ns].cpu().numpy(), ann_opts, q_levels=[0.01, 0.5, 0.99])
+        summ[ns] = s
+
+    # ---------------- exact-collocation sweep (config 1's second mode), same timing discipline
+    ex_ms = []
+    for _ in range(max(1, a.steps)):
+        flush.fill_(1.0)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in N_SWEEP]
+        sweep(ex_opts, sl7.COLLOC_EXACT_GBM, evs)
+        torch.cuda.synchronize()
+        ex_ms.append(sum(e0.elapsed_time(e1) for e0, e1 in evs))
+    ex_stats = {}
+    for ns in N_SWEEP:
+        ex_stats[ns] = sl7.stats_summary(stats[ns].cpu().numpy(), ex_opts)["strong_err"]
+
+    # ---------------- e2e: the same sweep through the C ABI with HOST buffers (copies inside timing)
+    h_out = np.empty(N, dtype=np.float32)
+    h_st = np.empty(sl7.stats_elems(N_BINS), dtype=np.float64)
+    e2e_ms, up_b, down_b = [], 0, 0
+    for it in range(1 + a.steps):
+        barrier()
+        t0 = time.perf_counter()
+        up_b = down_b = 0
+        for ns in N_SWEEP:
+            _, _, u, d = ctx.simulate_host(W.y0, 1.0 / ns, ns, (), N, W.seed, sl7.OUT_TERMINAL, ann_opts, h_out, h_st)
+            up_b += u
+            down_b += d
+        el = time.perf_counter() - t0
+        if it:
+            e2e_ms.append(el * 1e3)
+    e2e_step = statistics.mean(e2e_ms)
+    if dist:
+        t = torch.tensor([e2e_step], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_step = float(t.item())
+
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+
+    # ---------------- roofline of the dominant kernel (the ANN step kernel)
+    peaks = measured_peaks()
+    sm_max = peaks.get("sm_max_mhz", 1965.0)
+    n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    flops_ps = ann_flops_per_path_step(W.dims)
+    tot_kernel_ms = statistics.mean([sum(k) for k in kernel_ms])
+    if prec == sl7.PREC_FP32:
+        achieved = flops_ps * path_steps / (tot_kernel_ms * 1e-3) / 1e12
+        peak = n_sms * 128 * 2 * sm_max * 1e6 / 1e12     # FP32 FFMA: 128 lanes/SM, 2 FLOP per FFMA
+        roof = {"bound": "alu", "pipe": "fp32 FFMA", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": None,
+                "peak_basis": "148 SM x 128 FFMA lanes x 2 FLOP x %g MHz (max SM clock, MEASURED_PEAKS.json)" % sm_max,
+                "algorithmic": "%d FLOP per path-step (rank-1 layer 1 + 2x50x50 + 50x7 MACs)" % flops_ps}
+    else:
+        bf16 = peaks.get("bf16_tflops", 1642.7)
+        achieved = flops_ps * path_steps / (tot_kernel_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s", "frac": achieved / bf16,
+                "traffic": None, "peak_basis": "MEASURED_PEAKS.json bf16_tflops (burst)"}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if prec == sl7.PREC_FP32 else "bf16", "data": "synthetic (oracle-fitted weights)",
+            "config": dict(config, prec="fp32" if prec == sl7.PREC_FP32 else "bf16", parallelism="dp%d" % world),
+            "roofline": roof, "gpu_launches": a.steps * 2 * len(N_SWEEP),
+            "clocks": clk.summary(),
+            "e2e": {"value": world * path_steps / (e2e_step * 1e-3), "unit": UNIT, "h2d_bytes_per_step": up_b,
+                    "d2h_bytes_per_step": down_b, "ms_per_step": e2e_step},
+            "modes": {"ann": {"path_steps_per_s": value, "strong_err_by_n": {ns: summ[ns]["strong_err"] for ns in N_SWEEP},
+                              "terminal_mean_n64": summ[64]["mean"], "terminal_var_n64": summ[64]["var"]},
+                      "exact_gbm": {"path_steps_per_s": world * path_steps / (statistics.mean(ex_ms) * 1e-3),
+                                    "strong_err_by_n": ex_stats}},
+            "kernel_ms_by_n": {ns: statistics.mean(k[i] for k in kernel_ms) for i, ns in enumerate(N_SWEEP)}}
+    if not a.no_cpu_baseline and world == 1:
+        sample = 32768
+        v, cores, el, done = oracle_throughput(sample, W.seed, W.blob)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                "sample": "%d paths x 127 path-steps (full dt sweep, %.1f s), float64 numpy oracle, "
+                                          "multiprocessing pool" % (sample, el)}
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

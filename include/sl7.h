@@ -1,0 +1,196 @@
+/*
+ * sl7.h -- C ABI of the B200-native Seven-League (7L) online path generator.
+ *
+ * The method (arXiv 2302.05170, "GPU acceleration of the Seven-League scheme", PAPER.md):
+ * for each of N_P Monte Carlo paths and each large step t_i -> t_{i+1} = t_i + dt
+ * (Algorithm I):
+ *   step 3 (Eq. 6.4): predict the m conditional collocation points
+ *           y_j = H_hat_j(Y_i, dt, theta) with a trained MLP (or, in the "exact-collocation"
+ *           modes, with the closed form H_j of Eq. 6.3 for GBM / OU (Eq. 6.6));
+ *   step 6: draw X_hat ~ N(0,1)  (Philox4x32-10 + Box-Muller keyed by
+ *           (seed, path, step), see sl7_philox_u32 below);
+ *   steps 5-6: Y_{i+1} = g_m(X_hat), g_m the (barycentric)
+ *           Lagrange interpolant through (x_j, y_j) on the m Gauss-Hermite nodes x_j;
+ *   steps 7-8: collect all paths at t_{i+1}, loop until T.
+ *
+ * Everything between sl7_simulate's entry and its return runs in the library's own CUDA
+ * kernels for sm_100a.  There is no CPU fallback: on a machine without a usable device every
+ * compute entry point returns SL7_ECUDA.
+ *
+ * Conventions
+ *   - "d_" pointers are DEVICE pointers on the context's device, "h_" pointers are HOST
+ *     pointers.  The caller owns every buffer it passes; the library never frees them.
+ *   - All compute calls are asynchronous on the caller's CUDA stream (opts->stream, a
+ *     cudaStream_t; NULL = legacy default stream) unless stated otherwise.  Argument errors are
+ *     detected synchronously, before any launch, and leave the outputs untouched.
+ *   - Every call returns an sl7_status; sl7_last_error(ctx) gives a one-line message naming the
+ *     offending field (e.g. "layer_dims", "version").
+ *   - A context is bound to one device and is NOT thread-safe; use one context per thread.
+ */
+#ifndef SL7_H
+#define SL7_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SL7_ABI_VERSION 1
+#define SL7_MAX_M 16          /* nodes per collocation grid */
+#define SL7_MAX_WIDTH 64      /* hidden width of the MLP */
+#define SL7_MAX_HIDDEN 6      /* hidden layers of the MLP */
+#define SL7_MAX_THETA 8       /* model parameters appended to the network input */
+#define SL7_STATS_HEAD 8      /* doubles before the histogram in the stats vector */
+
+typedef struct sl7_ctx_s* sl7_ctx;
+
+typedef enum {
+  SL7_OK = 0,
+  SL7_EINVAL = 1,        /* an argument is out of range (message names it) */
+  SL7_ESTATE = 2,        /* call out of order, e.g. ANN mode before sl7_load_weights */
+  SL7_EFORMAT = 3,       /* malformed weights blob (message names the field) */
+  SL7_ENOMEM = 4,        /* host or device allocation failed */
+  SL7_ECUDA = 5,         /* no device / launch or copy failure (message holds cudaGetErrorString) */
+  SL7_ENONFINITE = 6,    /* sl7_stats: at least one non-finite terminal value was counted */
+  SL7_EUNSUPPORTED = 7   /* valid request this build does not implement (e.g. a precision mode) */
+} sl7_status;
+
+/* Hidden-layer activation (PAPER.md:85 uses Softplus; BASELINE configs 0,1,3 use tanh). */
+typedef enum { SL7_ACT_TANH = 0, SL7_ACT_SOFTPLUS = 1 } sl7_act;
+
+/* What sl7_simulate writes.
+ *  FULL:     d_out[i * n_paths + p] = Y_hat_i of path p, i = 0..n_steps (row 0 = Y0), fp32,
+ *            step-major (SPEC's N_P x (N+1) PathSet, transposed for coalescing).
+ *  TERMINAL: d_out[p] = Y_hat_{n_steps} of path p.
+ *  STATS:    no path output; only the fused statistics (d_stats required).
+ * In FULL and TERMINAL modes statistics are also accumulated when d_stats != NULL. */
+typedef enum { SL7_OUT_FULL = 0, SL7_OUT_TERMINAL = 1, SL7_OUT_STATS = 2 } sl7_out;
+
+/* Arithmetic of the ANN contractions (hidden layers 2..L and the output layer).
+ *  FP32:  CUDA-core fp32 FFMA, accurate activations ("exact mode").
+ *  BF16:  tcgen05 tensor cores, operands rounded to bf16 (RNE), fp32 accumulate, fp32 bias and
+ *         activations; reproduces the quantisation-aware oracle O6.
+ *  TF32:  tcgen05 kind::tf32, operands rounded with cvt.rna (reserved; SL7_EUNSUPPORTED here).
+ *  SPLIT: error-compensated multi-pass bf16 (reserved; SL7_EUNSUPPORTED here).
+ * Layer 1 (rank-1 in Y once dt and theta are folded into its bias) is always fp32. */
+typedef enum { SL7_PREC_FP32 = 0, SL7_PREC_TF32 = 1, SL7_PREC_BF16 = 2, SL7_PREC_SPLIT = 3 } sl7_prec;
+
+/* Source of the collocation points y_j (step 3 of Algorithm I).
+ *  ANN:        the loaded MLP, input (Y, dt, theta...) (Eq. 6.4).
+ *  EXACT_GBM:  y_j = Y exp((mu - sigma^2/2) dt + sigma sqrt(dt) x_j), theta = (mu, sigma).
+ *  EXACT_OU:   y_j = Y e^{-lam dt} + Ybar (1 - e^{-lam dt}) + sigma sqrt((1-e^{-2 lam dt})/(2 lam)) x_j
+ *              (Eq. 6.6), theta = (Ybar, lam, sigma); series form when lam*dt < 1e-6. */
+typedef enum { SL7_COLLOC_ANN = 0, SL7_COLLOC_EXACT_GBM = 1, SL7_COLLOC_EXACT_OU = 2 } sl7_colloc;
+
+/* Path-wise reference evaluated on the SAME normals, for the strong error E|Y_T - Y(T)|
+ * (PAPER.md:81, :16, :110).  GBM: Y(T) = Y0 exp((mu - s^2/2) T + s sqrt(dt) sum_i X_i),
+ * ref_theta = (mu, s).  OU: the exact Eq. 6.6 transition per step, ref_theta = (Ybar, lam, s). */
+typedef enum { SL7_REF_NONE = 0, SL7_REF_GBM = 1, SL7_REF_OU = 2 } sl7_ref;
+
+typedef struct {
+  sl7_prec prec;            /* ANN arithmetic (ignored by the exact modes) */
+  sl7_colloc colloc;        /* source of y_j */
+  uint64_t path_offset;     /* global index of this call's first path (Philox counter, sharding) */
+  void* stream;             /* cudaStream_t of the caller (e.g. torch.cuda.current_stream()) */
+  double hist_lo, hist_hi;  /* histogram range; n_bins equal bins [lo + k w, lo + (k+1) w) */
+  double shift;             /* shift for the power sums S_k = sum (Y_T - shift)^k */
+  int32_t n_bins;           /* 0 = no histogram; else 1..16384 (shared-memory histogram) */
+  int32_t accumulate;       /* 0: zero d_stats first; 1: add into it (chunked / resumed runs) */
+  sl7_ref ref;              /* strong-error reference (SL7_REF_NONE: E1 = E2 = 0) */
+  double ref_theta[3];
+} sl7_run_opts;
+
+/* Summary computed on the host from a (possibly all-reduced) stats vector. */
+typedef struct {
+  uint64_t n, n_nonfinite;
+  double mean, var;         /* population variance (divisor n) */
+  double skew, exkurt;
+  double strong_err;        /* E1 / n = mean |Y_T - Y(T)| (0 without a reference) */
+  double rms_err;           /* sqrt(E2 / n) */
+  const double* q_levels;   /* in: n_q probability levels in (0,1) */
+  double* q_values;         /* out: n_q quantiles from the histogram CDF; NaN if the level falls
+                               in the under/overflow bin or no histogram was kept */
+  int32_t n_q;
+} sl7_summary;
+
+/* Create a context on `device`.
+ * m           : collocation nodes, 1..SL7_MAX_M (m=5 in PAPER.md:83).
+ * layer_dims  : [d_in, h_1..h_L, m] of the MLP (4 hidden x 50), or NULL with
+ *               n_dims = 0 for a context that only runs the exact-collocation modes.
+ *               d_in = 2 + n_theta (input order (Y, dt, theta...)), 1 <= L <= SL7_MAX_HIDDEN,
+ *               h_l <= SL7_MAX_WIDTH, last entry == m.
+ * act         : hidden activation.
+ * Host setup done here (once): Gauss-Hermite nodes (own Golub-Welsch QL in double), barycentric
+ * weights, fp32 hi/lo node split.  Errors: SL7_EINVAL (m, layer_dims), SL7_ECUDA (device). */
+sl7_status sl7_create(int32_t m, const int32_t* layer_dims, int32_t n_dims, sl7_act act,
+                      int32_t device, sl7_ctx* out);
+
+/* Load the trained network (Algorithm I step 1 output) from a blob; copied, so the
+ * caller may free it on return.  Little-endian "SL7W" container:
+ *   char magic[4] = "SL7W"; u32 version = 1; u32 n_dims; u32 dims[n_dims]; u32 act; u32 flags
+ *   (bit0 has_norm); then per layer l: f32 W[out][in] (row-major), f32 b[out];
+ *   if has_norm: f32 in_shift[d_in], in_scale[d_in], out_shift[m], out_scale[m]
+ *   (network sees (f - in_shift)/in_scale; prediction is out * out_scale + out_shift).
+ * The size must match exactly.  dims/act must equal the context's.  Errors: SL7_EFORMAT. */
+sl7_status sl7_load_weights(sl7_ctx ctx, const void* blob, size_t nbytes);
+
+/* Run Algorithm I steps 2-8 for paths [opts->path_offset, opts->path_offset + n_paths).
+ * Y0        : initial value (rounded to fp32; FULL row 0).
+ * dt        : large step, > 0; t_i = i dt, T = n_steps dt.
+ * n_steps   : >= 1.   theta/n_theta : model parameters (see sl7_colloc; ANN: n_theta = d_in-2).
+ * n_paths   : >= 1; path_offset + n_paths must not overflow 2^64.
+ * seed      : Philox key.  Step i of path p uses normal Z_{4b + (i & 3)}, b = i >> 2, of
+ *             Philox4x32-10(key = (seed_lo, seed_hi), counter = (b, 0, p_lo, p_hi)).
+ * d_out     : device fp32 buffer of sl7_out_elems(n_steps, n_paths, out_mode) elements, or NULL
+ *             in STATS mode.
+ * d_stats   : device fp64 buffer of sl7_stats_elems(opts->n_bins) elements, or NULL (FULL /
+ *             TERMINAL without statistics).  Layout: [n, n_nonfinite, S1, S2, S3, S4, E1, E2,
+ *             hist_under, hist[0..n_bins-1], hist_over]; sums over finite Y_T only.
+ * Asynchronous on opts->stream.  Errors: SL7_EINVAL, SL7_ESTATE, SL7_EUNSUPPORTED, SL7_ECUDA. */
+sl7_status sl7_simulate(sl7_ctx ctx, double Y0, double dt, int32_t n_steps, const double* theta,
+                        int32_t n_theta, uint64_t n_paths, uint64_t seed, sl7_out out_mode,
+                        const sl7_run_opts* opts, float* d_out, double* d_stats);
+
+/* Same as sl7_simulate but with HOST buffers (end-to-end use): the library stages through
+ * context-owned device scratch, copies results back on opts->stream and synchronises it before
+ * returning.  h_out/h_stats as d_out/d_stats (h_stats is always overwritten unless
+ * opts->accumulate, in which case it is added into).  *h2d_bytes / *d2h_bytes (may be NULL)
+ * receive the bytes moved across PCIe by this call. */
+sl7_status sl7_simulate_host(sl7_ctx ctx, double Y0, double dt, int32_t n_steps, const double* theta,
+                             int32_t n_theta, uint64_t n_paths, uint64_t seed, sl7_out out_mode,
+                             const sl7_run_opts* opts, float* h_out, double* h_stats,
+                             uint64_t* h2d_bytes, uint64_t* d2h_bytes);
+
+/* Moments, strong error and quantiles from a HOST copy of a stats vector (which the caller may
+ * have all-reduced across ranks first).  opts supplies shift, hist_lo, hist_hi, n_bins.
+ * Returns SL7_ENONFINITE (after filling *out) if n_nonfinite > 0; SL7_EINVAL if n == 0. */
+sl7_status sl7_stats(const double* h_stats, const sl7_run_opts* opts, sl7_summary* out);
+
+/* Raw Philox4x32-10 outputs of the path generator's RNG (step a1), for verification:
+ * d_out[k * n_paths + q] = r_k of path (path_offset + q) at block `block`, k = 0..3. */
+sl7_status sl7_philox_u32(uint64_t seed, uint64_t path_offset, uint64_t n_paths, uint32_t block,
+                          uint32_t* d_out, void* stream);
+
+/* The normals the path generator consumes: d_out[i * n_paths + q] = X_hat of path
+ * (path_offset + q) at step i, i = 0..n_steps-1, computed by the same device code as the step
+ * kernels. */
+sl7_status sl7_normals(uint64_t seed, uint64_t path_offset, uint64_t n_paths, int32_t n_steps,
+                       float* d_out, void* stream);
+
+/* Host setup introspection (no device needed): the context-independent grid of m nodes in
+ * double (x[m], ascending) and barycentric weights w[m] = 1 / prod_{k != j}(x_j - x_k). */
+sl7_status sl7_gh_grid(int32_t m, double* x, double* w);
+
+size_t sl7_out_elems(int32_t n_steps, uint64_t n_paths, sl7_out mode); /* (n+1)N_P | N_P | 0 */
+size_t sl7_stats_elems(int32_t n_bins);                                /* 8 + n_bins + 2 */
+const char* sl7_last_error(sl7_ctx ctx);   /* never NULL; ctx may be NULL (thread-global msg) */
+const char* sl7_status_str(sl7_status s);
+int32_t sl7_abi_version(void);
+void sl7_destroy(sl7_ctx ctx);              /* NULL is a no-op */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SL7_H */

@@ -326,16 +326,39 @@ def mlp_forward(net: Mlp, F, quant: str | None = None) -> np.ndarray:
     return h
 
 
-def ann_collocation(net: Mlp, Y, dt, theta, quant=None) -> np.ndarray:
-    """y_hat_j(t_{i+1}) | Y_i = H_hat_j(Y_i, dt, theta) (Eq. 6.4); input order (Y, dt, theta...)
-    (reading R-10).  No sorting of the predicted points (reading R-6)."""
+def mlp_abs_scale(net: Mlp, F, quant: str | None = None) -> np.ndarray:
+    """Forward-error scale of each output: A_j = |out_shift_j| + |out_scale_j| (|b_j| + sum_k |W_jk h_k|)
+    with h the last hidden layer (the standard bound for a rounded dot product).  Used only to
+    scale parity tolerances, not part of the method."""
+    F = np.asarray(F, dtype=np.float64)
+    rnd = {None: (lambda a: a), "bf16": round_bf16, "tf32": round_tf32}[quant]
+    h = F
+    if net.norm is not None:
+        h = (h - net.norm[0]) / net.norm[1]
+    L = len(net.W) - 1
+    for l in range(L):
+        z = h @ net.W[l].T + net.b[l] if l == 0 else rnd(h) @ rnd(net.W[l]).T + net.b[l]
+        h = activation(z, net.act)
+    A = np.abs(rnd(h)) @ np.abs(rnd(net.W[L])).T + np.abs(net.b[L])
+    if net.norm is not None:
+        A = A * np.abs(net.norm[3]) + np.abs(net.norm[2])
+    return A
+
+
+def ann_features(Y, dt, theta) -> np.ndarray:
     Y = np.asarray(Y, dtype=np.float64)
     F = np.empty(Y.shape + (2 + len(theta),))
     F[..., 0] = Y
     F[..., 1] = dt
     for c, t in enumerate(theta):
         F[..., 2 + c] = t
-    return mlp_forward(net, F, quant)
+    return F
+
+
+def ann_collocation(net: Mlp, Y, dt, theta, quant=None) -> np.ndarray:
+    """y_hat_j(t_{i+1}) | Y_i = H_hat_j(Y_i, dt, theta) (Eq. 6.4); input order (Y, dt, theta...)
+    (reading R-10).  No sorting of the predicted points (reading R-6)."""
+    return mlp_forward(net, ann_features(Y, dt, theta), quant)
 
 
 # ----------------------------------------------------------------------------------------------
@@ -368,6 +391,22 @@ class Spec:
             ybar, lam, sigma = self.theta
             return ou_collocation(Y, self.dt, ybar, lam, sigma, self.x)
         raise ValueError(self.colloc)
+
+
+def step_error_scale(spec: Spec, Y, Z) -> np.ndarray:
+    """kappa = sum_j |l_j(Z)| A_j(Y): forward-error scale of one step; A_j = |y_j|
+    in the exact modes, mlp_abs_scale in ANN mode.  kappa >= |Y_{i+1}|.  Tolerance helper only."""
+    if spec.colloc == "ann":
+        A = mlp_abs_scale(spec.net, ann_features(Y, spec.dt, spec.theta), spec.quant)
+    elif spec.colloc == "ou":
+        # y_j = Y e + Ybar (1 - e) + std x_j: the scale of each term, not of their (cancelling) sum
+        ybar, lam, sigma = spec.theta
+        e = np.exp(-lam * spec.dt)
+        _, std = ou_conditional_moments(Y, spec.dt, ybar, lam, sigma)
+        A = (np.abs(np.asarray(Y) * e) + abs(ybar * (1 - e)))[..., None] + np.abs(std * spec.x)
+    else:
+        A = np.abs(spec.points(Y))
+    return np.sum(np.abs(lagrange_basis(Z, spec.x)) * A, axis=-1)
 
 
 def step(spec: Spec, Y, Z) -> np.ndarray:

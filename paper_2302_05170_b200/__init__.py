@@ -1,0 +1,220 @@
+"""Python binding of libsl7.so, the B200-native Seven-League online path generator.
+
+Argument marshalling only (ctypes): every step of the path runs inside the library's CUDA kernels.
+Names follow include/sl7.h.  PyTorch provides device memory and streams; there is NO CPU fallback --
+if the library or a CUDA device is missing, calls raise.
+
+    import paper_2302_05170_b200 as sl7
+    ctx = sl7.Context(m=7, layer_dims=[2, 50, 50, 50, 7], act=sl7.ACT_TANH)
+    ctx.load_weights(blob)
+    out, stats = ctx.simulate(y0=1.0, dt=1/64, n_steps=64, theta=(), n_paths=10**7, seed=1,
+                              out_mode=sl7.OUT_STATS, prec=sl7.PREC_FP32, n_bins=4096, ...)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libsl7.so")
+
+OK, EINVAL, ESTATE, EFORMAT, ENOMEM, ECUDA, ENONFINITE, EUNSUPPORTED = range(8)
+ACT_TANH, ACT_SOFTPLUS = 0, 1
+OUT_FULL, OUT_TERMINAL, OUT_STATS = 0, 1, 2
+PREC_FP32, PREC_TF32, PREC_BF16, PREC_SPLIT = 0, 1, 2, 3
+COLLOC_ANN, COLLOC_EXACT_GBM, COLLOC_EXACT_OU = 0, 1, 2
+REF_NONE, REF_GBM, REF_OU = 0, 1, 2
+STATS_HEAD = 8
+MAX_M = 16
+
+
+class sl7_run_opts(ctypes.Structure):
+    _fields_ = [("prec", ctypes.c_int), ("colloc", ctypes.c_int), ("path_offset", ctypes.c_uint64),
+                ("stream", ctypes.c_void_p), ("hist_lo", ctypes.c_double), ("hist_hi", ctypes.c_double),
+                ("shift", ctypes.c_double), ("n_bins", ctypes.c_int32), ("accumulate", ctypes.c_int32),
+                ("ref", ctypes.c_int), ("ref_theta", ctypes.c_double * 3)]
+
+
+class sl7_summary(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_uint64), ("n_nonfinite", ctypes.c_uint64), ("mean", ctypes.c_double),
+                ("var", ctypes.c_double), ("skew", ctypes.c_double), ("exkurt", ctypes.c_double),
+                ("strong_err", ctypes.c_double), ("rms_err", ctypes.c_double),
+                ("q_levels", ctypes.POINTER(ctypes.c_double)), ("q_values", ctypes.POINTER(ctypes.c_double)),
+                ("n_q", ctypes.c_int32)]
+
+
+class Sl7Error(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__("%s: %s" % (STATUS_NAMES.get(status, status), msg))
+        self.status = status
+
+
+STATUS_NAMES = {0: "SL7_OK", 1: "SL7_EINVAL", 2: "SL7_ESTATE", 3: "SL7_EFORMAT", 4: "SL7_ENOMEM",
+                5: "SL7_ECUDA", 6: "SL7_ENONFINITE", 7: "SL7_EUNSUPPORTED"}
+
+EXPORTS = ["sl7_create", "sl7_load_weights", "sl7_simulate", "sl7_simulate_host", "sl7_stats",
+           "sl7_philox_u32", "sl7_normals", "sl7_gh_grid", "sl7_out_elems", "sl7_stats_elems",
+           "sl7_last_error", "sl7_status_str", "sl7_abi_version", "sl7_destroy"]
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libsl7.so (raises if it has not been built: there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError("libsl7.so not built (run python -m paper_2302_05170_b200.build): %s" % path)
+    L = ctypes.CDLL(path)
+    c = ctypes
+    u64, i32, vp, dp, fp = c.c_uint64, c.c_int32, c.c_void_p, c.POINTER(c.c_double), c.c_void_p
+    L.sl7_create.argtypes = [i32, c.POINTER(i32), i32, c.c_int, i32, c.POINTER(vp)]
+    L.sl7_load_weights.argtypes = [vp, c.c_char_p, c.c_size_t]
+    L.sl7_simulate.argtypes = [vp, c.c_double, c.c_double, i32, dp, i32, u64, u64, c.c_int,
+                               c.POINTER(sl7_run_opts), fp, fp]
+    L.sl7_simulate_host.argtypes = [vp, c.c_double, c.c_double, i32, dp, i32, u64, u64, c.c_int,
+                                    c.POINTER(sl7_run_opts), fp, fp, c.POINTER(u64), c.POINTER(u64)]
+    L.sl7_stats.argtypes = [dp, c.POINTER(sl7_run_opts), c.POINTER(sl7_summary)]
+    L.sl7_philox_u32.argtypes = [u64, u64, u64, c.c_uint32, vp, vp]
+    L.sl7_normals.argtypes = [u64, u64, u64, i32, vp, vp]
+    L.sl7_gh_grid.argtypes = [i32, dp, dp]
+    L.sl7_out_elems.argtypes = [i32, u64, c.c_int]
+    L.sl7_out_elems.restype = c.c_size_t
+    L.sl7_stats_elems.argtypes = [i32]
+    L.sl7_stats_elems.restype = c.c_size_t
+    L.sl7_last_error.argtypes = [vp]
+    L.sl7_last_error.restype = c.c_char_p
+    L.sl7_status_str.argtypes = [c.c_int]
+    L.sl7_status_str.restype = c.c_char_p
+    L.sl7_abi_version.restype = i32
+    L.sl7_destroy.argtypes = [vp]
+    L.sl7_destroy.restype = None
+    for name in ("sl7_create", "sl7_load_weights", "sl7_simulate", "sl7_simulate_host", "sl7_stats",
+                 "sl7_philox_u32", "sl7_normals", "sl7_gh_grid"):
+        getattr(L, name).restype = c.c_int
+    _lib = L
+    return L
+
+
+def _check(st, ctx=None):
+    if st != OK:
+        msg = _lib.sl7_last_error(ctx).decode()
+        raise Sl7Error(st, msg)
+
+
+def _dptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream_ptr(stream):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def make_opts(prec=PREC_FP32, colloc=COLLOC_ANN, path_offset=0, stream=None, hist_lo=0.0, hist_hi=0.0,
+              shift=0.0, n_bins=0, accumulate=0, ref=REF_NONE, ref_theta=(0.0, 0.0, 0.0), raw_stream=None):
+    o = sl7_run_opts()
+    o.prec, o.colloc, o.path_offset = prec, colloc, int(path_offset)
+    o.stream = raw_stream if raw_stream is not None else (_stream_ptr(stream) if stream is not False else None)
+    o.hist_lo, o.hist_hi, o.shift, o.n_bins, o.accumulate = hist_lo, hist_hi, shift, int(n_bins), int(accumulate)
+    o.ref = ref
+    for k in range(3):
+        o.ref_theta[k] = float(ref_theta[k]) if k < len(ref_theta) else 0.0
+    return o
+
+
+def gh_grid(m: int):
+    """Host-setup nodes and barycentric weights (double) as computed inside the library."""
+    L = load_library()
+    x = (ctypes.c_double * m)()
+    w = (ctypes.c_double * m)()
+    _check(L.sl7_gh_grid(m, x, w))
+    return list(x), list(w)
+
+
+def out_elems(n_steps, n_paths, mode):
+    return load_library().sl7_out_elems(n_steps, n_paths, mode)
+
+
+def stats_elems(n_bins):
+    return load_library().sl7_stats_elems(n_bins)
+
+
+def stats_summary(h_stats, opts, q_levels=()):
+    """Moments / strong error / histogram quantiles of a host stats vector (list, numpy or tensor)."""
+    L = load_library()
+    import numpy as np
+    v = np.ascontiguousarray(np.asarray(h_stats, dtype=np.float64))
+    s = sl7_summary()
+    lv = (ctypes.c_double * max(1, len(q_levels)))(*q_levels)
+    qv = (ctypes.c_double * max(1, len(q_levels)))()
+    s.q_levels, s.q_values, s.n_q = lv, qv, len(q_levels)
+    st = L.sl7_stats(v.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(opts), ctypes.byref(s))
+    if st not in (OK, ENONFINITE):
+        _check(st)
+    return {"n": s.n, "n_nonfinite": s.n_nonfinite, "mean": s.mean, "var": s.var, "skew": s.skew,
+            "exkurt": s.exkurt, "strong_err": s.strong_err, "rms_err": s.rms_err,
+            "quantiles": [qv[i] for i in range(len(q_levels))], "status": st}
+
+
+def philox_u32(seed, path_offset, n_paths, block, out, stream=None):
+    L = load_library()
+    _check(L.sl7_philox_u32(int(seed), int(path_offset), int(n_paths), int(block), _dptr(out), _stream_ptr(stream)))
+    return out
+
+
+def normals(seed, path_offset, n_paths, n_steps, out, stream=None):
+    L = load_library()
+    _check(L.sl7_normals(int(seed), int(path_offset), int(n_paths), int(n_steps), _dptr(out), _stream_ptr(stream)))
+    return out
+
+
+class Context:
+    """Owns one sl7_ctx (one device)."""
+
+    def __init__(self, m, layer_dims=None, act=ACT_TANH, device=None):
+        import torch
+        L = load_library()
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.m = m
+        dims = list(layer_dims or [])
+        arr = (ctypes.c_int32 * max(1, len(dims)))(*dims)
+        h = ctypes.c_void_p()
+        _check(L.sl7_create(m, arr if dims else None, len(dims), act, self.device, ctypes.byref(h)))
+        self._h = h
+        self.layer_dims = dims
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.sl7_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def load_weights(self, blob: bytes):
+        _check(_lib.sl7_load_weights(self._h, blob, len(blob)), self._h)
+
+    def simulate(self, y0, dt, n_steps, theta, n_paths, seed, out_mode, opts, out=None, stats=None):
+        """sl7_simulate on torch device tensors (float32 out, float64 stats); allocates if None."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        if out is None and out_mode != OUT_STATS:
+            out = torch.empty(out_elems(n_steps, n_paths, out_mode), dtype=torch.float32, device=dev)
+        th = (ctypes.c_double * max(1, len(theta)))(*theta)
+        _check(_lib.sl7_simulate(self._h, float(y0), float(dt), int(n_steps), th, len(theta), int(n_paths),
+                                 int(seed), out_mode, ctypes.byref(opts), _dptr(out), _dptr(stats)), self._h)
+        return out, stats
+
+    def simulate_host(self, y0, dt, n_steps, theta, n_paths, seed, out_mode, opts, h_out=None, h_stats=None):
+        """sl7_simulate_host on host numpy buffers; returns (h_out, h_stats, h2d_bytes, d2h_bytes)."""
+        import numpy as np
+        th = (ctypes.c_double * max(1, len(theta)))(*theta)
+        up, down = ctypes.c_uint64(), ctypes.c_uint64()
+        po = None if h_out is None else h_out.ctypes.data_as(ctypes.c_void_p)
+        ps = None if h_stats is None else h_stats.ctypes.data_as(ctypes.c_void_p)
+        _check(_lib.sl7_simulate_host(self._h, float(y0), float(dt), int(n_steps), th, len(theta), int(n_paths),
+                                      int(seed), out_mode, ctypes.byref(opts), po, ps, ctypes.byref(up),
+                                      ctypes.byref(down)), self._h)
+        return h_out, h_stats, up.value, down.value

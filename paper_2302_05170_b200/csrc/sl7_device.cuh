@@ -1,0 +1,212 @@
+// sl7_device.cuh -- device building blocks of the Seven-League step kernels (sm_100a).
+//
+//   a1  normals:       Philox4x32-10 + Box-Muller keyed by (seed, global path, step block)
+//   a5/a6 g_m:         product form of the normalised barycentric Lagrange formula
+//   a7  statistics:    shifted power sums, strong error, histogram; per-thread -> warp -> CTA -> global
+//   activations:       MUFU-based tanh / softplus with absolute error ~2e-7
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sl7_internal.h"
+
+namespace sl7 {
+
+// ------------------------------------------------------------------------------------------------
+// a1.  Philox4x32-10 (Salmon et al. SC'11): 10 rounds of two 32x32->64 multiplies (IMAD.HI + IMAD),
+// key schedule (W0, W1).  counter = (block, 0, path_lo, path_hi), key = (seed_lo, seed_hi):
+// identical to cuRAND curand4() after curand_init(seed, path, 4*block) (checked on the box).
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+  constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) { k.x += W0; k.y += W1; }
+    const uint32_t hi0 = __umulhi(M0, c.x), lo0 = M0 * c.x;
+    const uint32_t hi1 = __umulhi(M1, c.z), lo1 = M1 * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+  }
+  return c;
+}
+
+__device__ __forceinline__ uint4 philox_path_block(uint32_t key0, uint32_t key1, uint64_t path, uint32_t block) {
+  return philox4x32_10(make_uint4(block, 0u, (uint32_t)path, (uint32_t)(path >> 32)), make_uint2(key0, key1));
+}
+
+// u = (2 (r >> 9) + 1) 2^-24: exact in fp32, in [2^-24, 1 - 2^-24], never 0 or 1.
+__device__ __forceinline__ float u32_to_unit(uint32_t r) {
+  return __uint2float_rn(((r >> 9) << 1) | 1u) * 0x1p-24f;
+}
+
+// Box-Muller with accurate libm logf/sincospif (1-2 ulp everywhere, including u -> 1 where
+// MUFU lg2.approx would lose the relative accuracy of ln u).
+__device__ __forceinline__ void box_muller(uint32_t ra, uint32_t rb, float& za, float& zb) {
+  const float ua = u32_to_unit(ra), ub = u32_to_unit(rb);
+  const float rad = sqrtf(-2.0f * logf(ua));
+  float s, c;
+  sincospif(2.0f * ub, &s, &c);
+  za = rad * c;
+  zb = rad * s;
+}
+
+__device__ __forceinline__ void normals4(uint32_t key0, uint32_t key1, uint64_t path, uint32_t block,
+                                         float& z0, float& z1, float& z2, float& z3) {
+  const uint4 r = philox_path_block(key0, key1, path, block);
+  box_muller(r.x, r.y, z0, z1);
+  box_muller(r.z, r.w, z2, z3);
+}
+
+// ------------------------------------------------------------------------------------------------
+// a5/a6.  g_m(Z) = sum_j y_j l_j(Z) / sum_j l_j(Z), l_j(Z) = w_j prod_{k != j}(Z - x_k)
+// (barycentric, PAPER.md:48 / ref [8]).  sum_j l_j == 1 exactly, so the division only removes the
+// rounding of the fp32 weights (no poles, no node-hit branch).  d_k = (Z - xhi_k) - xlo_k keeps the
+// node to ~2^-48 relative.  Prefix/suffix products: 3(M-1) FMUL + 2M FFMA/FADD + 1 rcp.
+// MR = compile-time slot count; m_rt < MR means runtime m with padded slots (w = 0, d = 1).
+// ------------------------------------------------------------------------------------------------
+template <int MR, bool RUNTIME_M = false>
+__device__ __forceinline__ float gm_eval(const RunParams& p, float Z, const float (&y)[MR]) {
+  float d[MR];
+#pragma unroll
+  for (int k = 0; k < MR; ++k) {
+    const float dk = (Z - p.xhi[k]) - p.xlo[k];
+    d[k] = (RUNTIME_M && k >= p.m) ? 1.0f : dk;
+  }
+  float pre[MR];
+  pre[0] = 1.0f;
+#pragma unroll
+  for (int k = 1; k < MR; ++k) pre[k] = pre[k - 1] * d[k - 1];
+  float suf = 1.0f, num = 0.0f, den = 0.0f;
+#pragma unroll
+  for (int j = MR - 1; j >= 0; --j) {
+    const float l = p.w[j] * (pre[j] * suf);
+    num = fmaf(l, y[j], num);
+    den += l;
+    suf *= d[j];
+  }
+  return __fdividef(num, den);
+}
+
+// ------------------------------------------------------------------------------------------------
+// Activations (PAPER.md:85 Softplus; tanh for BASELINE configs 0,1,3).  Two MUFU ops each.
+// tanh(z) = sign(z) (1 - 2 / (e^{2|z|} + 1)),  |z| clamped at 15 (tanh(15) rounds to 1 in fp32).
+// softplus(z) = max(z, 0) + ln 2 * log2(1 + e^{-|z|}).   Absolute error <= ~2.5e-7 for both.
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float lg2_approx(float x) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+__device__ __forceinline__ float act_tanh(float z) {
+  const float a = fminf(fabsf(z), 15.0f);
+  const float e = ex2_approx(a * 2.8853900817779268f);  // e^{2a}
+  const float t = fmaf(-2.0f, rcp_approx(e + 1.0f), 1.0f);
+  return copysignf(t, z);
+}
+
+__device__ __forceinline__ float act_softplus(float z) {
+  const float t = ex2_approx(fabsf(z) * -1.4426950408889634f);  // e^{-|z|}
+  return fmaf(0.69314718055994531f, lg2_approx(1.0f + t), fmaxf(z, 0.0f));
+}
+
+template <int ACT>
+__device__ __forceinline__ float activate(float z) {
+  if constexpr (ACT == SL7_ACT_TANH) return act_tanh(z);
+  else return act_softplus(z);
+}
+
+// ------------------------------------------------------------------------------------------------
+// a7.  Fused statistics of the terminal values.
+// ------------------------------------------------------------------------------------------------
+struct StatAcc {
+  double s1 = 0, s2 = 0, s3 = 0, s4 = 0, e1 = 0, e2 = 0;
+  uint32_t n = 0, nnf = 0;
+};
+
+__device__ __forceinline__ void stat_add(StatAcc& a, const RunParams& p, float y, double ref, uint32_t* hist) {
+  if (isfinite(y)) {
+    const double yd = (double)y;
+    const double d = yd - p.shift, d2 = d * d;
+    a.s1 += d;
+    a.s2 += d2;
+    a.s3 += d2 * d;
+    a.s4 += d2 * d2;
+    a.n += 1;
+    if (p.ref != kRefNone) {
+      const double e = yd - ref;
+      a.e1 += fabs(e);
+      a.e2 += e * e;
+    }
+    if (p.n_bins > 0) {
+      const double t = (yd - p.hist_lo) * p.hist_scale;
+      int bin;
+      if (yd < p.hist_lo) bin = 0;
+      else if (t >= (double)p.n_bins) bin = p.n_bins + 1;
+      else bin = 1 + (int)t;
+      atomicAdd(&hist[bin], 1u);
+    }
+  } else {
+    a.nnf += 1;
+  }
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Call by ALL threads of the CTA (contains __syncthreads).  red: 8 doubles of shared memory.
+__device__ __forceinline__ void stat_flush(const StatAcc& a, const RunParams& p, uint32_t* hist, double* red) {
+  const int tid = threadIdx.x;
+  if (tid < 8) red[tid] = 0.0;
+  __syncthreads();
+  double v[8] = {(double)a.n, (double)a.nnf, a.s1, a.s2, a.s3, a.s4, a.e1, a.e2};
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const double s = warp_sum(v[k]);
+    if ((tid & 31) == 0 && s != 0.0) atomicAdd(&red[k], s);
+  }
+  __syncthreads();
+  if (tid < 8 && red[tid] != 0.0) atomicAdd(&p.stats[tid], red[tid]);
+  if (p.n_bins > 0) {
+    for (int b = tid; b < p.n_bins + 2; b += blockDim.x) {
+      const uint32_t c = hist[b];
+      if (c) atomicAdd(&p.stats[kStatsHead + b], (double)c);
+    }
+  }
+}
+
+__device__ __forceinline__ void hist_init(const RunParams& p, uint32_t* hist) {
+  if (p.has_stats && p.n_bins > 0)
+    for (int b = threadIdx.x; b < p.n_bins + 2; b += blockDim.x) hist[b] = 0u;
+}
+
+// Path-wise exact reference state on the same normals.
+struct RefState {
+  double r;   // GBM: sum of Z; OU: exact state
+};
+
+__device__ __forceinline__ void ref_init(RefState& s, const RunParams& p) {
+  s.r = (p.ref == kRefOu) ? p.y0_d : 0.0;
+}
+__device__ __forceinline__ void ref_step(RefState& s, const RunParams& p, float Z) {
+  if (p.ref == kRefGbm) s.r += (double)Z;
+  else if (p.ref == kRefOu) s.r = fma(p.ref_a, s.r, p.ref_b) + p.ref_s * (double)Z;
+}
+__device__ __forceinline__ double ref_final(const RefState& s, const RunParams& p) {
+  if (p.ref == kRefGbm) return p.y0_d * exp(p.ref_drift_T + p.ref_vol * s.r);
+  return s.r;
+}
+
+}  // namespace sl7

@@ -1,0 +1,634 @@
+// sl7_host.cpp -- host runtime of the C ABI (include/sl7.h): validation, host setup, weight blob
+// parsing and folding, per-run constants, launches, host-buffer staging, statistics summary.
+//
+// Host setup (Algorithm I step 2 prerequisites, done in double, rounded once to fp32):
+//   * Gauss-Hermite nodes (probabilists' reading): eigenvalues of the symmetric
+//     tridiagonal Jacobi matrix (0 diagonal, sqrt(k) off-diagonal) by our own implicit QL
+//     iteration (no LAPACK), polished by Newton on the He_m three-term recurrence, symmetrised.
+//   * barycentric weights w_j = 1 / prod_{k != j}(x_j - x_k) (ref [8]).
+//   * fp32 hi/lo split of the nodes: x = xhi + xlo.
+//   * ANN layer 1 folding: dt and theta are constant per run, so
+//     W1 (f - in_shift)/in_scale + b1 = l1w * Y + l1b with l1w, l1b computed in double here.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "sl7_internal.h"
+
+using namespace sl7;
+
+namespace {
+
+thread_local std::string g_err = "";
+
+}  // namespace
+
+struct sl7_ctx_s {
+  int device = 0;
+  int m = 0;
+  int act = 0;
+  std::vector<int> dims;   // empty: exact-only context
+  double x[kMaxM] = {0}, w[kMaxM] = {0};
+  // network (host copy, as loaded)
+  bool has_net = false;
+  std::vector<std::vector<float>> W, b;
+  bool has_norm = false;
+  std::vector<float> in_shift, in_scale, out_shift, out_scale;
+  // device images
+  int width = 0;           // hidden width used by the FP32 kernel (50 or 64 padded)
+  float* d_wf32 = nullptr;
+  int num_sms = 148;
+  // host-mode staging
+  float* d_out_scratch = nullptr;
+  size_t out_cap = 0;
+  double* d_stats_scratch = nullptr;
+  size_t stats_cap = 0;
+  std::string err;
+};
+
+namespace {
+
+sl7_status fail(sl7_ctx ctx, sl7_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  if (ctx) ctx->err = buf;
+  return s;
+}
+
+sl7_status cuda_fail(sl7_ctx ctx, cudaError_t e, const char* what) {
+  return fail(ctx, SL7_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = false;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) { prev = -1; return; }
+    ok = (prev == dev) || (cudaSetDevice(dev) == cudaSuccess);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// ---- Golub-Welsch: eigenvalues of symmetric tridiagonal (d, e) by implicit QL with shifts ----
+void tridiag_ql_eigenvalues(std::vector<double>& d, std::vector<double> e) {
+  const int n = (int)d.size();
+  // e[i] couples d[i] and d[i+1]; e[n-1] = 0
+  e.push_back(0.0);
+  for (int l = 0; l < n; ++l) {
+    for (int iter = 0; iter < 200; ++iter) {
+      int mm;
+      for (mm = l; mm < n - 1; ++mm) {
+        const double dd = std::fabs(d[mm]) + std::fabs(d[mm + 1]);
+        if (std::fabs(e[mm]) <= 1e-17 * dd) break;
+      }
+      if (mm == l) break;
+      double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+      double r = std::hypot(g, 1.0);
+      g = d[mm] - d[l] + e[l] / (g + (g >= 0 ? std::fabs(r) : -std::fabs(r)));
+      double s = 1.0, c = 1.0, p = 0.0;
+      int i;
+      for (i = mm - 1; i >= l; --i) {
+        double f = s * e[i];
+        const double bb = c * e[i];
+        r = std::hypot(f, g);
+        e[i + 1] = r;
+        if (r == 0.0) {
+          d[i + 1] -= p;
+          e[mm] = 0.0;
+          break;
+        }
+        s = f / r;
+        c = g / r;
+        g = d[i + 1] - p;
+        r = (d[i] - g) * s + 2.0 * c * bb;
+        p = s * r;
+        d[i + 1] = g + p;
+        g = c * r - bb;
+      }
+      if (r == 0.0 && i >= l) continue;
+      d[l] -= p;
+      e[l] = g;
+      e[mm] = 0.0;
+    }
+  }
+}
+
+// He_m(x) and He_{m-1}(x) by the recurrence He_{k+1} = x He_k - k He_{k-1}.
+void hermite_pair(int m, double x, double& hm, double& hm1) {
+  double a = 1.0, b = x;  // He_0, He_1
+  if (m == 0) { hm = 1.0; hm1 = 0.0; return; }
+  for (int k = 1; k < m; ++k) {
+    const double c = x * b - k * a;
+    a = b;
+    b = c;
+  }
+  hm = b;
+  hm1 = a;
+}
+
+void gh_grid(int m, double* x, double* w) {
+  std::vector<double> d(m, 0.0), e;
+  for (int k = 1; k < m; ++k) e.push_back(std::sqrt((double)k));
+  tridiag_ql_eigenvalues(d, e);
+  std::sort(d.begin(), d.end());
+  for (int j = 0; j < m; ++j) {
+    double xj = d[j];
+    for (int it = 0; it < 3; ++it) {  // Newton polish: He_m' = m He_{m-1}
+      double hm, hm1;
+      hermite_pair(m, xj, hm, hm1);
+      if (hm1 == 0.0) break;
+      xj -= hm / (m * hm1);
+    }
+    d[j] = xj;
+  }
+  for (int j = 0; j < m; ++j) x[j] = 0.5 * (d[j] - d[m - 1 - j]);  // exact symmetry
+  for (int j = 0; j < m; ++j) {
+    double p = 1.0;
+    for (int k = 0; k < m; ++k)
+      if (k != j) p *= (x[j] - x[k]);
+    w[j] = 1.0 / p;
+  }
+}
+
+bool finite_all(const double* v, int n) {
+  for (int i = 0; i < n; ++i)
+    if (!std::isfinite(v[i])) return false;
+  return true;
+}
+
+uint32_t rd_u32(const unsigned char* p) {
+  uint32_t v;
+  std::memcpy(&v, p, 4);
+  return v;
+}
+
+// OU conditional std factor sqrt((1 - e^{-2 lam dt}) / (2 lam)), series for lam dt < 1e-6 (Eq. 6.6)
+double ou_std(double lam, double sigma, double dt) {
+  const double a = lam * dt;
+  const double vf = (a < 1e-6) ? dt * (1.0 - a + (2.0 / 3.0) * a * a) : -std::expm1(-2.0 * a) / (2.0 * lam);
+  return sigma * std::sqrt(vf);
+}
+
+sl7_status build_f32_image(sl7_ctx c) {
+  const int L = (int)c->dims.size() - 2;   // hidden layers
+  const int M = c->m;
+  bool all50 = true;
+  for (int l = 1; l <= L; ++l) all50 = all50 && c->dims[l] == 50;
+  const int H = (all50 && (M == 5 || M == 7)) ? 50 : 64;
+  const int HS = (H == 50) ? 52 : 64;
+  const int MR = (H == 50) ? M : kMaxM;
+  c->width = H;
+  std::vector<float> img(f32_weight_floats(H, HS, L, MR), 0.0f);
+  size_t off = 0;
+  for (int l = 1; l < L; ++l) {  // blob layer l maps hidden l -> hidden l+1
+    const int fi = c->dims[l], fo = c->dims[l + 1];
+    for (int j = 0; j < fo; ++j)
+      for (int k = 0; k < fi; ++k) img[off + (size_t)j * HS + k] = c->W[l][(size_t)j * fi + k];
+    off += (size_t)H * HS;
+    for (int j = 0; j < fo; ++j) img[off + j] = c->b[l][j];
+    off += (size_t)((H + 3) & ~3);
+  }
+  {
+    const int fi = c->dims[L];
+    for (int j = 0; j < M; ++j)
+      for (int k = 0; k < fi; ++k) img[off + (size_t)j * HS + k] = c->W[L][(size_t)j * fi + k];
+    off += (size_t)MR * HS;
+    for (int j = 0; j < M; ++j) img[off + j] = c->b[L][j];
+  }
+  if (c->d_wf32) cudaFree(c->d_wf32);
+  c->d_wf32 = nullptr;
+  cudaError_t e = cudaMalloc(&c->d_wf32, img.size() * sizeof(float));
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaMalloc(weights)");
+  e = cudaMemcpy(c->d_wf32, img.data(), img.size() * sizeof(float), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemcpy(weights)");
+  return SL7_OK;
+}
+
+// Fill RunParams for one call; all validation happens here (synchronously, before any launch).
+sl7_status prepare(sl7_ctx c, double Y0, double dt, int32_t n_steps, const double* theta, int32_t n_theta,
+                   uint64_t n_paths, uint64_t seed, sl7_out out_mode, const sl7_run_opts* o, RunParams& p,
+                   bool have_out, bool have_stats) {
+  if (!c) return fail(c, SL7_EINVAL, "ctx is NULL");
+  if (!o) return fail(c, SL7_EINVAL, "opts is NULL");
+  if (!(dt > 0.0) || !std::isfinite(dt)) return fail(c, SL7_EINVAL, "dt must be finite and > 0");
+  if (n_steps < 1) return fail(c, SL7_EINVAL, "n_steps must be >= 1");
+  if (n_paths < 1) return fail(c, SL7_EINVAL, "n_paths must be >= 1");
+  if (o->path_offset + (n_paths - 1) < o->path_offset) return fail(c, SL7_EINVAL, "path_offset + n_paths - 1 overflows 2^64");
+  if (!std::isfinite(Y0)) return fail(c, SL7_EINVAL, "Y0 must be finite");
+  if (n_theta < 0 || n_theta > SL7_MAX_THETA || (n_theta > 0 && !theta)) return fail(c, SL7_EINVAL, "theta/n_theta");
+  if (n_theta > 0 && !finite_all(theta, n_theta)) return fail(c, SL7_EINVAL, "theta must be finite");
+  if (out_mode != SL7_OUT_FULL && out_mode != SL7_OUT_TERMINAL && out_mode != SL7_OUT_STATS)
+    return fail(c, SL7_EINVAL, "out_mode");
+  if (out_mode != SL7_OUT_STATS && !have_out) return fail(c, SL7_EINVAL, "d_out is NULL for a FULL/TERMINAL run");
+  if (out_mode == SL7_OUT_STATS && !have_stats) return fail(c, SL7_EINVAL, "d_stats is NULL for a STATS run");
+  if (have_stats) {
+    if (o->n_bins < 0 || o->n_bins > 16384) return fail(c, SL7_EINVAL, "n_bins must be in 0..16384");
+    if (o->n_bins > 0 && !(o->hist_hi > o->hist_lo && std::isfinite(o->hist_lo) && std::isfinite(o->hist_hi)))
+      return fail(c, SL7_EINVAL, "hist_lo/hist_hi");
+    if (!std::isfinite(o->shift)) return fail(c, SL7_EINVAL, "shift");
+  }
+  if (o->ref != SL7_REF_NONE && o->ref != SL7_REF_GBM && o->ref != SL7_REF_OU) return fail(c, SL7_EINVAL, "ref");
+  if (o->ref != SL7_REF_NONE && !finite_all(o->ref_theta, 3)) return fail(c, SL7_EINVAL, "ref_theta");
+  if (o->ref == SL7_REF_OU && (o->ref_theta[1] < 0 || o->ref_theta[2] < 0)) return fail(c, SL7_EINVAL, "ref_theta (lam, sigma >= 0)");
+
+  std::memset(&p, 0, sizeof p);
+  p.m = c->m;
+  p.n_steps = n_steps;
+  p.out_mode = (int)out_mode;
+  p.n_paths = n_paths;
+  p.path_offset = o->path_offset;
+  p.key0 = (uint32_t)seed;
+  p.key1 = (uint32_t)(seed >> 32);
+  p.y0 = (float)Y0;
+  p.y0_d = (double)(float)Y0;
+  for (int j = 0; j < kMaxM; ++j) {
+    if (j < c->m) {
+      const float hi = (float)c->x[j];
+      p.xhi[j] = hi;
+      p.xlo[j] = (float)(c->x[j] - (double)hi);
+      p.w[j] = (float)c->w[j];
+    } else {
+      p.xhi[j] = p.xlo[j] = p.w[j] = 0.0f;   // padded slot: w = 0 (no contribution)
+    }
+  }
+  switch (o->colloc) {
+    case SL7_COLLOC_EXACT_GBM: {
+      if (n_theta != 2) return fail(c, SL7_EINVAL, "EXACT_GBM needs theta = (mu, sigma)");
+      const double mu = theta[0], s = theta[1];
+      if (s < 0) return fail(c, SL7_EINVAL, "theta: sigma >= 0");
+      for (int j = 0; j < c->m; ++j) p.c[j] = (float)std::exp((mu - 0.5 * s * s) * dt + s * std::sqrt(dt) * c->x[j]);
+      p.colloc = kExactGbm;
+      break;
+    }
+    case SL7_COLLOC_EXACT_OU: {
+      if (n_theta != 3) return fail(c, SL7_EINVAL, "EXACT_OU needs theta = (Ybar, lam, sigma)");
+      const double ybar = theta[0], lam = theta[1], s = theta[2];
+      if (lam < 0 || s < 0) return fail(c, SL7_EINVAL, "theta: lam >= 0 and sigma >= 0");
+      const double e = std::exp(-lam * dt), sd = ou_std(lam, s, dt);
+      p.ou_a = (float)e;
+      p.ou_b = (float)(ybar * (1.0 - e));
+      for (int j = 0; j < c->m; ++j) p.c[j] = (float)(sd * c->x[j]);
+      p.colloc = kExactOu;
+      break;
+    }
+    case SL7_COLLOC_ANN: {
+      if (c->dims.empty()) return fail(c, SL7_ESTATE, "ANN mode on a context created without layer_dims");
+      if (!c->has_net) return fail(c, SL7_ESTATE, "ANN mode before sl7_load_weights");
+      const int d_in = c->dims[0];
+      if (n_theta != d_in - 2) return fail(c, SL7_EINVAL, "n_theta must equal layer_dims[0] - 2");
+      if (o->prec != SL7_PREC_FP32)
+        return fail(c, SL7_EUNSUPPORTED, "precision mode %d not available in this build", (int)o->prec);
+      const int H1 = c->dims[1];
+      // features f = (Y, dt, theta...); normalised f' = (f - in_shift) / in_scale
+      std::vector<double> f(d_in), sh(d_in, 0.0), sc(d_in, 1.0);
+      f[0] = 0.0;
+      f[1] = dt;
+      for (int t = 0; t < n_theta; ++t) f[2 + t] = theta[t];
+      if (c->has_norm)
+        for (int k = 0; k < d_in; ++k) { sh[k] = c->in_shift[k]; sc[k] = c->in_scale[k]; }
+      for (int k = 0; k < kMaxW; ++k) { p.l1w[k] = 0.0f; p.l1b[k] = 0.0f; }
+      for (int k = 0; k < H1; ++k) {
+        const float* Wr = &c->W[0][(size_t)k * d_in];
+        double bias = c->b[0][k] - (double)Wr[0] * sh[0] / sc[0];
+        for (int q = 1; q < d_in; ++q) bias += (double)Wr[q] * (f[q] - sh[q]) / sc[q];
+        p.l1w[k] = (float)((double)Wr[0] / sc[0]);
+        p.l1b[k] = (float)bias;
+      }
+      for (int j = 0; j < kMaxM; ++j) {
+        p.out_scale[j] = (j < c->m && c->has_norm) ? c->out_scale[j] : (j < c->m ? 1.0f : 0.0f);
+        p.out_shift[j] = (j < c->m && c->has_norm) ? c->out_shift[j] : 0.0f;
+      }
+      p.act = c->act;
+      p.n_hidden = (int)c->dims.size() - 2;
+      p.width = c->width;
+      p.wdev = c->d_wf32;
+      p.colloc = kAnn;
+      break;
+    }
+    default:
+      return fail(c, SL7_EINVAL, "colloc");
+  }
+  p.ref = (int)o->ref;
+  if (o->ref == SL7_REF_GBM) {
+    const double mu = o->ref_theta[0], s = o->ref_theta[1];
+    p.ref_drift_T = (mu - 0.5 * s * s) * dt * n_steps;
+    p.ref_vol = s * std::sqrt(dt);
+  } else if (o->ref == SL7_REF_OU) {
+    const double ybar = o->ref_theta[0], lam = o->ref_theta[1], s = o->ref_theta[2];
+    const double e = std::exp(-lam * dt);
+    p.ref_a = e;
+    p.ref_b = ybar * (1.0 - e);
+    p.ref_s = ou_std(lam, s, dt);
+  }
+  p.has_stats = have_stats ? 1 : 0;
+  p.n_bins = have_stats ? o->n_bins : 0;
+  p.shift = o->shift;
+  p.hist_lo = o->hist_lo;
+  p.hist_scale = (p.n_bins > 0) ? (double)p.n_bins / (o->hist_hi - o->hist_lo) : 0.0;
+  return SL7_OK;
+}
+
+sl7_status run(sl7_ctx c, RunParams& p, const sl7_run_opts* o, float* d_out, double* d_stats) {
+  p.out = d_out;
+  p.stats = d_stats;
+  if (d_stats && !o->accumulate) {
+    const int e = launch_zero_stats(d_stats, sl7_stats_elems(o->n_bins), o->stream);
+    if (e) return cuda_fail(c, (cudaError_t)e, "zero stats");
+  }
+  const int e = launch_step_kernel(p, (int)o->prec, o->stream, c->num_sms);
+  if (e) return cuda_fail(c, (cudaError_t)e, "step kernel launch");
+  return SL7_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t sl7_abi_version(void) { return SL7_ABI_VERSION; }
+
+const char* sl7_status_str(sl7_status s) {
+  switch (s) {
+    case SL7_OK: return "SL7_OK";
+    case SL7_EINVAL: return "SL7_EINVAL";
+    case SL7_ESTATE: return "SL7_ESTATE";
+    case SL7_EFORMAT: return "SL7_EFORMAT";
+    case SL7_ENOMEM: return "SL7_ENOMEM";
+    case SL7_ECUDA: return "SL7_ECUDA";
+    case SL7_ENONFINITE: return "SL7_ENONFINITE";
+    case SL7_EUNSUPPORTED: return "SL7_EUNSUPPORTED";
+  }
+  return "SL7_?";
+}
+
+const char* sl7_last_error(sl7_ctx ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+size_t sl7_out_elems(int32_t n_steps, uint64_t n_paths, sl7_out mode) {
+  if (mode == SL7_OUT_FULL) return (size_t)(n_steps + 1) * (size_t)n_paths;
+  if (mode == SL7_OUT_TERMINAL) return (size_t)n_paths;
+  return 0;
+}
+
+size_t sl7_stats_elems(int32_t n_bins) { return (size_t)kStatsHead + (size_t)(n_bins > 0 ? n_bins : 0) + 2; }
+
+sl7_status sl7_gh_grid(int32_t m, double* x, double* w) {
+  if (m < 1 || m > kMaxM) return fail(nullptr, SL7_EINVAL, "m must be in 1..%d", kMaxM);
+  if (!x || !w) return fail(nullptr, SL7_EINVAL, "x/w NULL");
+  gh_grid(m, x, w);
+  return SL7_OK;
+}
+
+sl7_status sl7_create(int32_t m, const int32_t* layer_dims, int32_t n_dims, sl7_act act, int32_t device, sl7_ctx* out) {
+  if (!out) return fail(nullptr, SL7_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (m < 1 || m > kMaxM) return fail(nullptr, SL7_EINVAL, "m must be in 1..%d", kMaxM);
+  if (act != SL7_ACT_TANH && act != SL7_ACT_SOFTPLUS) return fail(nullptr, SL7_EINVAL, "act");
+  if (n_dims != 0) {
+    if (!layer_dims) return fail(nullptr, SL7_EINVAL, "layer_dims is NULL");
+    const int L = n_dims - 2;
+    if (L < 1 || L > kMaxHidden) return fail(nullptr, SL7_EINVAL, "layer_dims: 1..%d hidden layers", kMaxHidden);
+    if (layer_dims[n_dims - 1] != m) return fail(nullptr, SL7_EINVAL, "layer_dims: last entry must equal m");
+    if (layer_dims[0] < 2 || layer_dims[0] > 2 + SL7_MAX_THETA) return fail(nullptr, SL7_EINVAL, "layer_dims: d_in = 2 + n_theta");
+    for (int l = 1; l <= L; ++l)
+      if (layer_dims[l] < 1 || layer_dims[l] > kMaxW) return fail(nullptr, SL7_EINVAL, "layer_dims: hidden width 1..%d", kMaxW);
+  }
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) return fail(nullptr, SL7_ECUDA, "no CUDA device: %s", cudaGetErrorString(e));
+  if (device < 0 || device >= ndev) return fail(nullptr, SL7_EINVAL, "device %d out of range", device);
+  sl7_ctx c = new (std::nothrow) sl7_ctx_s();
+  if (!c) return fail(nullptr, SL7_ENOMEM, "context allocation");
+  c->device = device;
+  c->m = m;
+  c->act = (int)act;
+  for (int i = 0; i < n_dims; ++i) c->dims.push_back(layer_dims[i]);
+  gh_grid(m, c->x, c->w);
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) {
+    c->num_sms = prop.multiProcessorCount;
+    if (prop.major != 10) {
+      delete c;
+      return fail(nullptr, SL7_ECUDA, "device %d is sm_%d%d; this library is built for sm_100a", device, prop.major, prop.minor);
+    }
+  }
+  *out = c;
+  return SL7_OK;
+}
+
+sl7_status sl7_load_weights(sl7_ctx c, const void* blob, size_t nbytes) {
+  if (!c) return fail(nullptr, SL7_EINVAL, "ctx is NULL");
+  if (c->dims.empty()) return fail(c, SL7_ESTATE, "context created without layer_dims");
+  if (!blob) return fail(c, SL7_EINVAL, "blob is NULL");
+  const unsigned char* p = static_cast<const unsigned char*>(blob);
+  size_t off = 0;
+  auto need = [&](size_t k) { return off + k <= nbytes; };
+  if (!need(12) || std::memcmp(p, "SL7W", 4) != 0) return fail(c, SL7_EFORMAT, "magic");
+  if (rd_u32(p + 4) != 1) return fail(c, SL7_EFORMAT, "version");
+  const uint32_t nd = rd_u32(p + 8);
+  off = 12;
+  if (nd != c->dims.size() || !need(4 * (size_t)nd + 8)) return fail(c, SL7_EFORMAT, "layer_dims (n_dims)");
+  for (uint32_t i = 0; i < nd; ++i)
+    if ((int)rd_u32(p + off + 4 * i) != c->dims[i]) return fail(c, SL7_EFORMAT, "layer_dims[%u]", i);
+  off += 4 * (size_t)nd;
+  if ((int)rd_u32(p + off) != c->act) return fail(c, SL7_EFORMAT, "act");
+  const uint32_t flags = rd_u32(p + off + 4);
+  off += 8;
+  std::vector<std::vector<float>> W, b;
+  for (uint32_t l = 0; l + 1 < nd; ++l) {
+    const size_t fi = c->dims[l], fo = c->dims[l + 1];
+    if (!need(4 * (fo * fi + fo))) return fail(c, SL7_EFORMAT, "size (layer %u)", l);
+    W.emplace_back(fo * fi);
+    std::memcpy(W.back().data(), p + off, 4 * fo * fi);
+    off += 4 * fo * fi;
+    b.emplace_back(fo);
+    std::memcpy(b.back().data(), p + off, 4 * fo);
+    off += 4 * fo;
+  }
+  const bool has_norm = flags & 1u;
+  std::vector<float> ish, isc, osh, osc;
+  if (has_norm) {
+    const size_t d_in = c->dims[0], m = c->m;
+    if (!need(4 * (2 * d_in + 2 * m))) return fail(c, SL7_EFORMAT, "size (normalisation)");
+    auto take = [&](std::vector<float>& v, size_t n) {
+      v.resize(n);
+      std::memcpy(v.data(), p + off, 4 * n);
+      off += 4 * n;
+    };
+    take(ish, d_in);
+    take(isc, d_in);
+    take(osh, m);
+    take(osc, m);
+    for (float s : isc)
+      if (!(s != 0.0f) || !std::isfinite(s)) return fail(c, SL7_EFORMAT, "in_scale");
+  }
+  if (off != nbytes) return fail(c, SL7_EFORMAT, "size (%zu bytes, expected %zu)", nbytes, off);
+  for (auto& v : W)
+    for (float x : v)
+      if (!std::isfinite(x)) return fail(c, SL7_EFORMAT, "non-finite weight");
+  c->W = std::move(W);
+  c->b = std::move(b);
+  c->has_norm = has_norm;
+  c->in_shift = ish;
+  c->in_scale = isc;
+  c->out_shift = osh;
+  c->out_scale = osc;
+  DeviceGuard g(c->device);
+  if (!g.ok) return fail(c, SL7_ECUDA, "cudaSetDevice(%d)", c->device);
+  sl7_status s = build_f32_image(c);
+  if (s != SL7_OK) return s;
+  c->has_net = true;
+  return SL7_OK;
+}
+
+sl7_status sl7_simulate(sl7_ctx c, double Y0, double dt, int32_t n_steps, const double* theta, int32_t n_theta,
+                        uint64_t n_paths, uint64_t seed, sl7_out out_mode, const sl7_run_opts* opts, float* d_out,
+                        double* d_stats) {
+  RunParams p;
+  sl7_status s = prepare(c, Y0, dt, n_steps, theta, n_theta, n_paths, seed, out_mode, opts, p, d_out != nullptr,
+                         d_stats != nullptr);
+  if (s != SL7_OK) return s;
+  DeviceGuard g(c->device);
+  if (!g.ok) return fail(c, SL7_ECUDA, "cudaSetDevice(%d)", c->device);
+  return run(c, p, opts, out_mode == SL7_OUT_STATS ? nullptr : d_out, d_stats);
+}
+
+sl7_status sl7_simulate_host(sl7_ctx c, double Y0, double dt, int32_t n_steps, const double* theta, int32_t n_theta,
+                             uint64_t n_paths, uint64_t seed, sl7_out out_mode, const sl7_run_opts* opts, float* h_out,
+                             double* h_stats, uint64_t* h2d_bytes, uint64_t* d2h_bytes) {
+  RunParams p;
+  sl7_status s = prepare(c, Y0, dt, n_steps, theta, n_theta, n_paths, seed, out_mode, opts, p, h_out != nullptr,
+                         h_stats != nullptr);
+  if (s != SL7_OK) return s;
+  DeviceGuard g(c->device);
+  if (!g.ok) return fail(c, SL7_ECUDA, "cudaSetDevice(%d)", c->device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(opts->stream);
+  const size_t n_out = sl7_out_elems(n_steps, n_paths, out_mode);
+  const size_t n_st = h_stats ? sl7_stats_elems(opts->n_bins) : 0;
+  cudaError_t e;
+  if (n_out > c->out_cap) {
+    if (c->d_out_scratch) cudaFree(c->d_out_scratch);
+    c->d_out_scratch = nullptr;
+    c->out_cap = 0;
+    e = cudaMalloc(&c->d_out_scratch, n_out * sizeof(float));
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaMalloc(out scratch)");
+    c->out_cap = n_out;
+  }
+  if (n_st > c->stats_cap) {
+    if (c->d_stats_scratch) cudaFree(c->d_stats_scratch);
+    c->d_stats_scratch = nullptr;
+    c->stats_cap = 0;
+    e = cudaMalloc(&c->d_stats_scratch, n_st * sizeof(double));
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaMalloc(stats scratch)");
+    c->stats_cap = n_st;
+  }
+  uint64_t up = 0, down = 0;
+  sl7_run_opts o = *opts;
+  if (h_stats && opts->accumulate) {
+    e = cudaMemcpyAsync(c->d_stats_scratch, h_stats, n_st * sizeof(double), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(c, e, "H2D stats");
+    up += n_st * sizeof(double);
+  }
+  s = run(c, p, &o, n_out ? c->d_out_scratch : nullptr, h_stats ? c->d_stats_scratch : nullptr);
+  if (s != SL7_OK) return s;
+  if (n_out) {
+    e = cudaMemcpyAsync(h_out, c->d_out_scratch, n_out * sizeof(float), cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return cuda_fail(c, e, "D2H out");
+    down += n_out * sizeof(float);
+  }
+  if (n_st) {
+    e = cudaMemcpyAsync(h_stats, c->d_stats_scratch, n_st * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return cuda_fail(c, e, "D2H stats");
+    down += n_st * sizeof(double);
+  }
+  e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "stream synchronize");
+  // kernel parameters (RunParams) travel host->device with the launch
+  up += sizeof(RunParams);
+  if (h2d_bytes) *h2d_bytes = up;
+  if (d2h_bytes) *d2h_bytes = down;
+  return SL7_OK;
+}
+
+sl7_status sl7_stats(const double* v, const sl7_run_opts* o, sl7_summary* out) {
+  if (!v || !o || !out) return fail(nullptr, SL7_EINVAL, "NULL argument");
+  if (o->n_bins < 0 || o->n_bins > 16384) return fail(nullptr, SL7_EINVAL, "n_bins");
+  if (out->n_q > 0 && (!out->q_levels || !out->q_values)) return fail(nullptr, SL7_EINVAL, "q_levels/q_values");
+  const double n = v[0];
+  out->n = (uint64_t)n;
+  out->n_nonfinite = (uint64_t)v[1];
+  if (!(n > 0)) return fail(nullptr, SL7_EINVAL, "no finite terminal values (n == 0)");
+  const double a1 = v[2] / n, a2 = v[3] / n, a3 = v[4] / n, a4 = v[5] / n;
+  const double var = a2 - a1 * a1;
+  const double m3 = a3 - 3 * a1 * a2 + 2 * a1 * a1 * a1;
+  const double m4 = a4 - 4 * a1 * a3 + 6 * a1 * a1 * a2 - 3 * a1 * a1 * a1 * a1;
+  out->mean = o->shift + a1;
+  out->var = var;
+  out->skew = var > 0 ? m3 / std::pow(var, 1.5) : 0.0;
+  out->exkurt = var > 0 ? m4 / (var * var) - 3.0 : 0.0;
+  out->strong_err = v[6] / n;
+  out->rms_err = std::sqrt(v[7] / n);
+  // quantiles from the histogram CDF, plotting position (k - 0.5)/M, uniform spread inside a bin
+  const int B = o->n_bins;
+  for (int q = 0; q < out->n_q; ++q) {
+    double res = std::nan("");
+    const double lev = out->q_levels[q];
+    if (B > 0 && lev > 0.0 && lev < 1.0) {
+      const double target = lev * n + 0.5 - 0.5;   // counts strictly below the quantile point
+      const double w = (o->hist_hi - o->hist_lo) / B;
+      double cum = v[kStatsHead];                   // underflow
+      if (target >= cum) {
+        for (int k = 0; k < B; ++k) {
+          const double ck = v[kStatsHead + 1 + k];
+          if (target < cum + ck || (k == B - 1 && target <= cum + ck)) {
+            const double frac = ck > 0 ? (target - cum) / ck : 0.0;
+            res = o->hist_lo + (k + frac) * w;
+            break;
+          }
+          cum += ck;
+        }
+      }
+    }
+    out->q_values[q] = res;
+  }
+  if (out->n_nonfinite > 0) return fail(nullptr, SL7_ENONFINITE, "%llu non-finite terminal values", (unsigned long long)out->n_nonfinite);
+  return SL7_OK;
+}
+
+sl7_status sl7_philox_u32(uint64_t seed, uint64_t off, uint64_t n, uint32_t block, uint32_t* d_out, void* stream) {
+  if (!d_out || n == 0) return fail(nullptr, SL7_EINVAL, "d_out/n_paths");
+  if (off + (n - 1) < off) return fail(nullptr, SL7_EINVAL, "path_offset + n_paths - 1 overflows 2^64");
+  const int e = launch_philox_u32(seed, off, n, block, d_out, stream);
+  return e ? cuda_fail(nullptr, (cudaError_t)e, "philox kernel") : SL7_OK;
+}
+
+sl7_status sl7_normals(uint64_t seed, uint64_t off, uint64_t n, int32_t n_steps, float* d_out, void* stream) {
+  if (!d_out || n == 0 || n_steps < 1) return fail(nullptr, SL7_EINVAL, "d_out/n_paths/n_steps");
+  if (off + (n - 1) < off) return fail(nullptr, SL7_EINVAL, "path_offset + n_paths - 1 overflows 2^64");
+  const int e = launch_normals(seed, off, n, n_steps, d_out, stream);
+  return e ? cuda_fail(nullptr, (cudaError_t)e, "normals kernel") : SL7_OK;
+}
+
+void sl7_destroy(sl7_ctx c) {
+  if (!c) return;
+  {
+    DeviceGuard g(c->device);
+    if (c->d_wf32) cudaFree(c->d_wf32);
+    if (c->d_out_scratch) cudaFree(c->d_out_scratch);
+    if (c->d_stats_scratch) cudaFree(c->d_stats_scratch);
+  }
+  delete c;
+}
+
+}  // extern "C"

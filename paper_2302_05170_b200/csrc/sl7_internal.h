@@ -1,0 +1,79 @@
+// sl7_internal.h -- structures shared by the host runtime (sl7_host.cpp) and the sm_100a kernels.
+// Not part of the ABI.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include "../../include/sl7.h"
+
+namespace sl7 {
+
+constexpr int kMaxM = SL7_MAX_M;
+constexpr int kMaxW = SL7_MAX_WIDTH;
+constexpr int kMaxHidden = SL7_MAX_HIDDEN;
+constexpr int kStatsHead = SL7_STATS_HEAD;
+
+enum Colloc : int { kAnn = 0, kExactGbm = 1, kExactOu = 2 };
+enum Ref : int { kRefNone = 0, kRefGbm = 1, kRefOu = 2 };
+enum OutMode : int { kFull = 0, kTerminal = 1, kStatsOnly = 2 };
+
+// Everything one launch of a step kernel needs, passed by value as a __grid_constant__ parameter
+// (kernel parameters live in the constant bank: uniform, broadcast, no global loads).
+struct RunParams {
+  // ---- problem ----
+  int m;                 // nodes
+  int n_steps;
+  int out_mode;          // OutMode
+  int colloc;            // Colloc
+  uint64_t n_paths;
+  uint64_t path_offset;  // global id of path 0 of this launch
+  uint32_t key0, key1;   // Philox key = (seed_lo, seed_hi)
+  float y0;
+  // ---- interpolation grid (Algorithm I step 5): nodes split x = xhi + xlo, barycentric w ----
+  float xhi[kMaxM], xlo[kMaxM], w[kMaxM];
+  // ---- exact collocation: GBM y_j = Y*c[j]; OU y_j = ou_a*Y + ou_b + c[j] (c[j] = std*x_j) ----
+  float c[kMaxM];
+  float ou_a, ou_b;
+  // ---- strong-error reference on the same normals ----
+  int ref;               // Ref
+  double ref_drift_T;    // GBM: (mu - s^2/2) T
+  double ref_vol;        // GBM: s sqrt(dt)
+  double ref_a, ref_b, ref_s;   // OU: R <- a R + b + s Z
+  double y0_d;
+  // ---- statistics ----
+  int has_stats;
+  int n_bins;
+  double shift, hist_lo, hist_scale;   // bin = floor((Y - lo) * scale)
+  float* out;
+  double* stats;
+  // ---- ANN (layer 1 folded: pre_k = l1w[k] * Y + l1b[k]) ----
+  int act;               // sl7_act
+  int n_hidden;          // L
+  int width;             // padded hidden width used by the kernel
+  float l1w[kMaxW], l1b[kMaxW];
+  float out_scale[kMaxM], out_shift[kMaxM];
+  const float* wdev;     // FP32 kernel: hidden + output weights (layout: WeightLayoutF32)
+  const void* wtc;       // TC kernel: packed bf16 operand images (layout: sl7_tc.cu)
+  const float* btc;      // TC kernel: fp32 biases [(L-1)][64] + out bias [16]
+};
+
+// FP32-kernel weight image: for hidden layer l = 1..L-1: W[H][HS] then b[H] padded to a multiple of 4
+// floats (HS = row stride, multiple of 4; every row starts 16-byte aligned), then Wout[M][HS], bout[M].
+// Zero padded.
+#ifdef __CUDACC__
+#define SL7_HD __host__ __device__
+#else
+#define SL7_HD
+#endif
+SL7_HD inline size_t f32_layer_floats(int H, int HS) { return (size_t)H * HS + (size_t)((H + 3) & ~3); }
+SL7_HD inline size_t f32_weight_floats(int H, int HS, int L, int M) {
+  return (size_t)(L - 1) * f32_layer_floats(H, HS) + (size_t)M * HS + (size_t)((M + 3) & ~3);
+}
+
+// launchers (sl7_kernels.cu / sl7_tc.cu); return cudaError_t as int
+int launch_step_kernel(const RunParams& p, int prec, void* stream, int num_sms);
+int launch_philox_u32(uint64_t seed, uint64_t off, uint64_t n, uint32_t block, uint32_t* out, void* stream);
+int launch_normals(uint64_t seed, uint64_t off, uint64_t n, int n_steps, float* out, void* stream);
+int launch_zero_stats(double* stats, size_t n, void* stream);
+
+}  // namespace sl7

@@ -1,0 +1,254 @@
+// sl7_kernels.cu -- CUDA-core step kernels for sm_100a:
+//   * exact-collocation kernel (GBM / OU closed-form H_j, BASELINE north_star + Eq. 6.6)
+//   * ANN-FP32 kernel ("exact mode" MLP on the FMA pipe, weights staged in shared memory)
+//   * RNG verification kernels (raw Philox words, normals)
+//
+// Persistent grid-stride design: one thread owns one path for ALL n_steps (Algorithm I steps 3-8
+// run without leaving the kernel: state Y in a register, no host round trip per step, no HBM
+// traffic except the optional path output).  Consecutive threads own consecutive paths, so a
+// FULL-mode store of step i by a warp is one contiguous 128-byte segment of row i.
+#include <cuda_runtime.h>
+
+#include "sl7_device.cuh"
+
+namespace sl7 {
+
+// ------------------------------------------------------------------------------------------------
+// Exact-collocation step kernel.  y_j = H_j(Y) in closed form, then g_m(Z).
+// ------------------------------------------------------------------------------------------------
+template <int MR, bool RT_M, int COLLOC>
+__global__ void __launch_bounds__(256) exact_step_kernel(const __grid_constant__ RunParams p) {
+  extern __shared__ uint32_t hist[];
+  __shared__ double red[8];
+  hist_init(p, hist);
+  __syncthreads();
+  StatAcc acc;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < p.n_paths; q += stride) {
+    const uint64_t gp = p.path_offset + q;
+    float Y = p.y0;
+    if (p.out_mode == kFull) p.out[q] = Y;
+    RefState rs;
+    ref_init(rs, p);
+    float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
+    for (int i = 0; i < p.n_steps; ++i) {
+      if ((i & 3) == 0) normals4(p.key0, p.key1, gp, (uint32_t)(i >> 2), z0, z1, z2, z3);
+      const float Z = z0;
+      z0 = z1; z1 = z2; z2 = z3;
+      float y[MR];
+      if constexpr (COLLOC == kExactGbm) {
+#pragma unroll
+        for (int j = 0; j < MR; ++j) y[j] = Y * p.c[j];
+      } else {
+        const float mean = fmaf(p.ou_a, Y, p.ou_b);
+#pragma unroll
+        for (int j = 0; j < MR; ++j) y[j] = mean + p.c[j];
+      }
+      Y = gm_eval<MR, RT_M>(p, Z, y);
+      ref_step(rs, p, Z);
+      if (p.out_mode == kFull) p.out[(uint64_t)(i + 1) * p.n_paths + q] = Y;
+    }
+    if (p.out_mode == kTerminal) p.out[q] = Y;
+    if (p.has_stats) stat_add(acc, p, Y, ref_final(rs, p), hist);
+  }
+  if (p.has_stats) stat_flush(acc, p, hist, red);
+}
+
+// ------------------------------------------------------------------------------------------------
+// ANN-FP32 step kernel.  Layer 1 folded (pre_k = l1w_k Y + l1b_k, constant bank); hidden and output
+// layers read from shared memory as float4 broadcasts (all lanes of a warp read the same row), one
+// FFMA per weight with the activation vector held in registers.
+// ------------------------------------------------------------------------------------------------
+template <int H, int HS, int MR, bool RT_M, int ACT>
+__global__ void __launch_bounds__(128) ann_f32_step_kernel(const __grid_constant__ RunParams p) {
+  extern __shared__ float4 smem4[];
+  float* sw = reinterpret_cast<float*>(smem4);
+  __shared__ double red[8];
+  const int L = p.n_hidden;
+  const size_t nw = f32_weight_floats(H, HS, L, MR);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(sw + ((nw + 3) & ~size_t(3)));
+  for (size_t k = threadIdx.x; k < nw; k += blockDim.x) sw[k] = p.wdev[k];
+  hist_init(p, hist);
+  __syncthreads();
+  const float* wout = sw + (size_t)(L - 1) * f32_layer_floats(H, HS);
+  const float* bout = wout + MR * HS;
+
+  StatAcc acc;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < p.n_paths; q += stride) {
+    const uint64_t gp = p.path_offset + q;
+    float Y = p.y0;
+    if (p.out_mode == kFull) p.out[q] = Y;
+    RefState rs;
+    ref_init(rs, p);
+    float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
+    for (int i = 0; i < p.n_steps; ++i) {
+      if ((i & 3) == 0) normals4(p.key0, p.key1, gp, (uint32_t)(i >> 2), z0, z1, z2, z3);
+      const float Z = z0;
+      z0 = z1; z1 = z2; z2 = z3;
+      // step 3 (Eq. 6.4): y_hat = H_hat(Y_i, dt, theta)
+      float h[H];
+#pragma unroll
+      for (int k = 0; k < H; ++k) h[k] = activate<ACT>(fmaf(p.l1w[k], Y, p.l1b[k]));
+      for (int l = 0; l < L - 1; ++l) {
+        const float* W = sw + (size_t)l * f32_layer_floats(H, HS);
+        const float* b = W + H * HS;
+        float g[H];
+#pragma unroll
+        for (int j = 0; j < H; ++j) {
+          const float4* row = reinterpret_cast<const float4*>(W + j * HS);
+          float a0 = b[j], a1 = 0.f;
+#pragma unroll
+          for (int kk = 0; kk < HS / 4; ++kk) {
+            const float4 wv = row[kk];
+            if (4 * kk + 0 < H) a0 = fmaf(wv.x, h[4 * kk + 0], a0);
+            if (4 * kk + 1 < H) a1 = fmaf(wv.y, h[4 * kk + 1], a1);
+            if (4 * kk + 2 < H) a0 = fmaf(wv.z, h[4 * kk + 2], a0);
+            if (4 * kk + 3 < H) a1 = fmaf(wv.w, h[4 * kk + 3], a1);
+          }
+          g[j] = activate<ACT>(a0 + a1);
+        }
+#pragma unroll
+        for (int k = 0; k < H; ++k) h[k] = g[k];
+      }
+      float y[MR];
+#pragma unroll
+      for (int j = 0; j < MR; ++j) {
+        const float4* row = reinterpret_cast<const float4*>(wout + j * HS);
+        float a0 = bout[j], a1 = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < HS / 4; ++kk) {
+          const float4 wv = row[kk];
+          if (4 * kk + 0 < H) a0 = fmaf(wv.x, h[4 * kk + 0], a0);
+          if (4 * kk + 1 < H) a1 = fmaf(wv.y, h[4 * kk + 1], a1);
+          if (4 * kk + 2 < H) a0 = fmaf(wv.z, h[4 * kk + 2], a0);
+          if (4 * kk + 3 < H) a1 = fmaf(wv.w, h[4 * kk + 3], a1);
+        }
+        y[j] = fmaf(a0 + a1, p.out_scale[j], p.out_shift[j]);
+      }
+      // steps 5-6: Y_{i+1} = g_m(X_hat)
+      Y = gm_eval<MR, RT_M>(p, Z, y);
+      ref_step(rs, p, Z);
+      if (p.out_mode == kFull) p.out[(uint64_t)(i + 1) * p.n_paths + q] = Y;
+    }
+    if (p.out_mode == kTerminal) p.out[q] = Y;
+    if (p.has_stats) stat_add(acc, p, Y, ref_final(rs, p), hist);
+  }
+  if (p.has_stats) stat_flush(acc, p, hist, red);
+}
+
+// ------------------------------------------------------------------------------------------------
+// RNG verification kernels (same device functions as the step kernels).
+// ------------------------------------------------------------------------------------------------
+__global__ void philox_u32_kernel(uint32_t k0, uint32_t k1, uint64_t off, uint64_t n, uint32_t block, uint32_t* out) {
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint4 r = philox_path_block(k0, k1, off + q, block);
+    out[q] = r.x;
+    out[n + q] = r.y;
+    out[2 * n + q] = r.z;
+    out[3 * n + q] = r.w;
+  }
+}
+
+__global__ void normals_kernel(uint32_t k0, uint32_t k1, uint64_t off, uint64_t n, int n_steps, float* out) {
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (uint64_t)gridDim.x * blockDim.x) {
+    float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
+    for (int i = 0; i < n_steps; ++i) {
+      if ((i & 3) == 0) normals4(k0, k1, off + q, (uint32_t)(i >> 2), z0, z1, z2, z3);
+      out[(uint64_t)i * n + q] = z0;
+      z0 = z1; z1 = z2; z2 = z3;
+    }
+  }
+}
+
+__global__ void zero_kernel(double* p, size_t n) {
+  for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (size_t)gridDim.x * blockDim.x) p[k] = 0.0;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Launchers
+// ------------------------------------------------------------------------------------------------
+namespace {
+
+template <typename K>
+cudaError_t launch_persistent(K kernel, int threads, size_t smem, const RunParams& p, cudaStream_t st, int num_sms) {
+  cudaError_t e;
+  if (smem > 48 * 1024) {
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  const uint64_t need = (p.n_paths + threads - 1) / threads;
+  const uint64_t full = (uint64_t)per_sm * (uint64_t)num_sms;
+  const unsigned grid = (unsigned)(need < full ? need : full);
+  kernel<<<grid, threads, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+size_t hist_bytes(const RunParams& p) {
+  return (p.has_stats && p.n_bins > 0) ? sizeof(uint32_t) * (size_t)(p.n_bins + 2) : 0;
+}
+
+template <int COLLOC>
+cudaError_t launch_exact(const RunParams& p, cudaStream_t st, int num_sms) {
+  const size_t smem = hist_bytes(p);
+  switch (p.m) {
+    case 5: return launch_persistent(exact_step_kernel<5, false, COLLOC>, 256, smem, p, st, num_sms);
+    case 7: return launch_persistent(exact_step_kernel<7, false, COLLOC>, 256, smem, p, st, num_sms);
+    default: return launch_persistent(exact_step_kernel<kMaxM, true, COLLOC>, 256, smem, p, st, num_sms);
+  }
+}
+
+template <int H, int HS, int MR, bool RT, int ACT>
+cudaError_t launch_ann_f32_t(const RunParams& p, cudaStream_t st, int num_sms) {
+  const size_t nw = f32_weight_floats(H, HS, p.n_hidden, MR);
+  const size_t smem = ((nw + 3) & ~size_t(3)) * sizeof(float) + hist_bytes(p);
+  return launch_persistent(ann_f32_step_kernel<H, HS, MR, RT, ACT>, 128, smem, p, st, num_sms);
+}
+
+template <int ACT>
+cudaError_t launch_ann_f32(const RunParams& p, cudaStream_t st, int num_sms) {
+  if (p.width == 50 && p.m == 5) return launch_ann_f32_t<50, 52, 5, false, ACT>(p, st, num_sms);
+  if (p.width == 50 && p.m == 7) return launch_ann_f32_t<50, 52, 7, false, ACT>(p, st, num_sms);
+  if (p.width == 64) return launch_ann_f32_t<64, 64, kMaxM, true, ACT>(p, st, num_sms);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+int launch_step_kernel(const RunParams& p, int prec, void* stream, int num_sms) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  (void)prec;
+  switch (p.colloc) {
+    case kExactGbm: return (int)launch_exact<kExactGbm>(p, st, num_sms);
+    case kExactOu: return (int)launch_exact<kExactOu>(p, st, num_sms);
+    default:
+      return (int)(p.act == SL7_ACT_TANH ? launch_ann_f32<SL7_ACT_TANH>(p, st, num_sms)
+                                         : launch_ann_f32<SL7_ACT_SOFTPLUS>(p, st, num_sms));
+  }
+}
+
+int launch_philox_u32(uint64_t seed, uint64_t off, uint64_t n, uint32_t block, uint32_t* out, void* stream) {
+  const unsigned grid = (unsigned)((n + 255) / 256 < 65535 ? (n + 255) / 256 : 65535);
+  philox_u32_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      (uint32_t)seed, (uint32_t)(seed >> 32), off, n, block, out);
+  return (int)cudaGetLastError();
+}
+
+int launch_normals(uint64_t seed, uint64_t off, uint64_t n, int n_steps, float* out, void* stream) {
+  const unsigned grid = (unsigned)((n + 255) / 256 < 65535 ? (n + 255) / 256 : 65535);
+  normals_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      (uint32_t)seed, (uint32_t)(seed >> 32), off, n, n_steps, out);
+  return (int)cudaGetLastError();
+}
+
+int launch_zero_stats(double* stats, size_t n, void* stream) {
+  const unsigned grid = (unsigned)((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024);
+  zero_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(stats, n);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace sl7

@@ -1,0 +1,273 @@
+"""GPU parity: the CUDA path (through the C ABI) against the float64 oracle, element by element.
+
+Tolerances (BASELINE north_star):
+  T-1 Philox words bit-exact (and equal to cuRAND curand4());
+  T-2 fp32 path values: teacher-forced one step, |Y_dev - Y_or| <= 1e-5 * kappa, kappa the
+      forward-error scale sum_j |l_j(Z)| A_j;
+  T-5 histogram counts equal except values within one fp32 ulp of an edge;
+  T-6 sharded runs bitwise equal per path, histogram equal, moments within 1e-12.
+"""
+import ctypes
+import os
+
+import numpy as np
+import pytest
+
+from oracle import sl7_oracle as O
+from sl7_inputs import ACT_SOFTPLUS, ACT_TANH, glorot_mlp, load_golden_blob, pack_blob, workloads
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _run(sl7, ctx, spec_kw, n_paths, seed, out_mode=None, colloc=None, prec=None, stats=False, n_bins=0,
+         lo=0.0, hi=1.0, shift=0.0, ref=0, ref_theta=(0, 0, 0), offset=0, theta=None):
+    torch = _torch()
+    opts = sl7.make_opts(prec=sl7.PREC_FP32 if prec is None else prec, colloc=colloc, path_offset=offset,
+                         n_bins=n_bins, hist_lo=lo, hist_hi=hi, shift=shift, ref=ref, ref_theta=ref_theta)
+    st = torch.zeros(sl7.stats_elems(n_bins), dtype=torch.float64, device="cuda") if stats else None
+    out, st = ctx.simulate(spec_kw["y0"], spec_kw["dt"], spec_kw["n_steps"], theta, n_paths, seed, out_mode, opts,
+                           stats=st)
+    torch.cuda.synchronize()
+    o = None if out is None else out.double().cpu().numpy()
+    return o, (None if st is None else st.cpu().numpy())
+
+
+def _teacher_forced(spec, Yd, Z, tol=1e-5):
+    worst = 0.0
+    for i in range(spec.n_steps):
+        ref = O.step(spec, Yd[i], Z[i])
+        kappa = O.step_error_scale(spec, Yd[i], Z[i])
+        r = np.abs(Yd[i + 1] - ref) / kappa
+        worst = max(worst, float(r.max()))
+        bad = r > tol
+        assert not bad.any(), "step %d: %d/%d paths off, worst %.3g (path %d: dev %r or %r)" % (
+            i, bad.sum(), bad.size, r.max(), int(np.argmax(r)), Yd[i + 1][np.argmax(r)], ref[np.argmax(r)])
+    return worst
+
+
+# ------------------------------------------------------------------------------------------- RNG
+
+@pytest.mark.parametrize("offset", [0, (1 << 32) - 300, (1 << 64) - 1000])
+def test_philox_bitexact_vs_oracle(gpu_lib, offset):
+    torch = _torch()
+    sl7 = gpu_lib
+    n = 1000 if offset else 70_001
+    for seed, block in [(2302051701, 0), (0xFFFFFFFFFFFFFFFF, 7), (123, 0xFFFFFFFF)]:
+        out = torch.empty(4 * n, dtype=torch.int32, device="cuda")
+        sl7.philox_u32(seed, offset, n, block, out)
+        torch.cuda.synchronize()
+        dev = out.cpu().numpy().view(np.uint32).reshape(4, n)
+        ref = O.philox_block(seed, np.uint64(offset) + np.arange(n, dtype=np.uint64), block)
+        for k in range(4):
+            np.testing.assert_array_equal(dev[k], ref[k].astype(np.uint32))
+
+
+def test_philox_equals_curand(gpu_lib):
+    torch = _torch()
+    sl7 = gpu_lib
+    lib = ctypes.CDLL(os.path.join(ROOT, "tests", "native", "libcurand_pin.so"))
+    lib.curand_pin_u32.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32,
+                                   ctypes.c_void_p, ctypes.c_void_p]
+    n = 50_000
+    for seed, off, block in [(2302051701, 0, 0), (99, (1 << 33) + 5, 3), (0xDEADBEEFCAFEF00D, 17, 1000)]:
+        a = torch.empty(4 * n, dtype=torch.int32, device="cuda")
+        b = torch.empty(4 * n, dtype=torch.int32, device="cuda")
+        sl7.philox_u32(seed, off, n, block, a)
+        assert lib.curand_pin_u32(seed, off, n, block, ctypes.c_void_p(b.data_ptr()),
+                                  ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)) == 0
+        torch.cuda.synchronize()
+        assert torch.equal(a, b)
+
+
+def test_normals_vs_oracle(gpu_lib):
+    torch = _torch()
+    sl7 = gpu_lib
+    n, steps, seed = 200_000, 9, 77
+    out = torch.empty(steps * n, dtype=torch.float32, device="cuda")
+    sl7.normals(seed, 5, n, steps, out)
+    torch.cuda.synchronize()
+    dev = out.double().cpu().numpy().reshape(steps, n)
+    ref = O.normals(seed, 5 + np.arange(n, dtype=np.uint64), steps)
+    err = np.abs(dev - ref)
+    assert err.max() <= 2e-6 * np.maximum(1.0, np.abs(ref)).max()
+    assert np.all(err <= 1e-6 * np.maximum(1.0, np.abs(ref)))
+
+
+# ----------------------------------------------------------------------------------- exact modes
+
+@pytest.mark.parametrize("m,n_steps,dt", [(5, 2, 0.5), (7, 64, 1 / 64), (3, 5, 0.3), (1, 3, 0.5), (12, 4, 1.0)])
+def test_exact_gbm_full_teacher_forced(gpu_lib, m, n_steps, dt):
+    sl7 = gpu_lib
+    n_paths = 20_000 + 33
+    ctx = sl7.Context(m)
+    kw = dict(y0=1.0, dt=dt, n_steps=n_steps)
+    Yd, _ = _run(sl7, ctx, kw, n_paths, 2302051700, sl7.OUT_FULL, sl7.COLLOC_EXACT_GBM, theta=(0.05, 0.2))
+    Yd = Yd.reshape(n_steps + 1, n_paths)
+    assert np.all(Yd[0] == 1.0)
+    spec = O.Spec(m, "gbm", (0.05, 0.2), 1.0, dt, n_steps)
+    Z = O.normals(2302051700, np.arange(n_paths, dtype=np.uint64), n_steps)
+    _teacher_forced(spec, Yd, Z)
+    # free running: drift of fp32 vs fp64 stays small (reported bound)
+    Yo, _ = O.simulate(spec, 2302051700, np.arange(n_paths, dtype=np.uint64))
+    rel = np.abs(Yd[-1] - Yo[-1]) / np.abs(Yo[-1])
+    assert np.median(rel) < 1e-5 and rel.max() < 5e-4
+
+
+@pytest.mark.parametrize("theta", [(0.0, 1.0, 0.5), (0.3, 1e-8, 0.7), (-0.2, 3.0, 0.0)])
+def test_exact_ou_full_teacher_forced_and_eq66(gpu_lib, theta):
+    sl7 = gpu_lib
+    n_paths, n_steps, dt = 30_000, 16, 0.125
+    ctx = sl7.Context(7)
+    Yd, _ = _run(sl7, ctx, dict(y0=1.0, dt=dt, n_steps=n_steps), n_paths, 5, sl7.OUT_FULL, sl7.COLLOC_EXACT_OU,
+                 theta=theta)
+    Yd = Yd.reshape(n_steps + 1, n_paths)
+    spec = O.Spec(7, "ou", theta, 1.0, dt, n_steps)
+    Z = O.normals(5, np.arange(n_paths, dtype=np.uint64), n_steps)
+    _teacher_forced(spec, Yd, Z)
+    R = O.exact_reference("ou", theta, 1.0, dt, Z)           # Eq. 6.6 on the same normals
+    assert np.max(np.abs(Yd[-1] - R)) < 2e-5
+
+
+def test_sigma_zero_and_degenerate_sizes(gpu_lib):
+    sl7 = gpu_lib
+    ctx = sl7.Context(5)
+    Yd, _ = _run(sl7, ctx, dict(y0=2.0, dt=0.25, n_steps=4), 1, 9, sl7.OUT_FULL, sl7.COLLOC_EXACT_GBM,
+                 theta=(0.05, 0.0))
+    np.testing.assert_allclose(Yd, 2.0 * np.exp(0.05 * 0.25 * np.arange(5)), rtol=3e-7)
+    Yd, _ = _run(sl7, ctx, dict(y0=1.0, dt=0.5, n_steps=1), 257, 9, sl7.OUT_TERMINAL, sl7.COLLOC_EXACT_OU,
+                 theta=(0.1, 1.0, 0.0))
+    np.testing.assert_allclose(Yd, np.exp(-0.5) + 0.1 * (1 - np.exp(-0.5)), rtol=3e-7)
+
+
+# ------------------------------------------------------------------------------------ ANN-FP32
+
+ANN_CASES = [
+    ("cfg0", None),
+    ("cfg1", None),
+    ("cfg2_ou", None),
+    ("cfg2_cir", None),
+    ("glorot_generic", ((4, 17, 9, 33, 6), ACT_TANH)),
+    ("glorot_generic_sp", ((3, 64, 64, 3), ACT_SOFTPLUS)),
+]
+
+
+def _ann_case(name, gen):
+    W = workloads()
+    if gen is None:
+        w = W[name]
+        blob = load_golden_blob(w.blob)
+        theta = tuple(w.theta) if w.process != "gbm" else ()
+        return blob, w.m, list(w.dims), w.act, theta, w.y0, min(w.n_steps, 16), w.dt
+    dims, act = gen
+    p = glorot_mlp(dims, act, seed=31, with_norm=True)
+    theta = tuple(0.1 * (k + 1) for k in range(dims[0] - 2))
+    return pack_blob(p), dims[-1], list(dims), act, theta, 0.7, 6, 0.2
+
+
+@pytest.mark.parametrize("name,gen", ANN_CASES, ids=[c[0] for c in ANN_CASES])
+def test_ann_fp32_full_teacher_forced(gpu_lib, name, gen):
+    sl7 = gpu_lib
+    blob, m, dims, act, theta, y0, n_steps, dt = _ann_case(name, gen)
+    n_paths = 8192 + 129
+    ctx = sl7.Context(m, dims, act)
+    ctx.load_weights(blob)
+    Yd, _ = _run(sl7, ctx, dict(y0=y0, dt=dt, n_steps=n_steps), n_paths, 424242, sl7.OUT_FULL, sl7.COLLOC_ANN,
+                 theta=theta)
+    Yd = Yd.reshape(n_steps + 1, n_paths)
+    spec = O.Spec(m, "ann", theta, y0, dt, n_steps, net=O.parse_blob(blob))
+    Z = O.normals(424242, np.arange(n_paths, dtype=np.uint64), n_steps)
+    _teacher_forced(spec, Yd, Z)
+
+
+def test_ann_requires_weights_and_supported_precision(gpu_lib):
+    sl7 = gpu_lib
+    w = workloads()["cfg0"]
+    ctx = sl7.Context(w.m, list(w.dims), w.act)
+    with pytest.raises(sl7.Sl7Error, match="ESTATE"):
+        _run(sl7, ctx, dict(y0=1.0, dt=0.5, n_steps=2), 100, 1, sl7.OUT_TERMINAL, sl7.COLLOC_ANN, theta=())
+    bad = bytearray(load_golden_blob(w.blob))
+    bad[4] = 9
+    with pytest.raises(sl7.Sl7Error, match="version"):
+        ctx.load_weights(bytes(bad))
+    with pytest.raises(sl7.Sl7Error, match="EFORMAT"):
+        ctx.load_weights(load_golden_blob(w.blob)[:-4])
+
+
+# ------------------------------------------------------------------------------------ statistics
+
+def test_stats_fused_vs_oracle(gpu_lib):
+    sl7 = gpu_lib
+    n_paths, n_bins, lo, hi = 300_007, 4096, 0.0, 3.0
+    ctx = sl7.Context(7)
+    kw = dict(y0=1.0, dt=1 / 16, n_steps=16)
+    YT, st = _run(sl7, ctx, kw, n_paths, 11, sl7.OUT_TERMINAL, sl7.COLLOC_EXACT_GBM, stats=True, n_bins=n_bins,
+                  lo=lo, hi=hi, shift=1.0, ref=sl7.REF_GBM, ref_theta=(0.05, 0.2, 0), theta=(0.05, 0.2))
+    # the reference Y(T) is evaluated on the normals the kernel consumed (fp32 X_hat, the same inputs):
+    # the exact-mode strong error is rounding-level (~3e-7), the size of the fp32-vs-fp64 normal gap
+    torch = _torch()
+    zd = torch.empty(16 * n_paths, dtype=torch.float32, device="cuda")
+    sl7.normals(11, 0, n_paths, 16, zd)
+    torch.cuda.synchronize()
+    Zd = zd.double().cpu().numpy().reshape(16, n_paths)
+    R = O.exact_reference("gbm", (0.05, 0.2), 1.0, 1 / 16, Zd)
+    v = O.stats_vector(YT, 1.0, lo, hi, n_bins, R)            # same terminal values, oracle statistics
+    assert st[0] == v[0] and st[1] == 0
+    np.testing.assert_allclose(st[2:6], v[2:6], rtol=1e-12, atol=1e-9)
+    np.testing.assert_allclose(st[6:8], v[6:8], rtol=1e-7)
+    w = (hi - lo) / n_bins
+    edge = np.abs((YT - lo) / w - np.round((YT - lo) / w)) * w <= np.spacing(YT.astype(np.float32)).astype(np.float64)
+    diff = np.abs(st[8:] - v[8:]).sum()
+    assert diff <= 2 * edge.sum()
+    # strong error of exact GBM collocation vs exact GBM: rounding-level, flat in dt
+    assert st[6] / st[0] < 5e-6
+
+
+def test_sharding_bitwise(gpu_lib):
+    """T-6: per-path outputs of W shards (path_offset) are bitwise the unsharded run's."""
+    sl7 = gpu_lib
+    torch = _torch()
+    w = workloads()["cfg2_ou"]
+    blob = load_golden_blob(w.blob)
+    ctx = sl7.Context(w.m, list(w.dims), w.act)
+    ctx.load_weights(blob)
+    N = 100_003
+    kw = dict(y0=w.y0, dt=w.dt, n_steps=w.n_steps)
+    full, st_full = _run(sl7, ctx, kw, N, w.seed, sl7.OUT_TERMINAL, sl7.COLLOC_ANN, stats=True, n_bins=512, lo=-2,
+                         hi=2, theta=w.theta)
+    for W in (2, 3, 8):
+        per = -(-N // W)
+        parts, acc = [], np.zeros_like(st_full)
+        for r in range(W):
+            lo_, n = r * per, min(N, (r + 1) * per) - r * per
+            o, s = _run(sl7, ctx, kw, n, w.seed, sl7.OUT_TERMINAL, sl7.COLLOC_ANN, stats=True, n_bins=512, lo=-2,
+                        hi=2, offset=lo_, theta=w.theta)
+            parts.append(o)
+            acc += s
+        assert np.array_equal(np.concatenate(parts), full)
+        assert np.array_equal(acc[8:], st_full[8:]) and acc[0] == st_full[0]
+        np.testing.assert_allclose(acc[2:6], st_full[2:6], rtol=1e-12)
+
+
+def test_host_buffers_equal_device_run(gpu_lib):
+    sl7 = gpu_lib
+    w = workloads()["cfg0"]
+    blob = load_golden_blob(w.blob)
+    ctx = sl7.Context(w.m, list(w.dims), w.act)
+    ctx.load_weights(blob)
+    n = 12_345
+    dev, dst = _run(sl7, ctx, dict(y0=1.0, dt=0.5, n_steps=2), n, 3, sl7.OUT_FULL, sl7.COLLOC_ANN, stats=True,
+                    n_bins=64, lo=0, hi=3, theta=())
+    h_out = np.empty(3 * n, dtype=np.float32)
+    h_st = np.empty(sl7.stats_elems(64), dtype=np.float64)
+    opts = sl7.make_opts(prec=sl7.PREC_FP32, colloc=sl7.COLLOC_ANN, n_bins=64, hist_lo=0, hist_hi=3)
+    _, _, up, down = ctx.simulate_host(1.0, 0.5, 2, (), n, 3, sl7.OUT_FULL, opts, h_out, h_st)
+    assert np.array_equal(h_out.astype(np.float64), dev)
+    np.testing.assert_allclose(h_st, dst, rtol=1e-12)
+    assert down == h_out.nbytes + h_st.nbytes and up > 0
