@@ -302,10 +302,22 @@ def main():
                 "peak_basis": "148 SM x 128 FFMA lanes x 2 FLOP x %g MHz (max SM clock, MEASURED_PEAKS.json)" % sm_max,
                 "algorithmic": "%d FLOP per path-step (rank-1 layer 1 + 2x50x50 + 50x7 MACs)" % flops_ps}
     else:
+        # The tcgen05 kernel is bound by the transcendental (XU / MUFU) pipe, not the tensor pipe
+        # (SURVEY §8(d)): one activation per hidden unit is the method's algorithmic transcendental count.
+        trans_ps = sum(W.dims[1:-1])
+        rate = path_steps / (tot_kernel_ms * 1e-3)
+        achieved = trans_ps * rate / 1e12
+        peak = n_sms * 16 * sm_max * 1e6 / 1e12
         bf16 = peaks.get("bf16_tflops", 1642.7)
-        achieved = flops_ps * path_steps / (tot_kernel_ms * 1e-3) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s", "frac": achieved / bf16,
-                "traffic": None, "peak_basis": "MEASURED_PEAKS.json bf16_tflops (burst)"}
+        mma_flops_ps = flops_ps - 2 * W.dims[1]
+        tens = mma_flops_ps * rate / 1e12
+        roof = {"bound": "alu", "pipe": "XU (MUFU)", "achieved": achieved, "peak": peak, "unit": "Top/s",
+                "frac": achieved / peak, "traffic": None,
+                "peak_basis": "148 SM x 16 MUFU op/clk x %g MHz (max SM clock)" % sm_max,
+                "algorithmic": "%d transcendental activations per path-step (one per hidden unit); the kernel "
+                               "spends 2 MUFU ops per activation (ex2 + rcp / ex2 + lg2) for ~2e-7 accuracy" % trans_ps,
+                "tensor": {"achieved": tens, "peak": bf16, "unit": "TFLOP/s", "frac": tens / bf16,
+                           "basis": "%d MMA FLOP per path-step vs MEASURED_PEAKS.json bf16_tflops (burst)" % mma_flops_ps}}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,

@@ -26,6 +26,7 @@ COLLOC_ANN, COLLOC_EXACT_GBM, COLLOC_EXACT_OU = 0, 1, 2
 REF_NONE, REF_GBM, REF_OU = 0, 1, 2
 STATS_HEAD = 8
 MAX_M = 16
+HAS_TC = True   # libsl7 has the tcgen05 (SL7_PREC_BF16) ANN kernel
 
 
 class sl7_run_opts(ctypes.Structure):

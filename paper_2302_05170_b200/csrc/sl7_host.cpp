@@ -43,6 +43,8 @@ struct sl7_ctx_s {
   // device images
   int width = 0;           // hidden width used by the FP32 kernel (50 or 64 padded)
   float* d_wf32 = nullptr;
+  void* d_wtc = nullptr;   // bf16 SWIZZLE_128B operand image for the tcgen05 kernel
+  TcParams tcp;            // biases + image pointer for the tcgen05 kernel
   int num_sms = 148;
   // host-mode staging
   float* d_out_scratch = nullptr;
@@ -217,6 +219,44 @@ sl7_status build_f32_image(sl7_ctx c) {
   return SL7_OK;
 }
 
+uint16_t f32_to_bf16_rne(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+
+// bf16 operand image of the MMA layers (layout: TcParams in sl7_internal.h) + fp32 biases.
+sl7_status build_tc_image(sl7_ctx c) {
+  const int L = (int)c->dims.size() - 2;
+  const int nL = L - 1;
+  std::vector<uint16_t> img((size_t)(nL * kTcTileBytes + kTcOutBytes) / 2, 0);
+  auto put = [&](size_t tile_off_bytes, int n, int k, float v) {
+    const size_t byte = tile_off_bytes + (size_t)n * 128 + (size_t)((((k * 2) >> 4) ^ (n & 7)) << 4) + (size_t)((k * 2) & 15);
+    img[byte / 2] = f32_to_bf16_rne(v);
+  };
+  std::memset(&c->tcp, 0, sizeof c->tcp);
+  for (int l = 1; l <= L; ++l) {   // blob layer l: hidden l -> hidden l+1 (l < L) or -> output (l == L)
+    const int fi = c->dims[l], fo = c->dims[l + 1];
+    const size_t off = (size_t)(l - 1) * kTcTileBytes;
+    for (int n = 0; n < fo; ++n)
+      for (int k = 0; k < fi; ++k) put(off, n, k, c->W[l][(size_t)n * fi + k]);
+    for (int n = 0; n < fo; ++n) {
+      if (l < L) c->tcp.bias[l - 1][n] = c->b[l][n];
+      else c->tcp.bout[n] = c->b[l][n];
+    }
+  }
+  c->tcp.n_mma_hidden = nL;
+  if (c->d_wtc) cudaFree(c->d_wtc);
+  c->d_wtc = nullptr;
+  cudaError_t e = cudaMalloc(&c->d_wtc, img.size() * 2);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaMalloc(tc weights)");
+  e = cudaMemcpy(c->d_wtc, img.data(), img.size() * 2, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemcpy(tc weights)");
+  c->tcp.wimg = c->d_wtc;
+  return SL7_OK;
+}
+
 // Fill RunParams for one call; all validation happens here (synchronously, before any launch).
 sl7_status prepare(sl7_ctx c, double Y0, double dt, int32_t n_steps, const double* theta, int32_t n_theta,
                    uint64_t n_paths, uint64_t seed, sl7_out out_mode, const sl7_run_opts* o, RunParams& p,
@@ -289,7 +329,7 @@ sl7_status prepare(sl7_ctx c, double Y0, double dt, int32_t n_steps, const doubl
       if (!c->has_net) return fail(c, SL7_ESTATE, "ANN mode before sl7_load_weights");
       const int d_in = c->dims[0];
       if (n_theta != d_in - 2) return fail(c, SL7_EINVAL, "n_theta must equal layer_dims[0] - 2");
-      if (o->prec != SL7_PREC_FP32)
+      if (o->prec != SL7_PREC_FP32 && o->prec != SL7_PREC_BF16)
         return fail(c, SL7_EUNSUPPORTED, "precision mode %d not available in this build", (int)o->prec);
       const int H1 = c->dims[1];
       // features f = (Y, dt, theta...); normalised f' = (f - in_shift) / in_scale
@@ -348,7 +388,9 @@ sl7_status run(sl7_ctx c, RunParams& p, const sl7_run_opts* o, float* d_out, dou
     const int e = launch_zero_stats(d_stats, sl7_stats_elems(o->n_bins), o->stream);
     if (e) return cuda_fail(c, (cudaError_t)e, "zero stats");
   }
-  const int e = launch_step_kernel(p, (int)o->prec, o->stream, c->num_sms);
+  const int e = (p.colloc == kAnn && o->prec == SL7_PREC_BF16)
+                    ? launch_tc_kernel(p, c->tcp, o->stream, c->num_sms)
+                    : launch_step_kernel(p, (int)o->prec, o->stream, c->num_sms);
   if (e) return cuda_fail(c, (cudaError_t)e, "step kernel launch");
   return SL7_OK;
 }
@@ -488,6 +530,8 @@ sl7_status sl7_load_weights(sl7_ctx c, const void* blob, size_t nbytes) {
   if (!g.ok) return fail(c, SL7_ECUDA, "cudaSetDevice(%d)", c->device);
   sl7_status s = build_f32_image(c);
   if (s != SL7_OK) return s;
+  s = build_tc_image(c);
+  if (s != SL7_OK) return s;
   c->has_net = true;
   return SL7_OK;
 }
@@ -625,6 +669,7 @@ void sl7_destroy(sl7_ctx c) {
   {
     DeviceGuard g(c->device);
     if (c->d_wf32) cudaFree(c->d_wf32);
+    if (c->d_wtc) cudaFree(c->d_wtc);
     if (c->d_out_scratch) cudaFree(c->d_out_scratch);
     if (c->d_stats_scratch) cudaFree(c->d_stats_scratch);
   }

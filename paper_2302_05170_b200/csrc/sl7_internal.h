@@ -70,8 +70,24 @@ SL7_HD inline size_t f32_weight_floats(int H, int HS, int L, int M) {
   return (size_t)(L - 1) * f32_layer_floats(H, HS) + (size_t)M * HS + (size_t)((M + 3) & ~3);
 }
 
+// Tensor-core (tcgen05) kernel extras: fp32 biases of the MMA layers and the bf16 operand image.
+// Image: for each hidden->hidden layer a [64 n][64 k] bf16 tile (8 KB), then the output layer as a
+// [16 n][64 k] tile (2 KB); each tile in the K-major SWIZZLE_128B layout (row n = 128 bytes, the 16-byte
+// chunk c of row n stored at chunk c ^ (n % 8)), weights rounded to bf16 with round-to-nearest-even.
+constexpr int kTcN = 64;       // hidden width on the tensor cores (zero padded)
+constexpr int kTcNOut = 16;    // output width (m padded)
+constexpr int kTcTileBytes = kTcN * kTcN * 2;
+constexpr int kTcOutBytes = kTcNOut * kTcN * 2;
+struct TcParams {
+  float bias[kMaxHidden - 1][kTcN];
+  float bout[kTcNOut];
+  const void* wimg;
+  int n_mma_hidden;   // L - 1
+};
+
 // launchers (sl7_kernels.cu / sl7_tc.cu); return cudaError_t as int
 int launch_step_kernel(const RunParams& p, int prec, void* stream, int num_sms);
+int launch_tc_kernel(const RunParams& p, const TcParams& t, void* stream, int num_sms);
 int launch_philox_u32(uint64_t seed, uint64_t off, uint64_t n, uint32_t block, uint32_t* out, void* stream);
 int launch_normals(uint64_t seed, uint64_t off, uint64_t n, int n_steps, float* out, void* stream);
 int launch_zero_stats(double* stats, size_t n, void* stream);

@@ -271,3 +271,63 @@ def test_host_buffers_equal_device_run(gpu_lib):
     assert np.array_equal(h_out.astype(np.float64), dev)
     np.testing.assert_allclose(h_st, dst, rtol=1e-12)
     assert down == h_out.nbytes + h_st.nbytes and up > 0
+
+
+# ------------------------------------------------------------------------------ ANN-BF16 (tcgen05)
+
+@pytest.mark.parametrize("name,gen", ANN_CASES, ids=[c[0] for c in ANN_CASES])
+def test_ann_bf16_tc_teacher_forced(gpu_lib, name, gen):
+    """T-3: tensor-core path within 5e-3 * kappa of the quantisation-aware oracle O6, one step at a time."""
+    sl7 = gpu_lib
+    blob, m, dims, act, theta, y0, n_steps, dt = _ann_case(name, gen)
+    n_paths = 4 * 128 * 3 + 77                       # several tiles per group, a ragged last tile
+    ctx = sl7.Context(m, dims, act)
+    ctx.load_weights(blob)
+    Yd, _ = _run(sl7, ctx, dict(y0=y0, dt=dt, n_steps=n_steps), n_paths, 99, sl7.OUT_FULL, sl7.COLLOC_ANN,
+                 prec=sl7.PREC_BF16, theta=theta)
+    Yd = Yd.reshape(n_steps + 1, n_paths)
+    spec = O.Spec(m, "ann", theta, y0, dt, n_steps, net=O.parse_blob(blob), quant="bf16")
+    Z = O.normals(99, np.arange(n_paths, dtype=np.uint64), n_steps)
+    worst = _teacher_forced(spec, Yd, Z, tol=5e-3)
+    print("bf16 teacher-forced worst |err|/kappa = %.3g" % worst)
+
+
+@pytest.mark.parametrize("name", ["cfg0", "cfg2_ou", "cfg2_cir"])
+def test_ann_bf16_terminal_moments(gpu_lib, name):
+    """T-4: free-running terminal mean and variance over the identical path set within 1e-4 relative
+    of the quantisation-aware oracle (|dmean| <= 1e-4 sd when the mean is ~0)."""
+    sl7 = gpu_lib
+    blob, m, dims, act, theta, y0, n_steps, dt = _ann_case(name, None)
+    w = workloads()[name]
+    n_steps, dt = w.n_steps, w.dt
+    n_paths = 20_000
+    ctx = sl7.Context(m, dims, act)
+    ctx.load_weights(blob)
+    YT, _ = _run(sl7, ctx, dict(y0=y0, dt=dt, n_steps=n_steps), n_paths, w.seed, sl7.OUT_TERMINAL, sl7.COLLOC_ANN,
+                 prec=sl7.PREC_BF16, theta=theta)
+    spec = O.Spec(m, "ann", theta, y0, dt, n_steps, net=O.parse_blob(blob), quant="bf16")
+    Yo, _ = O.simulate(spec, w.seed, np.arange(n_paths, dtype=np.uint64))
+    mo, md = Yo[-1].mean(), YT.mean()
+    vo, vd = Yo[-1].var(), YT.var()
+    sd = np.sqrt(vo)
+    assert abs(md - mo) <= 1e-4 * max(abs(mo), sd if abs(mo) < 1e-3 * sd else abs(mo))
+    assert abs(vd - vo) <= 1e-4 * vo
+    rel = np.abs(YT - Yo[-1]) / np.maximum(np.abs(Yo[-1]), sd)
+    print("%s bf16 free-running per-value: median %.2g p99 %.2g max %.2g" % (name, np.median(rel),
+                                                                           np.quantile(rel, 0.99), rel.max()))
+
+
+def test_ann_bf16_sharding_bitwise(gpu_lib):
+    sl7 = gpu_lib
+    w = workloads()["cfg0"]
+    blob = load_golden_blob(w.blob)
+    ctx = sl7.Context(w.m, list(w.dims), w.act)
+    ctx.load_weights(blob)
+    N = 3 * 512 + 5
+    kw = dict(y0=w.y0, dt=w.dt, n_steps=w.n_steps)
+    full, _ = _run(sl7, ctx, kw, N, w.seed, sl7.OUT_TERMINAL, sl7.COLLOC_ANN, prec=sl7.PREC_BF16, theta=())
+    parts = []
+    for lo, n in [(0, 700), (700, 129), (829, N - 829)]:
+        o, _ = _run(sl7, ctx, kw, n, w.seed, sl7.OUT_TERMINAL, sl7.COLLOC_ANN, prec=sl7.PREC_BF16, offset=lo, theta=())
+        parts.append(o)
+    assert np.array_equal(np.concatenate(parts), full)
