@@ -184,8 +184,9 @@ def main():
     prec = {"auto": sl7.PREC_FP32, "fp32": sl7.PREC_FP32, "bf16": sl7.PREC_BF16}[a.prec]
     if a.prec == "auto" and getattr(sl7, "HAS_TC", False):
         prec = sl7.PREC_BF16
+    from paper_2302_05170_b200.dist import allreduce_stats, max_over_ranks, weak_shard
     N = a.paths
-    offset = rank * N
+    offset, _ = weak_shard(N, rank)
     stream = torch.cuda.current_stream()
     dev = torch.device("cuda", local)
     out = torch.empty(N, dtype=torch.float32, device=dev)
@@ -201,13 +202,21 @@ def main():
     ex_opts = opts_for(sl7.COLLOC_EXACT_GBM, sl7.PREC_FP32)
 
     def sweep(opts, colloc, evs=None):
+        # one pass of the hot path for every dt of the sweep; under torchrun the exchange step (one
+        # SUM all-reduce of the fp64 stats vector) is part of the step and inside the timed events
         th = () if colloc == sl7.COLLOC_ANN else W.theta
         for k, ns in enumerate(N_SWEEP):
             if evs is not None:
                 evs[k][0].record(stream)
             ctx.simulate(W.y0, 1.0 / ns, ns, th, N, W.seed, sl7.OUT_TERMINAL, opts, out=out, stats=stats[ns])
             if evs is not None:
+                evs[k][2].record(stream)
+            allreduce_stats(stats[ns])
+            if evs is not None:
                 evs[k][1].record(stream)
+
+    def new_events():
+        return [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in N_SWEEP]
 
     def barrier():
         torch.cuda.synchronize()
@@ -226,26 +235,16 @@ def main():
     barrier()
     for _ in range(a.steps):
         flush.fill_(1.0)                                     # L2 flush (untimed)
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in N_SWEEP]
+        evs = new_events()
         sweep(ann_opts, sl7.COLLOC_ANN, evs)
         torch.cuda.synchronize()
-        ks = [e0.elapsed_time(e1) for e0, e1 in evs]
-        kernel_ms.append(ks)
-        per_step_ms.append(sum(ks))
+        kernel_ms.append([e0.elapsed_time(ek) for e0, _, ek in evs])
+        per_step_ms.append(sum(e0.elapsed_time(e1) for e0, e1, _ in evs))
     barrier()
     clk.stop()
-    step_ms = statistics.mean(per_step_ms)
+    step_ms = max_over_ranks(statistics.mean(per_step_ms), dev)
     path_steps = N * sum(N_SWEEP)
-    if dist:
-        t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        step_ms = float(t.item())
     value = world * path_steps / (step_ms * 1e-3)
-
-    # all-reduce of the statistics (the only collective of the path)
-    if dist:
-        for ns in N_SWEEP:
-            dist.all_reduce(stats[ns])
     summ = {}
     for ns in N_SWEEP:
         s = sl7.stats_summary(stats[ns].cpu().numpy(), ann_opts, q_levels=[0.01, 0.5, 0.99])
@@ -255,10 +254,11 @@ def main():
     ex_ms = []
     for _ in range(max(1, a.steps)):
         flush.fill_(1.0)
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in N_SWEEP]
+        evs = new_events()
         sweep(ex_opts, sl7.COLLOC_EXACT_GBM, evs)
         torch.cuda.synchronize()
-        ex_ms.append(sum(e0.elapsed_time(e1) for e0, e1 in evs))
+        ex_ms.append(sum(e0.elapsed_time(e1) for e0, e1, _ in evs))
+    ex_step = max_over_ranks(statistics.mean(ex_ms), dev)
     ex_stats = {}
     for ns in N_SWEEP:
         ex_stats[ns] = sl7.stats_summary(stats[ns].cpu().numpy(), ex_opts)["strong_err"]
@@ -278,11 +278,7 @@ def main():
         el = time.perf_counter() - t0
         if it:
             e2e_ms.append(el * 1e3)
-    e2e_step = statistics.mean(e2e_ms)
-    if dist:
-        t = torch.tensor([e2e_step], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_step = float(t.item())
+    e2e_step = max_over_ranks(statistics.mean(e2e_ms), dev)
 
     if rank != 0:
         dist.destroy_process_group()
@@ -329,7 +325,7 @@ def main():
                     "d2h_bytes_per_step": down_b, "ms_per_step": e2e_step},
             "modes": {"ann": {"path_steps_per_s": value, "strong_err_by_n": {ns: summ[ns]["strong_err"] for ns in N_SWEEP},
                               "terminal_mean_n64": summ[64]["mean"], "terminal_var_n64": summ[64]["var"]},
-                      "exact_gbm": {"path_steps_per_s": world * path_steps / (statistics.mean(ex_ms) * 1e-3),
+                      "exact_gbm": {"path_steps_per_s": world * path_steps / (ex_step * 1e-3),
                                     "strong_err_by_n": ex_stats}},
             "kernel_ms_by_n": {ns: statistics.mean(k[i] for k in kernel_ms) for i, ns in enumerate(N_SWEEP)}}
     if not a.no_cpu_baseline and world == 1:
