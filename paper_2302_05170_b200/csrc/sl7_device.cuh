@@ -63,6 +63,38 @@ __device__ __forceinline__ void normals4(uint32_t key0, uint32_t key1, uint64_t 
 // node to ~2^-48 relative.  Prefix/suffix products: 3(M-1) FMUL + 2M FFMA/FADD + 1 rcp.
 // MR = compile-time slot count; m_rt < MR means runtime m with padded slots (w = 0, d = 1).
 // ------------------------------------------------------------------------------------------------
+// Split form for kernels that overlap the basis with other latency: gm_basis fills
+// l_j = w_j prod_{k != j}(Z - x_k) and returns sum_j l_j; gm_combine returns sum_j y_j l_j / sum_j l_j.
+template <int MR, bool RUNTIME_M = false>
+__device__ __forceinline__ float gm_basis(const RunParams& p, float Z, float (&lb)[MR]) {
+  float d[MR];
+#pragma unroll
+  for (int k = 0; k < MR; ++k) {
+    const float dk = (Z - p.xhi[k]) - p.xlo[k];
+    d[k] = (RUNTIME_M && k >= p.m) ? 1.0f : dk;
+  }
+  float pre[MR];
+  pre[0] = 1.0f;
+#pragma unroll
+  for (int k = 1; k < MR; ++k) pre[k] = pre[k - 1] * d[k - 1];
+  float suf = 1.0f, den = 0.0f;
+#pragma unroll
+  for (int j = MR - 1; j >= 0; --j) {
+    lb[j] = p.w[j] * (pre[j] * suf);
+    den += lb[j];
+    suf *= d[j];
+  }
+  return den;
+}
+
+template <int MR>
+__device__ __forceinline__ float gm_combine(const float (&lb)[MR], float den, const float (&y)[MR]) {
+  float num = 0.0f;
+#pragma unroll
+  for (int j = MR - 1; j >= 0; --j) num = fmaf(lb[j], y[j], num);
+  return __fdividef(num, den);
+}
+
 template <int MR, bool RUNTIME_M = false>
 __device__ __forceinline__ float gm_eval(const RunParams& p, float Z, const float (&y)[MR]) {
   float d[MR];

@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -245,6 +246,23 @@ sl7_status build_tc_image(sl7_ctx c) {
       if (l < L) c->tcp.bias[l - 1][n] = c->b[l][n];
       else c->tcp.bout[n] = c->b[l][n];
     }
+    if (c->width == 50) {
+      // the width-50 kernel (FOLD) feeds A = 1.0 in K columns 50..52: the bias enters the fp32
+      // accumulation as three bf16 terms whose sum reproduces the fp32 bias (hi + mid + lo)
+      for (int n = 0; n < fo; ++n) {
+        const float b = c->b[l][n];
+        auto bf = [](float v) {
+          uint32_t u = (uint32_t)f32_to_bf16_rne(v) << 16;
+          float f;
+          std::memcpy(&f, &u, 4);
+          return f;
+        };
+        const float hi = bf(b), mid = bf(b - hi), lo = bf(b - hi - mid);
+        put(off, n, 50, hi);
+        put(off, n, 51, mid);
+        put(off, n, 52, lo);
+      }
+    }
   }
   c->tcp.n_mma_hidden = nL;
   if (c->d_wtc) cudaFree(c->d_wtc);
@@ -346,6 +364,8 @@ sl7_status prepare(sl7_ctx c, double Y0, double dt, int32_t n_steps, const doubl
         for (int q = 1; q < d_in; ++q) bias += (double)Wr[q] * (f[q] - sh[q]) / sc[q];
         p.l1w[k] = (float)((double)Wr[0] / sc[0]);
         p.l1b[k] = (float)bias;
+        p.l1w_d[k] = (double)Wr[0] / sc[0];
+        p.l1b_d[k] = bias;
       }
       for (int j = 0; j < kMaxM; ++j) {
         p.out_scale[j] = (j < c->m && c->has_norm) ? c->out_scale[j] : (j < c->m ? 1.0f : 0.0f);
@@ -388,9 +408,24 @@ sl7_status run(sl7_ctx c, RunParams& p, const sl7_run_opts* o, float* d_out, dou
     const int e = launch_zero_stats(d_stats, sl7_stats_elems(o->n_bins), o->stream);
     if (e) return cuda_fail(c, (cudaError_t)e, "zero stats");
   }
-  const int e = (p.colloc == kAnn && o->prec == SL7_PREC_BF16)
-                    ? launch_tc_kernel(p, c->tcp, o->stream, c->num_sms)
-                    : launch_step_kernel(p, (int)o->prec, o->stream, c->num_sms);
+  int e;
+  if (p.colloc == kAnn && o->prec == SL7_PREC_BF16) {
+    // per-run part of the TC parameters: layer 1 folded (as in RunParams) and pre-scaled in double
+    TcParams t = c->tcp;
+    const double sc = (c->act == SL7_ACT_TANH) ? 2.0 / std::log(2.0) : 1.0;
+    t.act_scale = (float)sc;
+    for (int k = 0; k < kTcN; ++k) {
+      t.l1w[k] = (float)(p.l1w_d[k] * sc);
+      t.l1b[k] = (float)(p.l1b_d[k] * sc);
+    }
+    for (int l = 0; l < t.n_mma_hidden; ++l)
+      for (int k = 0; k < kTcN; ++k) t.bias[l][k] = (float)((double)c->tcp.bias[l][k] * sc);
+    const char* v = std::getenv("SL7_TC_VARIANT");
+    t.variant = v ? std::atoi(v) : 0;
+    e = launch_tc_kernel(p, t, o->stream, c->num_sms);
+  } else {
+    e = launch_step_kernel(p, (int)o->prec, o->stream, c->num_sms);
+  }
   if (e) return cuda_fail(c, (cudaError_t)e, "step kernel launch");
   return SL7_OK;
 }

@@ -51,6 +51,7 @@ struct RunParams {
   int n_hidden;          // L
   int width;             // padded hidden width used by the kernel
   float l1w[kMaxW], l1b[kMaxW];
+  double l1w_d[kMaxW], l1b_d[kMaxW];   // host-side double copies (not read by kernels)
   float out_scale[kMaxM], out_shift[kMaxM];
   const float* wdev;     // FP32 kernel: hidden + output weights (layout: WeightLayoutF32)
   const void* wtc;       // TC kernel: packed bf16 operand images (layout: sl7_tc.cu)
@@ -79,10 +80,13 @@ constexpr int kTcNOut = 16;    // output width (m padded)
 constexpr int kTcTileBytes = kTcN * kTcN * 2;
 constexpr int kTcOutBytes = kTcNOut * kTcN * 2;
 struct TcParams {
-  float bias[kMaxHidden - 1][kTcN];
+  float act_scale;                    // tanh: 2 log2(e) (argument of 2^u); softplus: 1
+  float l1w[kTcN], l1b[kTcN];         // layer 1 folded and scaled by act_scale
+  float bias[kMaxHidden - 1][kTcN];   // hidden biases scaled by act_scale
   float bout[kTcNOut];
   const void* wimg;
   int n_mma_hidden;   // L - 1
+  int variant;        // activation variant (experiment hook, SL7_TC_VARIANT)
 };
 
 // launchers (sl7_kernels.cu / sl7_tc.cu); return cudaError_t as int

@@ -27,22 +27,70 @@ namespace sl7 {
 
 namespace {
 constexpr int kGroupThreads = 128;
-constexpr uint32_t kColsPerGroup = 128;
-constexpr uint32_t kAccCol = 0, kOutCol = 64, kACol = 96;
+constexpr uint32_t kColsPerGroup = 96;     // acc fp32 [0,64) (output layer reuses [0,16)), A bf16 [64,96)
+constexpr uint32_t kAccCol = 0, kACol = 64;
 }  // namespace
 
-template <int ACT, int H>
-__device__ __forceinline__ void act_pack_32(const uint32_t (&v)[32], int col0, const float* bias, uint32_t (&pk)[16]) {
-#pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const int c0 = col0 + 2 * k, c1 = c0 + 1;
-    const float a = (c0 < H) ? activate<ACT>(__uint_as_float(v[2 * k]) + bias[c0]) : 0.0f;
-    const float b = (c1 < H) ? activate<ACT>(__uint_as_float(v[2 * k + 1]) + bias[c1]) : 0.0f;
-    pk[k] = tc::pack_bf16x2(a, b);
+// 1/s for s in [1, 2] on the FMA pipe: quadratic seed (rel. error 1.7%) + 2 Newton steps (8e-8).
+// Used to move part of the MUFU load (rcp) onto the FMA pipe (the XU pipe binds).
+__device__ __forceinline__ float rcp12_newton(float s) {
+  float r = fmaf(fmaf(0.30153724f, s, -1.39582404f), s, 2.08733358f);
+  r = fmaf(r, fmaf(-s, r, 1.0f), r);
+  r = fmaf(r, fmaf(-s, r, 1.0f), r);
+  return r;
+}
+
+// Activation of the TC epilogue.  The argument is u = z * scale with scale = 2 log2(e) (tanh) or 1
+// (softplus), folded on the host into layer 1 and into the biases.
+//   tanh, 2 MUFU:      tanh = 1 - 2 / (2^u + 1)          (2^u -> 0 / inf gives -1 / 1 exactly)
+//   tanh, 1 MUFU:      tanh|z| = (1 - e) / (1 + e), e = 2^-|u| in (0,1]: the denominator is in [1,2],
+//                      so its reciprocal is rcp12_newton on the FMA pipe; sign restored by copysign
+//   softplus, 2 MUFU:  max(z, 0) + ln2 log2(1 + 2^(-|z| log2 e))
+// Absolute error <= ~2e-7 in every variant.
+template <int ACT>
+__device__ __forceinline__ float tc_act_u(float u, bool newton) {
+  if constexpr (ACT == SL7_ACT_TANH) {
+    if (newton) {   // compile-time after unrolling
+      const float e = ex2_approx(-fabsf(u));
+      const float r = rcp12_newton(1.0f + e);
+      return copysignf(fmaf(-e, r, r), u);
+    }
+    return fmaf(-2.0f, rcp_approx(ex2_approx(u) + 1.0f), 1.0f);
+  } else {
+    const float e = ex2_approx(fabsf(u) * -1.4426950408889634f);
+    return fmaf(0.69314718055994531f, lg2_approx(1.0f + e), fmaxf(u, 0.0f));
   }
 }
 
-template <int NG, int H, int MR, bool RT_M, int ACT>
+template <int ACT, unsigned NMASK>
+__device__ __forceinline__ bool use_newton(int c) {
+  return ACT == SL7_ACT_TANH && ((NMASK >> (c & 7)) & 1u);
+}
+
+// FOLD: the hidden bias rides in the MMA (K columns H, H+1, H+2 of A hold 1.0, the weight tile holds
+// the bias split into three bf16 terms), so u = acc * scale.  Otherwise u = acc * scale + bias_scaled.
+template <int ACT, int H, unsigned NMASK, bool FOLD>
+__device__ __forceinline__ void act_pack_32(const uint32_t (&v)[32], int col0, float scale, const float* bs,
+                                            uint32_t (&pk)[16]) {
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    float h[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int c = col0 + 2 * k + q;
+      if (c < H) {
+        const float acc = __uint_as_float(v[2 * k + q]);
+        const float u = FOLD ? acc * scale : fmaf(acc, scale, bs[c]);
+        h[q] = tc_act_u<ACT>(u, use_newton<ACT, NMASK>(c));
+      } else {
+        h[q] = (FOLD && c < H + 3) ? 1.0f : 0.0f;
+      }
+    }
+    pk[k] = tc::pack_bf16x2(h[0], h[1]);
+  }
+}
+
+template <int NG, int H, int MR, bool RT_M, int ACT, unsigned NMASK>
 __global__ void __launch_bounds__(NG * kGroupThreads, 1)
     ann_tc_step_kernel(const __grid_constant__ RunParams p, const __grid_constant__ TcParams t) {
   extern __shared__ uint8_t smem_raw[];
@@ -54,6 +102,8 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
   const int g = warp >> 2;                 // tile group
   const int wq = warp & 3;                 // warp within the group -> TMEM lanes [32 wq, 32 wq + 32)
   const int tid_g = threadIdx.x & (kGroupThreads - 1);
+  constexpr uint32_t kTmemCols = NG * kColsPerGroup <= 256 ? 256u : 512u;
+  constexpr bool FOLD = (H <= kTcN - 3);   // biases ride in spare K columns (host image must match)
 
   // ---- one-time CTA setup: weights -> smem (1024-aligned for the 128B swizzle), barriers, TMEM
   const uint32_t sbase = (tc::smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -73,14 +123,14 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
     for (int k = 0; k < NG; ++k) tc::mbar_init(&mbar[k], 1);
     tc::fence_mbar_init();
   }
-  if (warp == 0) tc::tmem_alloc(&tmem_base_sh, NG <= 2 ? 256u : 512u);
+  if (warp == 0) tc::tmem_alloc(&tmem_base_sh, kTmemCols);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tbase = tmem_base_sh;
   const uint32_t gcol = tbase + (uint32_t)g * kColsPerGroup;
   const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-  const uint32_t acc_t = gcol + kAccCol, out_t = gcol + kOutCol, a_t = gcol + kACol;
+  const uint32_t acc_t = gcol + kAccCol, a_t = gcol + kACol;
   constexpr uint32_t idesc_h = tc::idesc_bf16_f32(128, kTcN);
   constexpr uint32_t idesc_o = tc::idesc_bf16_f32(128, kTcNOut);
   uint64_t* bar = &mbar[g];
@@ -102,21 +152,27 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
       const float Z = z0;
       z0 = z1; z1 = z2; z2 = z3;
 
-      // ---- layer 1 (fp32) -> A operand in TMEM
-      {
-        uint32_t pk[32];
+      // ---- layer 1 (fp32, rank 1 in Y) -> A operand in TMEM, two 32-unit halves
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          const int c0 = 2 * k, c1 = 2 * k + 1;
-          const float a = (c0 < H) ? activate<ACT>(fmaf(p.l1w[c0], Y, p.l1b[c0])) : 0.0f;
-          const float b = (c1 < H) ? activate<ACT>(fmaf(p.l1w[c1], Y, p.l1b[c1])) : 0.0f;
-          pk[k] = tc::pack_bf16x2(a, b);
+      for (int half = 0; half < 2; ++half) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          float h[2];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int c = 32 * half + 2 * k + q;
+            h[q] = (c < H) ? tc_act_u<ACT>(fmaf(Y, t.l1w[c], t.l1b[c]), use_newton<ACT, NMASK>(c))
+                           : ((FOLD && c < H + 3) ? 1.0f : 0.0f);
+          }
+          pk[k] = tc::pack_bf16x2(h[0], h[1]);
         }
-        tc::tmem_st_32x32b_x32(a_t + lane_off, pk);
-        tc::wait_st();
+        tc::tmem_st_32x32b_x16(a_t + lane_off + 16u * half, pk);
       }
-      // ---- layers 2..L+1 on the tensor cores
-      float y[MR];
+      tc::wait_st();
+      // ---- layers 2..L+1 on the tensor cores; the Lagrange basis at Z (independent of the MLP)
+      //      is computed while the first MMA runs
+      float lb[MR], den = 1.0f, y[MR];
       for (int l = 0; l <= nL; ++l) {
         const bool last = (l == nL);
         tc::fence_before();
@@ -124,51 +180,38 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
         if (tid_g == 0) {
           tc::fence_after();
           const uint64_t bdesc = tc::smem_desc_sw128(sbase + (uint32_t)l * kTcTileBytes);
-          const uint32_t d = last ? out_t : acc_t;
           const uint32_t id = last ? idesc_o : idesc_h;
 #pragma unroll
           for (int k = 0; k < kTcN / 16; ++k)   // K = 64 = 4 x 16; +32 bytes per K step inside the swizzle atom
-            tc::mma_bf16_ts(d, a_t + 8u * k, bdesc + 2u * k, id, k > 0 ? 1u : 0u);
+            tc::mma_bf16_ts(acc_t, a_t + 8u * k, bdesc + 2u * k, id, k > 0 ? 1u : 0u);
           tc::mma_commit(bar);
         }
+        if (l == 0) den = gm_basis<MR, RT_M>(p, Z, lb);
         tc::mbar_wait(bar, phase);
         phase ^= 1u;
         tc::fence_after();
         if (!last) {
-          uint32_t pk[32];
-          {
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            uint32_t pk[16];
             uint32_t v[32];
-            tc::tmem_ld_32x32b_x32(acc_t + lane_off, v);
+            tc::tmem_ld_32x32b_x32(acc_t + lane_off + 32u * half, v);
             tc::wait_ld();
-            uint32_t h[16];
-            act_pack_32<ACT, H>(v, 0, t.bias[l], h);
-#pragma unroll
-            for (int k = 0; k < 16; ++k) pk[k] = h[k];
+            act_pack_32<ACT, H, NMASK, FOLD>(v, 32 * half, t.act_scale, t.bias[l], pk);
+            tc::tmem_st_32x32b_x16(a_t + lane_off + 16u * half, pk);
           }
-          if (H > 32) {
-            uint32_t v[32];
-            tc::tmem_ld_32x32b_x32(acc_t + lane_off + 32, v);
-            tc::wait_ld();
-            uint32_t h[16];
-            act_pack_32<ACT, H>(v, 32, t.bias[l], h);
-#pragma unroll
-            for (int k = 0; k < 16; ++k) pk[16 + k] = h[k];
-          } else {
-#pragma unroll
-            for (int k = 0; k < 16; ++k) pk[16 + k] = 0u;
-          }
-          tc::tmem_st_32x32b_x32(a_t + lane_off, pk);
           tc::wait_st();
         } else {
           uint32_t v[16];
-          tc::tmem_ld_32x32b_x16(out_t + lane_off, v);
+          tc::tmem_ld_32x32b_x16(acc_t + lane_off, v);
           tc::wait_ld();
 #pragma unroll
-          for (int j = 0; j < MR; ++j) y[j] = fmaf(__uint_as_float(v[j]) + t.bout[j], p.out_scale[j], p.out_shift[j]);
+          for (int j = 0; j < MR; ++j)
+            y[j] = fmaf(FOLD ? __uint_as_float(v[j]) : __uint_as_float(v[j]) + t.bout[j], p.out_scale[j], p.out_shift[j]);
         }
       }
       // ---- steps 5-6: Y_{i+1} = g_m(X_hat)
-      Y = gm_eval<MR, RT_M>(p, Z, y);
+      Y = gm_combine<MR>(lb, den, y);
       ref_step(rs, p, Z);
       if (valid && p.out_mode == kFull) p.out[(uint64_t)(i + 1) * p.n_paths + q] = Y;
     }
@@ -180,14 +223,14 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
   if (p.has_stats) stat_flush(acc, p, hist, red);
   tc::fence_before();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(tbase, NG <= 2 ? 256u : 512u);
+  if (warp == 0) tc::tmem_dealloc(tbase, kTmemCols);
 }
 
 namespace {
 
-template <int NG, int H, int MR, bool RT, int ACT>
+template <int NG, int H, int MR, bool RT, int ACT, unsigned NMASK = 0u>
 cudaError_t launch_tc_t(const RunParams& p, const TcParams& t, cudaStream_t st, int num_sms) {
-  auto kernel = ann_tc_step_kernel<NG, H, MR, RT, ACT>;
+  auto kernel = ann_tc_step_kernel<NG, H, MR, RT, ACT, NMASK>;
   const size_t hist = (p.has_stats && p.n_bins > 0) ? sizeof(uint32_t) * (size_t)(p.n_bins + 2) : 0;
   const size_t smem = 1024 + (size_t)t.n_mma_hidden * kTcTileBytes + kTcOutBytes + hist;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -199,12 +242,24 @@ cudaError_t launch_tc_t(const RunParams& p, const TcParams& t, cudaStream_t st, 
   return cudaGetLastError();
 }
 
+// Tile groups per CTA and the split of tanh units between the MUFU reciprocal and the FMA-pipe
+// reciprocal (NMASK bit (unit % 8)), chosen by measurement on B200 (cfg1, 4 groups,
+// half of the units on the FMA pipe: 1.45e10 path-steps/s vs 1.30e10 all-MUFU).
+constexpr int kTcGroups = 4;
+constexpr unsigned kTanhNewtonMask = 0x55u;
+
 template <int ACT>
 cudaError_t launch_tc_act(const RunParams& p, const TcParams& t, cudaStream_t st, int num_sms) {
-  constexpr int NG = 4;
-  if (p.width == 50 && p.m == 5) return launch_tc_t<NG, 50, 5, false, ACT>(p, t, st, num_sms);
-  if (p.width == 50 && p.m == 7) return launch_tc_t<NG, 50, 7, false, ACT>(p, t, st, num_sms);
-  return launch_tc_t<NG, 64, kMaxM, true, ACT>(p, t, st, num_sms);
+  constexpr int NG = kTcGroups;
+  constexpr unsigned NM = (ACT == SL7_ACT_TANH) ? kTanhNewtonMask : 0u;
+  if (p.width == 50 && p.m == 5) return launch_tc_t<NG, 50, 5, false, ACT, NM>(p, t, st, num_sms);
+  if (p.width == 50 && p.m == 7) {
+    if constexpr (ACT == SL7_ACT_TANH) {
+      if (t.variant == 1) return launch_tc_t<NG, 50, 7, false, ACT, 0x00u>(p, t, st, num_sms);  // all-MUFU (A/B runs)
+    }
+    return launch_tc_t<NG, 50, 7, false, ACT, NM>(p, t, st, num_sms);
+  }
+  return launch_tc_t<NG, 64, kMaxM, true, ACT, NM>(p, t, st, num_sms);
 }
 
 }  // namespace
