@@ -1,0 +1,146 @@
+"""Per-config measurements beyond bench.py's headline (BASELINE.json configs[2] and [3]), one JSON
+line per (config, mode).  Same timing discipline as bench.py: warm-up, L2 flush before each timed
+launch, CUDA events on the launch stream, NVML clocks sampled during the timed region.
+
+  python bench_configs.py [--config cfg2|cfg3|all] [--steps K] [--warmup W]
+
+cfg2: OU (Ybar=0, lam=1, sigma=0.5, Y0=1) and CIR (kappa=1, Ybar=0.1, sigma=0.3, Y0=0.1), T=2, 16 steps,
+      m=7, [5,50,50,50,50,7] softplus (theta as network input), 1e8 paths, STATS (moments + 4096-bin
+      histogram).  Modes: ANN-BF16 (tcgen05), ANN-FP32, exact OU (general / specialised).
+cfg3: GBM, T=1, 64 steps, m=5, 2e8 paths, FULL step-major path tensor (65 x 2e8 fp32 = 52 GB in HBM).
+      Modes: exact GBM with fast normals + closed-form g_m (HBM-store-bound), exact GBM general,
+      ANN-BF16 (tcgen05).  Roofline: bound "hbm", algorithmic bytes = 4 (n+1) N_P per launch.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from bench import ClockSampler, measured_peaks  # noqa: E402
+
+UNIT = "path-steps/s"
+
+
+def timed_launches(fn, steps, warmup, flush, stream):
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(steps):
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    return statistics.mean(ms), min(ms)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="all", choices=["cfg2", "cfg3", "all"])
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--cfg3-paths", type=int, default=200_000_000)
+    ap.add_argument("--cfg2-paths", type=int, default=100_000_000)
+    a = ap.parse_args()
+
+    import torch
+    import paper_2302_05170_b200 as sl7
+    from sl7_inputs import load_golden_blob, workloads
+    sl7.load_library()
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty((512 << 20) // 4, dtype=torch.float32, device=dev)
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs", 6454.3)
+    sm_max = peaks.get("sm_max_mhz", 1965.0)
+    n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    Wl = workloads()
+
+    def emit(d):
+        print(json.dumps(d), flush=True)
+
+    if a.config in ("cfg3", "all"):
+        w = Wl["cfg3"]
+        N, n = a.cfg3_paths, w.n_steps
+        out = torch.empty((n + 1) * N, dtype=torch.float32, device=dev)
+        bytes_per_launch = 4 * (n + 1) * N
+        ctx_ex = sl7.Context(w.m, device=0)
+        ctx_ann = sl7.Context(w.m, list(w.dims), w.act, device=0)
+        ctx_ann.load_weights(load_golden_blob(w.blob))
+        modes = [("exact_gbm_fast_specialized", ctx_ex, sl7.COLLOC_EXACT_GBM, sl7.PREC_FP32,
+                  sl7.FLAG_FAST_NORMALS | sl7.FLAG_SPECIALIZED, w.theta),
+                 ("exact_gbm_general", ctx_ex, sl7.COLLOC_EXACT_GBM, sl7.PREC_FP32, 0, w.theta),
+                 ("ann_bf16_tcgen05", ctx_ann, sl7.COLLOC_ANN, sl7.PREC_BF16, 0, ())]
+        for label, ctx, colloc, prec, flags, theta in modes:
+            opts = sl7.make_opts(prec=prec, colloc=colloc, stream=stream, flags=flags)
+            fn = (lambda ctx=ctx, theta=theta, opts=opts:
+                  ctx.simulate(w.y0, w.dt, n, theta, N, w.seed, sl7.OUT_FULL, opts, out=out))
+            clk = ClockSampler(0)
+            clk.start()
+            ms, ms_min = timed_launches(fn, a.steps, a.warmup, flush, stream)
+            clk.stop()
+            gbs = bytes_per_launch / (ms * 1e-3) / 1e9
+            emit({"config": "cfg3", "mode": label, "metric": "7L path-steps/sec (device-timed)",
+                  "value": N * n / (ms * 1e-3), "unit": UNIT, "ms_per_launch": ms, "ms_min": ms_min,
+                  "paths": N, "n_steps": n, "m": w.m, "output": "FULL step-major [65][N] fp32 (%.1f GB)" % (bytes_per_launch / 1e9),
+                  "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                               "traffic": None, "algorithmic": "4 B per path-step + row 0 (4 (n+1) N_P per launch)",
+                               "peak_basis": "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"},
+                  "clocks": clk.summary()})
+        del out
+        torch.cuda.empty_cache()
+
+    if a.config in ("cfg2", "all"):
+        N = a.cfg2_paths
+        stats = torch.zeros(sl7.stats_elems(4096), dtype=torch.float64, device=dev)
+        for key in ("cfg2_ou", "cfg2_cir"):
+            w = Wl[key]
+            ctx = sl7.Context(w.m, list(w.dims), w.act, device=0)
+            ctx.load_weights(load_golden_blob(w.blob))
+            lo, hi = (-3.0, 3.0) if w.process == "ou" else (0.0, 0.6)
+            modes = [("ann_bf16_tcgen05", ctx, sl7.COLLOC_ANN, sl7.PREC_BF16, 0, w.theta, N),
+                     ("ann_fp32", ctx, sl7.COLLOC_ANN, sl7.PREC_FP32, 0, w.theta, N // 10)]
+            if w.process == "ou":
+                ex = sl7.Context(w.m, device=0)
+                modes += [("exact_ou_general", ex, sl7.COLLOC_EXACT_OU, sl7.PREC_FP32, 0, w.theta, N),
+                          ("exact_ou_fast_specialized", ex, sl7.COLLOC_EXACT_OU, sl7.PREC_FP32,
+                           sl7.FLAG_FAST_NORMALS | sl7.FLAG_SPECIALIZED, w.theta, N)]
+            for label, c, colloc, prec, flags, theta, n_paths in modes:
+                ref = sl7.REF_OU if w.process == "ou" else sl7.REF_NONE
+                opts = sl7.make_opts(prec=prec, colloc=colloc, stream=stream, flags=flags, n_bins=4096,
+                                     hist_lo=lo, hist_hi=hi, shift=w.y0, ref=ref, ref_theta=w.theta)
+                fn = (lambda c=c, theta=theta, opts=opts, n_paths=n_paths:
+                      c.simulate(w.y0, w.dt, w.n_steps, theta, n_paths, w.seed, sl7.OUT_STATS, opts, stats=stats))
+                clk = ClockSampler(0)
+                clk.start()
+                ms, ms_min = timed_launches(fn, a.steps, a.warmup, flush, stream)
+                clk.stop()
+                s = sl7.stats_summary(stats.cpu().numpy(), opts, q_levels=[0.01, 0.5, 0.99])
+                rate = n_paths * w.n_steps / (ms * 1e-3)
+                line = {"config": key, "mode": label, "metric": "7L path-steps/sec (device-timed)", "value": rate,
+                        "unit": UNIT, "ms_per_launch": ms, "paths": n_paths, "n_steps": w.n_steps, "m": w.m,
+                        "terminal": {k: s[k] for k in ("mean", "var", "skew", "exkurt", "strong_err")},
+                        "quantiles_1_50_99": s["quantiles"], "clocks": clk.summary()}
+                if colloc == sl7.COLLOC_ANN and prec == sl7.PREC_BF16:
+                    trans = sum(w.dims[1:-1])
+                    ach = trans * rate / 1e12
+                    pk = n_sms * 16 * sm_max * 1e6 / 1e12
+                    line["roofline"] = {"bound": "alu", "pipe": "XU (MUFU)", "achieved": ach, "peak": pk,
+                                        "unit": "Top/s", "frac": ach / pk,
+                                        "algorithmic": "%d softplus activations per path-step" % trans}
+                emit(line)
+
+
+if __name__ == "__main__":
+    main()

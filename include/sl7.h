@@ -100,7 +100,18 @@ typedef struct {
   int32_t accumulate;       /* 0: zero d_stats first; 1: add into it (chunked / resumed runs) */
   sl7_ref ref;              /* strong-error reference (SL7_REF_NONE: E1 = E2 = 0) */
   double ref_theta[3];
+  uint32_t flags;           /* SL7_FLAG_* below; 0 = defaults */
 } sl7_run_opts;
+
+/* opts->flags (exact-collocation modes only; ignored otherwise):
+ *  SL7_FLAG_FAST_NORMALS : Box-Muller with MUFU lg2 (exact series for u -> 1) and a polynomial sincos
+ *                          reduced exactly in revolutions: ~3x fewer instructions, |X_hat - X| <= ~1e-6.
+ *  SL7_FLAG_SPECIALIZED  : evaluate g_m in closed form for the linear structure of the exact points:
+ *                          GBM y_j = Y c_j  =>  g_m(Z) = Y Q(Z), Q the degree-(m-1) interpolant of c_j
+ *                          in monomial form (Horner; m <= 8); OU y_j = mean + std x_j  =>  g_m(Z) =
+ *                          mean + std Z (linear reproduction).  Same interpolant, fewer operations. */
+#define SL7_FLAG_FAST_NORMALS 1u
+#define SL7_FLAG_SPECIALIZED 2u
 
 /* Summary computed on the host from a (possibly all-reduced) stats vector. */
 typedef struct {
@@ -175,9 +186,10 @@ sl7_status sl7_philox_u32(uint64_t seed, uint64_t path_offset, uint64_t n_paths,
 
 /* The normals the path generator consumes: d_out[i * n_paths + q] = X_hat of path
  * (path_offset + q) at step i, i = 0..n_steps-1, computed by the same device code as the step
- * kernels. */
+ * kernels.  flags: 0 = libm Box-Muller (ANN kernels and default exact kernels), SL7_FLAG_FAST_NORMALS
+ * = the fast variant the exact kernels use under that flag. */
 sl7_status sl7_normals(uint64_t seed, uint64_t path_offset, uint64_t n_paths, int32_t n_steps,
-                       float* d_out, void* stream);
+                       uint32_t flags, float* d_out, void* stream);
 
 /* Host setup introspection (no device needed): the context-independent grid of m nodes in
  * double (x[m], ascending) and barycentric weights w[m] = 1 / prod_{k != j}(x_j - x_k). */

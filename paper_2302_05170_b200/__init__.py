@@ -33,7 +33,11 @@ class sl7_run_opts(ctypes.Structure):
     _fields_ = [("prec", ctypes.c_int), ("colloc", ctypes.c_int), ("path_offset", ctypes.c_uint64),
                 ("stream", ctypes.c_void_p), ("hist_lo", ctypes.c_double), ("hist_hi", ctypes.c_double),
                 ("shift", ctypes.c_double), ("n_bins", ctypes.c_int32), ("accumulate", ctypes.c_int32),
-                ("ref", ctypes.c_int), ("ref_theta", ctypes.c_double * 3)]
+                ("ref", ctypes.c_int), ("ref_theta", ctypes.c_double * 3), ("flags", ctypes.c_uint32)]
+
+
+FLAG_FAST_NORMALS = 1
+FLAG_SPECIALIZED = 2
 
 
 class sl7_summary(ctypes.Structure):
@@ -78,7 +82,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                     c.POINTER(sl7_run_opts), fp, fp, c.POINTER(u64), c.POINTER(u64)]
     L.sl7_stats.argtypes = [dp, c.POINTER(sl7_run_opts), c.POINTER(sl7_summary)]
     L.sl7_philox_u32.argtypes = [u64, u64, u64, c.c_uint32, vp, vp]
-    L.sl7_normals.argtypes = [u64, u64, u64, i32, vp, vp]
+    L.sl7_normals.argtypes = [u64, u64, u64, i32, c.c_uint32, vp, vp]
     L.sl7_gh_grid.argtypes = [i32, dp, dp]
     L.sl7_out_elems.argtypes = [i32, u64, c.c_int]
     L.sl7_out_elems.restype = c.c_size_t
@@ -115,9 +119,10 @@ def _stream_ptr(stream):
 
 
 def make_opts(prec=PREC_FP32, colloc=COLLOC_ANN, path_offset=0, stream=None, hist_lo=0.0, hist_hi=0.0,
-              shift=0.0, n_bins=0, accumulate=0, ref=REF_NONE, ref_theta=(0.0, 0.0, 0.0), raw_stream=None):
+              shift=0.0, n_bins=0, accumulate=0, ref=REF_NONE, ref_theta=(0.0, 0.0, 0.0), raw_stream=None,
+              flags=0):
     o = sl7_run_opts()
-    o.prec, o.colloc, o.path_offset = prec, colloc, int(path_offset)
+    o.prec, o.colloc, o.path_offset, o.flags = prec, colloc, int(path_offset), int(flags)
     o.stream = raw_stream if raw_stream is not None else (_stream_ptr(stream) if stream is not False else None)
     o.hist_lo, o.hist_hi, o.shift, o.n_bins, o.accumulate = hist_lo, hist_hi, shift, int(n_bins), int(accumulate)
     o.ref = ref
@@ -166,9 +171,10 @@ def philox_u32(seed, path_offset, n_paths, block, out, stream=None):
     return out
 
 
-def normals(seed, path_offset, n_paths, n_steps, out, stream=None):
+def normals(seed, path_offset, n_paths, n_steps, out, stream=None, flags=0):
     L = load_library()
-    _check(L.sl7_normals(int(seed), int(path_offset), int(n_paths), int(n_steps), _dptr(out), _stream_ptr(stream)))
+    _check(L.sl7_normals(int(seed), int(path_offset), int(n_paths), int(n_steps), int(flags), _dptr(out),
+                         _stream_ptr(stream)))
     return out
 
 

@@ -33,6 +33,21 @@ __device__ __forceinline__ uint4 philox_path_block(uint32_t key0, uint32_t key1,
   return philox4x32_10(make_uint4(block, 0u, (uint32_t)path, (uint32_t)(path >> 32)), make_uint2(key0, key1));
 }
 
+// The same generator with the key schedule precomputed on the host (round keys rk = key + r (W0, W1)
+// live in the kernel-parameter constant bank and feed the LOP3s directly: no per-call key adds).
+__device__ __forceinline__ uint4 philox_path_block_rk(const uint32_t* rk0, const uint32_t* rk1, uint64_t path,
+                                                      uint32_t block) {
+  constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+  uint4 c = make_uint4(block, 0u, (uint32_t)path, (uint32_t)(path >> 32));
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(M0, c.x), lo0 = M0 * c.x;
+    const uint32_t hi1 = __umulhi(M1, c.z), lo1 = M1 * c.z;
+    c = make_uint4(hi1 ^ c.y ^ rk0[r], lo1, hi0 ^ c.w ^ rk1[r], lo0);
+  }
+  return c;
+}
+
 // u = (2 (r >> 9) + 1) 2^-24: exact in fp32, in [2^-24, 1 - 2^-24], never 0 or 1.
 __device__ __forceinline__ float u32_to_unit(uint32_t r) {
   return __uint2float_rn(((r >> 9) << 1) | 1u) * 0x1p-24f;
@@ -49,11 +64,75 @@ __device__ __forceinline__ void box_muller(uint32_t ra, uint32_t rb, float& za, 
   zb = rad * s;
 }
 
+__device__ __forceinline__ float lg2_fast(float x) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// Fast Box-Muller on the MUFU pipe (exact-collocation kernels, where the RNG dominates the cost).
+// -2 ln u: MUFU lg2 has ~2^-22 ABSOLUTE error (measured on B200: relative error 0.86 at u = 1 - 2^-24),
+// so for v = 1 - u < 2^-4 (v exact) the log is the series 2 (v + v^2/2 + v^3/3 + v^4/4 + v^5/5)
+// (truncation <= 1.6e-7 relative); elsewhere lg2 is relatively accurate to <= 3e-7.  The angle is
+// reduced exactly in revolutions: t = u - 1/2 (exact), quadrant q = rint(4t), f = t - q/4 in
+// [-1/8, 1/8] (exact), then minimax polynomials for sin(2 pi f) / cos(2 pi f) (abs. error <= 1e-7) and
+// a quadrant rotation; 2 pi u = 2 pi t + pi flips both signs.  |Z_fast - Z| <= ~3e-7 (1 + |Z|).
+__device__ __forceinline__ void sincos_2pi_rev(float t, float& s, float& c) {
+  const float magic = 12582912.0f;  // 1.5 * 2^23: adding it rounds to an integer in the low mantissa bits
+  const float qm = fmaf(t, 4.0f, magic);
+  const float qf = qm - magic;
+  const float f = fmaf(qf, -0.25f, t);
+  const float f2 = f * f;
+  const float sp = f * fmaf(fmaf(fmaf(-7.524006653e+01f, f2, 8.158812714e+01f), f2, -4.134162903e+01f), f2,
+                            6.283185005e+00f);
+  const float cp = fmaf(fmaf(fmaf(fmaf(5.922040939e+01f, f2, -8.544285583e+01f), f2, 6.493931580e+01f), f2,
+                             -1.973920822e+01f), f2, 1.0f);
+  const int j = __float_as_int(qm) & 3;
+  float S = (j & 1) ? cp : sp, C = (j & 1) ? sp : cp;
+  S = __int_as_float(__float_as_int(S) ^ (((j >> 1) & 1) << 31));
+  C = __int_as_float(__float_as_int(C) ^ ((((j + 1) >> 1) & 1) << 31));
+  s = S;
+  c = C;
+}
+
+__device__ __forceinline__ void box_muller_fast(uint32_t ra, uint32_t rb, float& za, float& zb) {
+  const float ua = u32_to_unit(ra), ub = u32_to_unit(rb);
+  const float v = 1.0f - ua;
+  const float ser = 2.0f * v * fmaf(v, fmaf(v, fmaf(v, fmaf(v, 0.2f, 0.25f), 0.33333333f), 0.5f), 1.0f);
+  const float lg = -1.3862943611198906f * lg2_fast(ua);       // -2 ln2 log2(u)
+  const float t = (v < 0.0625f) ? ser : lg;
+  float rad;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(rad) : "f"(t));
+  float s, c;
+  sincos_2pi_rev(ub - 0.5f, s, c);
+  za = -rad * c;
+  zb = -rad * s;
+}
+
+template <bool FAST = false>
+__device__ __forceinline__ void normals4_rk(const RunParams& p, uint64_t path, uint32_t block, float& z0, float& z1,
+                                            float& z2, float& z3) {
+  const uint4 r = philox_path_block_rk(p.rk0, p.rk1, path, block);
+  if constexpr (FAST) {
+    box_muller_fast(r.x, r.y, z0, z1);
+    box_muller_fast(r.z, r.w, z2, z3);
+  } else {
+    box_muller(r.x, r.y, z0, z1);
+    box_muller(r.z, r.w, z2, z3);
+  }
+}
+
+template <bool FAST = false>
 __device__ __forceinline__ void normals4(uint32_t key0, uint32_t key1, uint64_t path, uint32_t block,
                                          float& z0, float& z1, float& z2, float& z3) {
   const uint4 r = philox_path_block(key0, key1, path, block);
-  box_muller(r.x, r.y, z0, z1);
-  box_muller(r.z, r.w, z2, z3);
+  if constexpr (FAST) {
+    box_muller_fast(r.x, r.y, z0, z1);
+    box_muller_fast(r.z, r.w, z2, z3);
+  } else {
+    box_muller(r.x, r.y, z0, z1);
+    box_muller(r.z, r.w, z2, z3);
+  }
 }
 
 // ------------------------------------------------------------------------------------------------

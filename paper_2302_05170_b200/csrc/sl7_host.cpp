@@ -310,6 +310,10 @@ sl7_status prepare(sl7_ctx c, double Y0, double dt, int32_t n_steps, const doubl
   p.path_offset = o->path_offset;
   p.key0 = (uint32_t)seed;
   p.key1 = (uint32_t)(seed >> 32);
+  for (int r = 0; r < 10; ++r) {   // Philox4x32-10 key schedule: k += (W0, W1) between rounds
+    p.rk0[r] = p.key0 + (uint32_t)r * 0x9E3779B9u;
+    p.rk1[r] = p.key1 + (uint32_t)r * 0xBB67AE85u;
+  }
   p.y0 = (float)Y0;
   p.y0_d = (double)(float)Y0;
   for (int j = 0; j < kMaxM; ++j) {
@@ -327,7 +331,34 @@ sl7_status prepare(sl7_ctx c, double Y0, double dt, int32_t n_steps, const doubl
       if (n_theta != 2) return fail(c, SL7_EINVAL, "EXACT_GBM needs theta = (mu, sigma)");
       const double mu = theta[0], s = theta[1];
       if (s < 0) return fail(c, SL7_EINVAL, "theta: sigma >= 0");
-      for (int j = 0; j < c->m; ++j) p.c[j] = (float)std::exp((mu - 0.5 * s * s) * dt + s * std::sqrt(dt) * c->x[j]);
+      double cj[kMaxM];
+      for (int j = 0; j < c->m; ++j) {
+        cj[j] = std::exp((mu - 0.5 * s * s) * dt + s * std::sqrt(dt) * c->x[j]);
+        p.c[j] = (float)cj[j];
+      }
+      if (o->flags & SL7_FLAG_SPECIALIZED) {
+        if (c->m > 8) return fail(c, SL7_EUNSUPPORTED, "SL7_FLAG_SPECIALIZED needs m <= 8");
+        // monomial coefficients of the interpolant of c_j: solve sum_k q_k x_j^k = c_j (Gauss, pivoting)
+        const int m = c->m;
+        double A[8][9];
+        for (int j = 0; j < m; ++j) {
+          double xp = 1.0;
+          for (int k = 0; k < m; ++k) { A[j][k] = xp; xp *= c->x[j]; }
+          A[j][m] = cj[j];
+        }
+        for (int col = 0; col < m; ++col) {
+          int piv = col;
+          for (int r = col + 1; r < m; ++r)
+            if (std::fabs(A[r][col]) > std::fabs(A[piv][col])) piv = r;
+          for (int k = 0; k <= m; ++k) std::swap(A[col][k], A[piv][k]);
+          for (int r = 0; r < m; ++r) {
+            if (r == col) continue;
+            const double f = A[r][col] / A[col][col];
+            for (int k = col; k <= m; ++k) A[r][k] -= f * A[col][k];
+          }
+        }
+        for (int k = 0; k < 8; ++k) p.q[k] = (k < m) ? (float)(A[k][m] / A[k][k]) : 0.0f;
+      }
       p.colloc = kExactGbm;
       break;
     }
@@ -338,6 +369,7 @@ sl7_status prepare(sl7_ctx c, double Y0, double dt, int32_t n_steps, const doubl
       const double e = std::exp(-lam * dt), sd = ou_std(lam, s, dt);
       p.ou_a = (float)e;
       p.ou_b = (float)(ybar * (1.0 - e));
+      p.ou_s = (float)sd;
       for (int j = 0; j < c->m; ++j) p.c[j] = (float)(sd * c->x[j]);
       p.colloc = kExactOu;
       break;
@@ -381,6 +413,8 @@ sl7_status prepare(sl7_ctx c, double Y0, double dt, int32_t n_steps, const doubl
     default:
       return fail(c, SL7_EINVAL, "colloc");
   }
+  if (o->flags & ~(SL7_FLAG_FAST_NORMALS | SL7_FLAG_SPECIALIZED)) return fail(c, SL7_EINVAL, "flags");
+  p.flags = (p.colloc == kAnn) ? 0u : o->flags;
   p.ref = (int)o->ref;
   if (o->ref == SL7_REF_GBM) {
     const double mu = o->ref_theta[0], s = o->ref_theta[1];
@@ -692,10 +726,12 @@ sl7_status sl7_philox_u32(uint64_t seed, uint64_t off, uint64_t n, uint32_t bloc
   return e ? cuda_fail(nullptr, (cudaError_t)e, "philox kernel") : SL7_OK;
 }
 
-sl7_status sl7_normals(uint64_t seed, uint64_t off, uint64_t n, int32_t n_steps, float* d_out, void* stream) {
+sl7_status sl7_normals(uint64_t seed, uint64_t off, uint64_t n, int32_t n_steps, uint32_t flags, float* d_out,
+                       void* stream) {
   if (!d_out || n == 0 || n_steps < 1) return fail(nullptr, SL7_EINVAL, "d_out/n_paths/n_steps");
   if (off + (n - 1) < off) return fail(nullptr, SL7_EINVAL, "path_offset + n_paths - 1 overflows 2^64");
-  const int e = launch_normals(seed, off, n, n_steps, d_out, stream);
+  if (flags & ~SL7_FLAG_FAST_NORMALS) return fail(nullptr, SL7_EINVAL, "flags");
+  const int e = launch_normals(seed, off, n, n_steps, (flags & SL7_FLAG_FAST_NORMALS) != 0, d_out, stream);
   return e ? cuda_fail(nullptr, (cudaError_t)e, "normals kernel") : SL7_OK;
 }
 

@@ -28,12 +28,18 @@ struct RunParams {
   uint64_t n_paths;
   uint64_t path_offset;  // global id of path 0 of this launch
   uint32_t key0, key1;   // Philox key = (seed_lo, seed_hi)
+  uint32_t rk0[10], rk1[10];   // Philox round keys key + r (W0, W1), r = 0..9
   float y0;
   // ---- interpolation grid (Algorithm I step 5): nodes split x = xhi + xlo, barycentric w ----
   float xhi[kMaxM], xlo[kMaxM], w[kMaxM];
   // ---- exact collocation: GBM y_j = Y*c[j]; OU y_j = ou_a*Y + ou_b + c[j] (c[j] = std*x_j) ----
   float c[kMaxM];
   float ou_a, ou_b;
+  // ---- SL7_FLAG_SPECIALIZED: GBM g_m(Z) = Y * sum_k q[k] Z^k (monomial form, m <= 8);
+  //      OU g_m(Z) = ou_a Y + ou_b + ou_s Z
+  float q[8];
+  float ou_s;
+  uint32_t flags;
   // ---- strong-error reference on the same normals ----
   int ref;               // Ref
   double ref_drift_T;    // GBM: (mu - s^2/2) T
@@ -93,7 +99,7 @@ struct TcParams {
 int launch_step_kernel(const RunParams& p, int prec, void* stream, int num_sms);
 int launch_tc_kernel(const RunParams& p, const TcParams& t, void* stream, int num_sms);
 int launch_philox_u32(uint64_t seed, uint64_t off, uint64_t n, uint32_t block, uint32_t* out, void* stream);
-int launch_normals(uint64_t seed, uint64_t off, uint64_t n, int n_steps, float* out, void* stream);
+int launch_normals(uint64_t seed, uint64_t off, uint64_t n, int n_steps, bool fast, float* out, void* stream);
 int launch_zero_stats(double* stats, size_t n, void* stream);
 
 }  // namespace sl7

@@ -16,7 +16,11 @@ namespace sl7 {
 // ------------------------------------------------------------------------------------------------
 // Exact-collocation step kernel.  y_j = H_j(Y) in closed form, then g_m(Z).
 // ------------------------------------------------------------------------------------------------
-template <int MR, bool RT_M, int COLLOC>
+// SPECIAL (SL7_FLAG_SPECIALIZED): same interpolant through the exact points, evaluated in closed form:
+// GBM g_m(Z) = Y * Q(Z) with Q in monomial form (Horner, MR-1 FFMA); OU g_m(Z) = mean + std * Z.
+// FAST (SL7_FLAG_FAST_NORMALS): MUFU Box-Muller.  With both, a path-step is ~30 instructions and the
+// FULL-output kernel approaches the HBM store roofline (4 B per path-step).
+template <int MR, bool RT_M, int COLLOC, bool FAST = false, bool SPECIAL = false>
 __global__ void __launch_bounds__(256) exact_step_kernel(const __grid_constant__ RunParams p) {
   extern __shared__ uint32_t hist[];
   __shared__ double red[8];
@@ -32,24 +36,102 @@ __global__ void __launch_bounds__(256) exact_step_kernel(const __grid_constant__
     ref_init(rs, p);
     float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
     for (int i = 0; i < p.n_steps; ++i) {
-      if ((i & 3) == 0) normals4(p.key0, p.key1, gp, (uint32_t)(i >> 2), z0, z1, z2, z3);
+      if ((i & 3) == 0) normals4<FAST>(p.key0, p.key1, gp, (uint32_t)(i >> 2), z0, z1, z2, z3);
       const float Z = z0;
       z0 = z1; z1 = z2; z2 = z3;
-      float y[MR];
-      if constexpr (COLLOC == kExactGbm) {
+      if constexpr (SPECIAL) {
+        if constexpr (COLLOC == kExactGbm) {
+          float qz = p.q[MR - 1];
 #pragma unroll
-        for (int j = 0; j < MR; ++j) y[j] = Y * p.c[j];
+          for (int k = MR - 2; k >= 0; --k) qz = fmaf(qz, Z, p.q[k]);
+          Y *= qz;
+        } else {
+          Y = fmaf(p.ou_s, Z, fmaf(p.ou_a, Y, p.ou_b));
+        }
       } else {
-        const float mean = fmaf(p.ou_a, Y, p.ou_b);
+        float y[MR];
+        if constexpr (COLLOC == kExactGbm) {
 #pragma unroll
-        for (int j = 0; j < MR; ++j) y[j] = mean + p.c[j];
+          for (int j = 0; j < MR; ++j) y[j] = Y * p.c[j];
+        } else {
+          const float mean = fmaf(p.ou_a, Y, p.ou_b);
+#pragma unroll
+          for (int j = 0; j < MR; ++j) y[j] = mean + p.c[j];
+        }
+        Y = gm_eval<MR, RT_M>(p, Z, y);
       }
-      Y = gm_eval<MR, RT_M>(p, Z, y);
       ref_step(rs, p, Z);
       if (p.out_mode == kFull) p.out[(uint64_t)(i + 1) * p.n_paths + q] = Y;
     }
     if (p.out_mode == kTerminal) p.out[q] = Y;
     if (p.has_stats) stat_add(acc, p, Y, ref_final(rs, p), hist);
+  }
+  if (p.has_stats) stat_flush(acc, p, hist, red);
+}
+
+// Throughput form of the specialised exact kernel (the HBM-store-bound FULL mode of cfg3): steps are
+// processed in Philox blocks of 4 (no per-step rotation of the buffered normals), the output pointer
+// advances by one row per step, the key schedule comes from the constant bank, and the strong-error
+// reference is compiled in only when requested (REF_ON).
+template <int MR, int COLLOC>
+__device__ __forceinline__ float special_step(const RunParams& p, float Y, float Z) {
+  if constexpr (COLLOC == kExactGbm) {
+    float qz = p.q[MR - 1];
+#pragma unroll
+    for (int k = MR - 2; k >= 0; --k) qz = fmaf(qz, Z, p.q[k]);
+    return Y * qz;
+  } else {
+    return fmaf(p.ou_s, Z, fmaf(p.ou_a, Y, p.ou_b));
+  }
+}
+
+template <int MR, int COLLOC, bool FAST, bool REF_ON>
+__global__ void __launch_bounds__(256) exact_special_kernel(const __grid_constant__ RunParams p) {
+  extern __shared__ uint32_t hist[];
+  __shared__ double red[8];
+  hist_init(p, hist);
+  __syncthreads();
+  StatAcc acc;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const bool full = (p.out_mode == kFull);
+  const int nfull = p.n_steps >> 2, rem = p.n_steps & 3;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < p.n_paths; q += stride) {
+    const uint64_t gp = p.path_offset + q;
+    float Y = p.y0;
+    float* o = p.out + q;
+    if (full) *o = Y;
+    RefState rs;
+    if (REF_ON) ref_init(rs, p);
+    for (int b = 0; b < nfull; ++b) {
+      float z[4];
+      normals4_rk<FAST>(p, gp, (uint32_t)b, z[0], z[1], z[2], z[3]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        Y = special_step<MR, COLLOC>(p, Y, z[k]);
+        if (REF_ON) ref_step(rs, p, z[k]);
+        if (full) {
+          o += p.n_paths;
+          *o = Y;
+        }
+      }
+    }
+    if (rem) {
+      float z[4];
+      normals4_rk<FAST>(p, gp, (uint32_t)nfull, z[0], z[1], z[2], z[3]);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        if (k < rem) {
+          Y = special_step<MR, COLLOC>(p, Y, z[k]);
+          if (REF_ON) ref_step(rs, p, z[k]);
+          if (full) {
+            o += p.n_paths;
+            *o = Y;
+          }
+        }
+      }
+    }
+    if (p.out_mode == kTerminal) p.out[q] = Y;
+    if (p.has_stats) stat_add(acc, p, Y, REF_ON ? ref_final(rs, p) : 0.0, hist);
   }
   if (p.has_stats) stat_flush(acc, p, hist, red);
 }
@@ -150,11 +232,12 @@ __global__ void philox_u32_kernel(uint32_t k0, uint32_t k1, uint64_t off, uint64
   }
 }
 
+template <bool FAST>
 __global__ void normals_kernel(uint32_t k0, uint32_t k1, uint64_t off, uint64_t n, int n_steps, float* out) {
   for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (uint64_t)gridDim.x * blockDim.x) {
     float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
     for (int i = 0; i < n_steps; ++i) {
-      if ((i & 3) == 0) normals4(k0, k1, off + q, (uint32_t)(i >> 2), z0, z1, z2, z3);
+      if ((i & 3) == 0) normals4<FAST>(k0, k1, off + q, (uint32_t)(i >> 2), z0, z1, z2, z3);
       out[(uint64_t)i * n + q] = z0;
       z0 = z1; z1 = z2; z2 = z3;
     }
@@ -192,14 +275,38 @@ size_t hist_bytes(const RunParams& p) {
   return (p.has_stats && p.n_bins > 0) ? sizeof(uint32_t) * (size_t)(p.n_bins + 2) : 0;
 }
 
+template <int COLLOC, bool FAST, bool REF_ON>
+cudaError_t launch_exact_special_r(const RunParams& p, cudaStream_t st, int num_sms, size_t smem) {
+  // OU: the closed form does not depend on m; GBM: Horner of degree m-1 (m <= 8, zero padded)
+  if (COLLOC == kExactOu || (p.m != 5 && p.m != 7))
+    return launch_persistent(exact_special_kernel<8, COLLOC, FAST, REF_ON>, 256, smem, p, st, num_sms);
+  if (p.m == 5) return launch_persistent(exact_special_kernel<5, COLLOC, FAST, REF_ON>, 256, smem, p, st, num_sms);
+  return launch_persistent(exact_special_kernel<7, COLLOC, FAST, REF_ON>, 256, smem, p, st, num_sms);
+}
+
+template <int COLLOC, bool FAST>
+cudaError_t launch_exact_special(const RunParams& p, cudaStream_t st, int num_sms, size_t smem) {
+  return (p.ref != kRefNone && p.has_stats) ? launch_exact_special_r<COLLOC, FAST, true>(p, st, num_sms, smem)
+                                            : launch_exact_special_r<COLLOC, FAST, false>(p, st, num_sms, smem);
+}
+
+template <int COLLOC, bool FAST>
+cudaError_t launch_exact_general(const RunParams& p, cudaStream_t st, int num_sms, size_t smem) {
+  switch (p.m) {
+    case 5: return launch_persistent(exact_step_kernel<5, false, COLLOC, FAST>, 256, smem, p, st, num_sms);
+    case 7: return launch_persistent(exact_step_kernel<7, false, COLLOC, FAST>, 256, smem, p, st, num_sms);
+    default: return launch_persistent(exact_step_kernel<kMaxM, true, COLLOC, FAST>, 256, smem, p, st, num_sms);
+  }
+}
+
 template <int COLLOC>
 cudaError_t launch_exact(const RunParams& p, cudaStream_t st, int num_sms) {
   const size_t smem = hist_bytes(p);
-  switch (p.m) {
-    case 5: return launch_persistent(exact_step_kernel<5, false, COLLOC>, 256, smem, p, st, num_sms);
-    case 7: return launch_persistent(exact_step_kernel<7, false, COLLOC>, 256, smem, p, st, num_sms);
-    default: return launch_persistent(exact_step_kernel<kMaxM, true, COLLOC>, 256, smem, p, st, num_sms);
-  }
+  const bool fast = p.flags & SL7_FLAG_FAST_NORMALS, special = p.flags & SL7_FLAG_SPECIALIZED;
+  if (special) return fast ? launch_exact_special<COLLOC, true>(p, st, num_sms, smem)
+                           : launch_exact_special<COLLOC, false>(p, st, num_sms, smem);
+  return fast ? launch_exact_general<COLLOC, true>(p, st, num_sms, smem)
+              : launch_exact_general<COLLOC, false>(p, st, num_sms, smem);
 }
 
 template <int H, int HS, int MR, bool RT, int ACT>
@@ -238,9 +345,10 @@ int launch_philox_u32(uint64_t seed, uint64_t off, uint64_t n, uint32_t block, u
   return (int)cudaGetLastError();
 }
 
-int launch_normals(uint64_t seed, uint64_t off, uint64_t n, int n_steps, float* out, void* stream) {
+int launch_normals(uint64_t seed, uint64_t off, uint64_t n, int n_steps, bool fast, float* out, void* stream) {
   const unsigned grid = (unsigned)((n + 255) / 256 < 65535 ? (n + 255) / 256 : 65535);
-  normals_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  auto kernel = fast ? normals_kernel<true> : normals_kernel<false>;
+  kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       (uint32_t)seed, (uint32_t)(seed >> 32), off, n, n_steps, out);
   return (int)cudaGetLastError();
 }

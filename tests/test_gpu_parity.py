@@ -27,10 +27,11 @@ def _torch():
 
 
 def _run(sl7, ctx, spec_kw, n_paths, seed, out_mode=None, colloc=None, prec=None, stats=False, n_bins=0,
-         lo=0.0, hi=1.0, shift=0.0, ref=0, ref_theta=(0, 0, 0), offset=0, theta=None):
+         lo=0.0, hi=1.0, shift=0.0, ref=0, ref_theta=(0, 0, 0), offset=0, theta=None, flags=0):
     torch = _torch()
     opts = sl7.make_opts(prec=sl7.PREC_FP32 if prec is None else prec, colloc=colloc, path_offset=offset,
-                         n_bins=n_bins, hist_lo=lo, hist_hi=hi, shift=shift, ref=ref, ref_theta=ref_theta)
+                         n_bins=n_bins, hist_lo=lo, hist_hi=hi, shift=shift, ref=ref, ref_theta=ref_theta,
+                         flags=flags)
     st = torch.zeros(sl7.stats_elems(n_bins), dtype=torch.float64, device="cuda") if stats else None
     out, st = ctx.simulate(spec_kw["y0"], spec_kw["dt"], spec_kw["n_steps"], theta, n_paths, seed, out_mode, opts,
                            stats=st)
@@ -331,3 +332,72 @@ def test_ann_bf16_sharding_bitwise(gpu_lib):
         o, _ = _run(sl7, ctx, kw, n, w.seed, sl7.OUT_TERMINAL, sl7.COLLOC_ANN, prec=sl7.PREC_BF16, offset=lo, theta=())
         parts.append(o)
     assert np.array_equal(np.concatenate(parts), full)
+
+
+# ------------------------------------------------------------- exact modes: fast RNG + closed-form g_m
+
+@pytest.mark.parametrize("colloc,m,theta,n_steps,dt", [
+    ("gbm", 5, (0.05, 0.2), 64, 1 / 64), ("gbm", 7, (0.05, 0.2), 4, 1.0), ("gbm", 8, (0.1, 0.5), 6, 0.5),
+    ("gbm", 3, (0.05, 0.2), 5, 0.3), ("ou", 7, (0.0, 1.0, 0.5), 16, 0.125), ("ou", 5, (0.3, 1e-9, 0.7), 9, 0.25)])
+@pytest.mark.parametrize("flags", [1, 2, 3])
+def test_exact_flags_teacher_forced(gpu_lib, colloc, m, theta, n_steps, dt, flags):
+    """SL7_FLAG_FAST_NORMALS (MUFU Box-Muller, |dZ| <= ~4e-6) and SL7_FLAG_SPECIALIZED (closed-form
+    g_m) keep the fp32 tolerance 1e-5 * kappa against the float64 oracle."""
+    sl7 = gpu_lib
+    torch = _torch()
+    n_paths = 30_000 + 5
+    ctx = sl7.Context(m)
+    code = sl7.COLLOC_EXACT_GBM if colloc == "gbm" else sl7.COLLOC_EXACT_OU
+    opts = sl7.make_opts(prec=sl7.PREC_FP32, colloc=code, flags=flags)
+    out, _ = ctx.simulate(1.0, dt, n_steps, theta, n_paths, 77, sl7.OUT_FULL, opts)
+    torch.cuda.synchronize()
+    Yd = out.double().cpu().numpy().reshape(n_steps + 1, n_paths)
+    spec = O.Spec(m, colloc, theta, 1.0, dt, n_steps)
+    Z = O.normals(77, np.arange(n_paths, dtype=np.uint64), n_steps)
+    worst = _teacher_forced(spec, Yd, Z)
+    print("flags=%d worst |err|/kappa = %.3g" % (flags, worst))
+
+
+def test_fast_normals_vs_oracle(gpu_lib):
+    """The SL7_FLAG_FAST_NORMALS Box-Muller (MUFU lg2 + series near u -> 1, polynomial sincos in
+    revolutions) stays within 1e-6 (1 + |Z|) of the float64 normals, including the u -> 1 tail."""
+    torch = _torch()
+    sl7 = gpu_lib
+    n, steps, seed = 300_000, 8, 4242
+    out = torch.empty(steps * n, dtype=torch.float32, device="cuda")
+    sl7.normals(seed, 17, n, steps, out, flags=sl7.FLAG_FAST_NORMALS)
+    torch.cuda.synchronize()
+    dev = out.double().cpu().numpy().reshape(steps, n)
+    ref = O.normals(seed, 17 + np.arange(n, dtype=np.uint64), steps)
+    err = np.abs(dev - ref)
+    assert np.all(err <= 1e-6 * (1.0 + np.abs(ref))), err.max()
+
+
+@pytest.mark.parametrize("colloc,theta,ref", [("gbm", (0.05, 0.2), 1), ("ou", (0.0, 1.0, 0.5), 2)])
+def test_specialized_stats_and_reference(gpu_lib, colloc, theta, ref):
+    """Fused statistics and the strong-error reference in the specialised kernel (REF_ON variant):
+    terminal values equal the FULL run's last row bitwise; moments match the oracle's statistics of
+    those values; the strong error vs the exact solution on the same normals stays rounding-level."""
+    sl7 = gpu_lib
+    torch = _torch()
+    n_paths, n_steps, dt = 50_001, 13, 1.0 / 13
+    ctx = sl7.Context(7)
+    code = sl7.COLLOC_EXACT_GBM if colloc == "gbm" else sl7.COLLOC_EXACT_OU
+    flags = sl7.FLAG_FAST_NORMALS | sl7.FLAG_SPECIALIZED
+    full, _ = ctx.simulate(1.0, dt, n_steps, theta, n_paths, 5, sl7.OUT_FULL, sl7.make_opts(colloc=code, flags=flags))
+    YT, st = _run(sl7, ctx, dict(y0=1.0, dt=dt, n_steps=n_steps), n_paths, 5, sl7.OUT_TERMINAL, code, stats=True,
+                  n_bins=256, lo=-2.0, hi=3.0, shift=1.0, ref=ref, ref_theta=theta + (0,) * (3 - len(theta)),
+                  theta=theta, flags=flags)
+    torch.cuda.synchronize()
+    assert np.array_equal(full.double().cpu().numpy()[-n_paths:], YT)
+    v = O.stats_vector(YT, 1.0, -2.0, 3.0, 256)
+    np.testing.assert_allclose(st[2:6], v[2:6], rtol=1e-12, atol=1e-9)
+    assert st[0] == n_paths and st[6] / st[0] < 2e-6
+
+
+def test_specialized_rejects_large_m(gpu_lib):
+    sl7 = gpu_lib
+    ctx = sl7.Context(9)
+    opts = sl7.make_opts(colloc=sl7.COLLOC_EXACT_GBM, flags=sl7.FLAG_SPECIALIZED)
+    with pytest.raises(sl7.Sl7Error, match="EUNSUPPORTED"):
+        ctx.simulate(1.0, 0.5, 2, (0.05, 0.2), 100, 1, sl7.OUT_TERMINAL, opts)
