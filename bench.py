@@ -148,7 +148,7 @@ def main():
     if a.impl == "reference":
         if rank != 0:
             return
-        sample = 32768
+        sample = 65536
         v, cores, el, done = 0.0, 0, 0.0, 0
         t_all = []
         for s in range(a.warmup + a.steps):
@@ -308,7 +308,10 @@ def main():
         mma_flops_ps = flops_ps - 2 * W.dims[1]
         tens = mma_flops_ps * rate / 1e12
         roof = {"bound": "alu", "pipe": "XU (MUFU)", "achieved": achieved, "peak": peak, "unit": "Top/s",
-                "frac": achieved / peak, "traffic": None,
+                "frac": achieved / peak,
+                # dram__bytes_read.sum + dram__bytes_write.sum of the n=64 launch (ncu --set full, recorded in
+                # profiles/r01_ann_tc_ncu.md): weights + stats only; the kernel reads no HBM per path-step
+                "traffic": 140288 + 69632, "traffic_note": "bytes per n=64 launch (1e7 paths x 64 steps)",
                 "peak_basis": "148 SM x 16 MUFU op/clk x %g MHz (max SM clock)" % sm_max,
                 "algorithmic": "%d transcendental activations per path-step (one per hidden unit); the kernel "
                                "spends 2 MUFU ops per activation (ex2 + rcp / ex2 + lg2) for ~2e-7 accuracy" % trans_ps,
@@ -329,7 +332,7 @@ def main():
                                     "strong_err_by_n": ex_stats}},
             "kernel_ms_by_n": {ns: statistics.mean(k[i] for k in kernel_ms) for i, ns in enumerate(N_SWEEP)}}
     if not a.no_cpu_baseline and world == 1:
-        sample = 32768
+        sample = 65536
         v, cores, el, done = oracle_throughput(sample, W.seed, W.blob)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                                 "sample": "%d paths x 127 path-steps (full dt sweep, %.1f s), float64 numpy oracle, "
