@@ -131,7 +131,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="sl7", choices=["sl7", "reference"])
-    ap.add_argument("--prec", default="auto", choices=["auto", "fp32", "bf16"])
+    ap.add_argument("--prec", default="auto", choices=["auto", "fp32", "bf16", "split"])
     ap.add_argument("--paths", type=int, default=10_000_000, help="paths per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     a = ap.parse_args()
@@ -181,7 +181,8 @@ def main():
     blob = load_golden_blob(W.blob)
     ctx = sl7.Context(W.m, list(W.dims), W.act, device=local)
     ctx.load_weights(blob)
-    prec = {"auto": sl7.PREC_FP32, "fp32": sl7.PREC_FP32, "bf16": sl7.PREC_BF16}[a.prec]
+    prec = {"auto": sl7.PREC_FP32, "fp32": sl7.PREC_FP32, "bf16": sl7.PREC_BF16, "split": sl7.PREC_SPLIT}[a.prec]
+    prec_name = {sl7.PREC_FP32: "fp32", sl7.PREC_BF16: "bf16", sl7.PREC_SPLIT: "split-bf16x3"}
     if a.prec == "auto" and getattr(sl7, "HAS_TC", False):
         prec = sl7.PREC_BF16
     from paper_2302_05170_b200.dist import allreduce_stats, max_over_ranks, weak_shard
@@ -316,12 +317,14 @@ def main():
                 "algorithmic": "%d transcendental activations per path-step (one per hidden unit); the kernel "
                                "spends 2 MUFU ops per activation (ex2 + rcp / ex2 + lg2) for ~2e-7 accuracy" % trans_ps,
                 "tensor": {"achieved": tens, "peak": bf16, "unit": "TFLOP/s", "frac": tens / bf16,
-                           "basis": "%d MMA FLOP per path-step vs MEASURED_PEAKS.json bf16_tflops (burst)" % mma_flops_ps}}
+                           "basis": "%d MMA FLOP per path-step vs MEASURED_PEAKS.json bf16_tflops (burst)" % mma_flops_ps,
+                           "issued_per_algorithmic": 6 if prec == sl7.PREC_SPLIT else 1}}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32" if prec == sl7.PREC_FP32 else "bf16", "data": "synthetic (oracle-fitted weights)",
-            "config": dict(config, prec="fp32" if prec == sl7.PREC_FP32 else "bf16", parallelism="dp%d" % world),
+            "dtype": {sl7.PREC_FP32: "f32", sl7.PREC_BF16: "bf16", sl7.PREC_SPLIT: "bf16x3"}[prec],
+            "data": "synthetic (oracle-fitted weights)",
+            "config": dict(config, prec=prec_name[prec], parallelism="dp%d" % world),
             "roofline": roof, "gpu_launches": a.steps * 2 * len(N_SWEEP),
             "clocks": clk.summary(),
             "e2e": {"value": world * path_steps / (e2e_step * 1e-3), "unit": UNIT, "h2d_bytes_per_step": up_b,

@@ -73,7 +73,9 @@ typedef enum { SL7_OUT_FULL = 0, SL7_OUT_TERMINAL = 1, SL7_OUT_STATS = 2 } sl7_o
  *  BF16:  tcgen05 tensor cores, operands rounded to bf16 (RNE), fp32 accumulate, fp32 bias and
  *         activations; reproduces the quantisation-aware oracle O6.
  *  TF32:  tcgen05 kind::tf32, operands rounded with cvt.rna (reserved; SL7_EUNSUPPORTED here).
- *  SPLIT: error-compensated multi-pass bf16 (reserved; SL7_EUNSUPPORTED here).
+ *  SPLIT: tcgen05 with every operand split into three bf16 parts (a = a0 + a1 + a2, same for W) and
+ *         the six partial products of size >= 2^-16 accumulated in fp32: fp32-class results (checked
+ *         against the plain float64 oracle at the fp32 tolerance) at tensor-core speed.
  * Layer 1 (rank-1 in Y once dt and theta are folded into its bias) is always fp32. */
 typedef enum { SL7_PREC_FP32 = 0, SL7_PREC_TF32 = 1, SL7_PREC_BF16 = 2, SL7_PREC_SPLIT = 3 } sl7_prec;
 

@@ -45,6 +45,7 @@ struct sl7_ctx_s {
   int width = 0;           // hidden width used by the FP32 kernel (50 or 64 padded)
   float* d_wf32 = nullptr;
   void* d_wtc = nullptr;   // bf16 SWIZZLE_128B operand image for the tcgen05 kernel
+  void* d_wtc_split = nullptr;   // the same with W split into three bf16 parts (SL7_PREC_SPLIT)
   TcParams tcp;            // biases + image pointer for the tcgen05 kernel
   int num_sms = 148;
   // host-mode staging
@@ -231,47 +232,67 @@ uint16_t f32_to_bf16_rne(float f) {
 sl7_status build_tc_image(sl7_ctx c) {
   const int L = (int)c->dims.size() - 2;
   const int nL = L - 1;
-  std::vector<uint16_t> img((size_t)(nL * kTcTileBytes + kTcOutBytes) / 2, 0);
-  auto put = [&](size_t tile_off_bytes, int n, int k, float v) {
-    const size_t byte = tile_off_bytes + (size_t)n * 128 + (size_t)((((k * 2) >> 4) ^ (n & 7)) << 4) + (size_t)((k * 2) & 15);
-    img[byte / 2] = f32_to_bf16_rne(v);
+  auto bf = [](float v) {   // value of the bf16 (RNE) rounding of v
+    uint32_t u = (uint32_t)f32_to_bf16_rne(v) << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+  };
+  // np = 1: W rounded to bf16 (SL7_PREC_BF16).  np = 3: W = W0 + W1 + W2 split into bf16 parts
+  // (SL7_PREC_SPLIT); part p of hidden tile l at (np (l-1) + p) * 8 KB, output part p after them.
+  auto build = [&](int np) {
+    std::vector<uint16_t> img((size_t)np * (nL * kTcTileBytes + kTcOutBytes) / 2, 0);
+    auto put = [&](size_t tile_off_bytes, int n, int k, float v) {
+      const size_t byte =
+          tile_off_bytes + (size_t)n * 128 + (size_t)((((k * 2) >> 4) ^ (n & 7)) << 4) + (size_t)((k * 2) & 15);
+      img[byte / 2] = f32_to_bf16_rne(v);
+    };
+    for (int l = 1; l <= L; ++l) {   // blob layer l: hidden l -> hidden l+1 (l < L) or -> output (l == L)
+      const int fi = c->dims[l], fo = c->dims[l + 1];
+      const size_t part_bytes = (l < L) ? kTcTileBytes : kTcOutBytes;
+      const size_t base = (l < L) ? (size_t)np * (l - 1) * kTcTileBytes : (size_t)np * nL * kTcTileBytes;
+      for (int n = 0; n < fo; ++n)
+        for (int k = 0; k < fi; ++k) {
+          float r = c->W[l][(size_t)n * fi + k];
+          for (int pt = 0; pt < np; ++pt) {
+            const float q = bf(r);
+            put(base + pt * part_bytes, n, k, q);
+            r -= q;
+          }
+        }
+      if (c->width == 50) {
+        // the width-50 kernel (FOLD) feeds A = 1.0 in K columns 50..52 (part 0 only): the bias enters
+        // the fp32 accumulation as three bf16 terms whose sum reproduces the fp32 bias (hi + mid + lo)
+        for (int n = 0; n < fo; ++n) {
+          const float b = c->b[l][n];
+          const float hi = bf(b), mid = bf(b - hi), lo = bf(b - hi - mid);
+          put(base, n, 50, hi);
+          put(base, n, 51, mid);
+          put(base, n, 52, lo);
+        }
+      }
+    }
+    return img;
   };
   std::memset(&c->tcp, 0, sizeof c->tcp);
-  for (int l = 1; l <= L; ++l) {   // blob layer l: hidden l -> hidden l+1 (l < L) or -> output (l == L)
-    const int fi = c->dims[l], fo = c->dims[l + 1];
-    const size_t off = (size_t)(l - 1) * kTcTileBytes;
-    for (int n = 0; n < fo; ++n)
-      for (int k = 0; k < fi; ++k) put(off, n, k, c->W[l][(size_t)n * fi + k]);
-    for (int n = 0; n < fo; ++n) {
+  for (int l = 1; l <= L; ++l)
+    for (int n = 0; n < c->dims[l + 1]; ++n) {
       if (l < L) c->tcp.bias[l - 1][n] = c->b[l][n];
       else c->tcp.bout[n] = c->b[l][n];
     }
-    if (c->width == 50) {
-      // the width-50 kernel (FOLD) feeds A = 1.0 in K columns 50..52: the bias enters the fp32
-      // accumulation as three bf16 terms whose sum reproduces the fp32 bias (hi + mid + lo)
-      for (int n = 0; n < fo; ++n) {
-        const float b = c->b[l][n];
-        auto bf = [](float v) {
-          uint32_t u = (uint32_t)f32_to_bf16_rne(v) << 16;
-          float f;
-          std::memcpy(&f, &u, 4);
-          return f;
-        };
-        const float hi = bf(b), mid = bf(b - hi), lo = bf(b - hi - mid);
-        put(off, n, 50, hi);
-        put(off, n, 51, mid);
-        put(off, n, 52, lo);
-      }
-    }
-  }
   c->tcp.n_mma_hidden = nL;
-  if (c->d_wtc) cudaFree(c->d_wtc);
-  c->d_wtc = nullptr;
-  cudaError_t e = cudaMalloc(&c->d_wtc, img.size() * 2);
-  if (e != cudaSuccess) return cuda_fail(c, e, "cudaMalloc(tc weights)");
-  e = cudaMemcpy(c->d_wtc, img.data(), img.size() * 2, cudaMemcpyHostToDevice);
-  if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemcpy(tc weights)");
+  for (int np : {1, 3}) {
+    const std::vector<uint16_t> img = build(np);
+    void*& d = (np == 1) ? c->d_wtc : c->d_wtc_split;
+    if (d) cudaFree(d);
+    d = nullptr;
+    cudaError_t e = cudaMalloc(&d, img.size() * 2);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaMalloc(tc weights)");
+    e = cudaMemcpy(d, img.data(), img.size() * 2, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemcpy(tc weights)");
+  }
   c->tcp.wimg = c->d_wtc;
+  c->tcp.wimg_split = c->d_wtc_split;
   return SL7_OK;
 }
 
@@ -379,7 +400,7 @@ sl7_status prepare(sl7_ctx c, double Y0, double dt, int32_t n_steps, const doubl
       if (!c->has_net) return fail(c, SL7_ESTATE, "ANN mode before sl7_load_weights");
       const int d_in = c->dims[0];
       if (n_theta != d_in - 2) return fail(c, SL7_EINVAL, "n_theta must equal layer_dims[0] - 2");
-      if (o->prec != SL7_PREC_FP32 && o->prec != SL7_PREC_BF16)
+      if (o->prec != SL7_PREC_FP32 && o->prec != SL7_PREC_BF16 && o->prec != SL7_PREC_SPLIT)
         return fail(c, SL7_EUNSUPPORTED, "precision mode %d not available in this build", (int)o->prec);
       const int H1 = c->dims[1];
       // features f = (Y, dt, theta...); normalised f' = (f - in_shift) / in_scale
@@ -443,7 +464,7 @@ sl7_status run(sl7_ctx c, RunParams& p, const sl7_run_opts* o, float* d_out, dou
     if (e) return cuda_fail(c, (cudaError_t)e, "zero stats");
   }
   int e;
-  if (p.colloc == kAnn && o->prec == SL7_PREC_BF16) {
+  if (p.colloc == kAnn && (o->prec == SL7_PREC_BF16 || o->prec == SL7_PREC_SPLIT)) {
     // per-run part of the TC parameters: layer 1 folded (as in RunParams) and pre-scaled in double
     TcParams t = c->tcp;
     const double sc = (c->act == SL7_ACT_TANH) ? 2.0 / std::log(2.0) : 1.0;
@@ -456,6 +477,7 @@ sl7_status run(sl7_ctx c, RunParams& p, const sl7_run_opts* o, float* d_out, dou
       for (int k = 0; k < kTcN; ++k) t.bias[l][k] = (float)((double)c->tcp.bias[l][k] * sc);
     const char* v = std::getenv("SL7_TC_VARIANT");
     t.variant = v ? std::atoi(v) : 0;
+    t.split = (o->prec == SL7_PREC_SPLIT) ? 1 : 0;
     e = launch_tc_kernel(p, t, o->stream, c->num_sms);
   } else {
     e = launch_step_kernel(p, (int)o->prec, o->stream, c->num_sms);
@@ -741,6 +763,7 @@ void sl7_destroy(sl7_ctx c) {
     DeviceGuard g(c->device);
     if (c->d_wf32) cudaFree(c->d_wf32);
     if (c->d_wtc) cudaFree(c->d_wtc);
+    if (c->d_wtc_split) cudaFree(c->d_wtc_split);
     if (c->d_out_scratch) cudaFree(c->d_out_scratch);
     if (c->d_stats_scratch) cudaFree(c->d_stats_scratch);
   }

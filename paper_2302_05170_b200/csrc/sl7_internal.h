@@ -91,8 +91,10 @@ struct TcParams {
   float bias[kMaxHidden - 1][kTcN];   // hidden biases scaled by act_scale
   float bout[kTcNOut];
   const void* wimg;
+  const void* wimg_split;   // SL7_PREC_SPLIT: per tile the three bf16 parts W = W0 + W1 + W2 in turn
   int n_mma_hidden;   // L - 1
   int variant;        // activation variant (experiment hook, SL7_TC_VARIANT)
+  int split;          // 1: SL7_PREC_SPLIT
 };
 
 // launchers (sl7_kernels.cu / sl7_tc.cu); return cudaError_t as int

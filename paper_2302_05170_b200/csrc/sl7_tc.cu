@@ -67,11 +67,26 @@ __device__ __forceinline__ bool use_newton(int c) {
   return ACT == SL7_ACT_TANH && ((NMASK >> (c & 7)) & 1u);
 }
 
+// Pack two activations as NP bf16 parts: part 0 = bf16(h); NP = 3 (SL7_PREC_SPLIT) adds the rounded
+// residuals, so h = h0 + h1 + h2 to ~2^-24 relative (the split-precision A operand).
+template <int NP>
+__device__ __forceinline__ void split_pack(float a, float b, uint32_t (&pk)[NP][16], int k) {
+  uint32_t w = tc::pack_bf16x2(a, b);
+  pk[0][k] = w;
+#pragma unroll
+  for (int part = 1; part < NP; ++part) {
+    a -= __uint_as_float(w << 16);
+    b -= __uint_as_float(w & 0xFFFF0000u);
+    w = tc::pack_bf16x2(a, b);
+    pk[part][k] = w;
+  }
+}
+
 // FOLD: the hidden bias rides in the MMA (K columns H, H+1, H+2 of A hold 1.0, the weight tile holds
 // the bias split into three bf16 terms), so u = acc * scale.  Otherwise u = acc * scale + bias_scaled.
-template <int ACT, int H, unsigned NMASK, bool FOLD>
+template <int ACT, int H, unsigned NMASK, bool FOLD, int NP>
 __device__ __forceinline__ void act_pack_32(const uint32_t (&v)[32], int col0, float scale, const float* bs,
-                                            uint32_t (&pk)[16]) {
+                                            uint32_t (&pk)[NP][16]) {
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
     float h[2];
@@ -86,11 +101,30 @@ __device__ __forceinline__ void act_pack_32(const uint32_t (&v)[32], int col0, f
         h[q] = (FOLD && c < H + 3) ? 1.0f : 0.0f;
       }
     }
-    pk[k] = tc::pack_bf16x2(h[0], h[1]);
+    split_pack<NP>(h[0], h[1], pk, k);
   }
 }
 
-template <int NG, int H, int MR, bool RT_M, int ACT, unsigned NMASK>
+// MMA issue for one layer: sum over (A part, B part) pairs of [128 x 64] x [64 x N] with K = 4 x 16.
+// NP = 1: bf16 x bf16.  NP = 3: the six pairs whose products are >= 2^-16 of the leading one
+// (hh, hm, mh, hl, lh, mm): fp32-class products from bf16 tensor cores.
+template <int NP>
+__device__ __forceinline__ void issue_layer(uint32_t acc_t, uint32_t a_t, uint32_t b_base, uint32_t b_part_bytes,
+                                            uint32_t idesc) {
+  constexpr int NPAIR = (NP == 1) ? 1 : 6;
+  constexpr int PA[6] = {0, 0, 1, 0, 2, 1};
+  constexpr int PB[6] = {0, 1, 0, 2, 0, 1};
+#pragma unroll
+  for (int pr = 0; pr < NPAIR; ++pr) {
+    const uint64_t bdesc = tc::smem_desc_sw128(b_base + (uint32_t)PB[pr] * b_part_bytes);
+    const uint32_t a = a_t + 32u * PA[pr];
+#pragma unroll
+    for (int k = 0; k < kTcN / 16; ++k)   // +32 bytes per K step inside the 128-byte swizzle atom
+      tc::mma_bf16_ts(acc_t, a + 8u * k, bdesc + 2u * k, idesc, (pr > 0 || k > 0) ? 1u : 0u);
+  }
+}
+
+template <int NG, int H, int MR, bool RT_M, int ACT, unsigned NMASK, int NP = 1>
 __global__ void __launch_bounds__(NG * kGroupThreads, 1)
     ann_tc_step_kernel(const __grid_constant__ RunParams p, const __grid_constant__ TcParams t) {
   extern __shared__ uint8_t smem_raw[];
@@ -102,17 +136,19 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
   const int g = warp >> 2;                 // tile group
   const int wq = warp & 3;                 // warp within the group -> TMEM lanes [32 wq, 32 wq + 32)
   const int tid_g = threadIdx.x & (kGroupThreads - 1);
-  constexpr uint32_t kTmemCols = NG * kColsPerGroup <= 256 ? 256u : 512u;
+  constexpr uint32_t kCols = kAccCol + 64u + 32u * NP;     // acc fp32 [0,64) + NP bf16 A parts
+  constexpr uint32_t kTmemCols = NG * kCols <= 256 ? 256u : 512u;
+  static_assert(NG * kCols <= 512, "TMEM: 512 columns per SM");
   constexpr bool FOLD = (H <= kTcN - 3);   // biases ride in spare K columns (host image must match)
 
   // ---- one-time CTA setup: weights -> smem (1024-aligned for the 128B swizzle), barriers, TMEM
   const uint32_t sbase = (tc::smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* wsm = smem_raw + (sbase - tc::smem_u32(smem_raw));
   const int nL = t.n_mma_hidden;
-  const int wbytes = nL * kTcTileBytes + kTcOutBytes;
+  const int wbytes = NP * (nL * kTcTileBytes + kTcOutBytes);
   uint32_t* hist = reinterpret_cast<uint32_t*>(wsm + wbytes);
   {
-    const uint4* src = reinterpret_cast<const uint4*>(t.wimg);
+    const uint4* src = reinterpret_cast<const uint4*>(NP == 1 ? t.wimg : t.wimg_split);
     uint4* dst = reinterpret_cast<uint4*>(wsm);
     for (int i = threadIdx.x; i < wbytes / 16; i += blockDim.x) dst[i] = src[i];
   }
@@ -128,7 +164,7 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tbase = tmem_base_sh;
-  const uint32_t gcol = tbase + (uint32_t)g * kColsPerGroup;
+  const uint32_t gcol = tbase + (uint32_t)g * kCols;
   const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
   const uint32_t acc_t = gcol + kAccCol, a_t = gcol + kACol;
   constexpr uint32_t idesc_h = tc::idesc_bf16_f32(128, kTcN);
@@ -155,7 +191,7 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
       // ---- layer 1 (fp32, rank 1 in Y) -> A operand in TMEM, two 32-unit halves
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
-        uint32_t pk[16];
+        uint32_t pk[NP][16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
           float h[2];
@@ -165,9 +201,11 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
             h[q] = (c < H) ? tc_act_u<ACT>(fmaf(Y, t.l1w[c], t.l1b[c]), use_newton<ACT, NMASK>(c))
                            : ((FOLD && c < H + 3) ? 1.0f : 0.0f);
           }
-          pk[k] = tc::pack_bf16x2(h[0], h[1]);
+          split_pack<NP>(h[0], h[1], pk, k);
         }
-        tc::tmem_st_32x32b_x16(a_t + lane_off + 16u * half, pk);
+#pragma unroll
+        for (int part = 0; part < NP; ++part)
+          tc::tmem_st_32x32b_x16(a_t + 32u * part + lane_off + 16u * half, pk[part]);
       }
       tc::wait_st();
       // ---- layers 2..L+1 on the tensor cores; the Lagrange basis at Z (independent of the MLP)
@@ -179,11 +217,11 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
         tc::named_bar_sync(1 + g, kGroupThreads);
         if (tid_g == 0) {
           tc::fence_after();
-          const uint64_t bdesc = tc::smem_desc_sw128(sbase + (uint32_t)l * kTcTileBytes);
-          const uint32_t id = last ? idesc_o : idesc_h;
-#pragma unroll
-          for (int k = 0; k < kTcN / 16; ++k)   // K = 64 = 4 x 16; +32 bytes per K step inside the swizzle atom
-            tc::mma_bf16_ts(acc_t, a_t + 8u * k, bdesc + 2u * k, id, k > 0 ? 1u : 0u);
+          // weight image: NP parts of each hidden tile (8 KB), then NP parts of the output tile (2 KB)
+          if (last)
+            issue_layer<NP>(acc_t, a_t, sbase + (uint32_t)(NP * nL * kTcTileBytes), kTcOutBytes, idesc_o);
+          else
+            issue_layer<NP>(acc_t, a_t, sbase + (uint32_t)(NP * l * kTcTileBytes), kTcTileBytes, idesc_h);
           tc::mma_commit(bar);
         }
         if (l == 0) den = gm_basis<MR, RT_M>(p, Z, lb);
@@ -193,12 +231,14 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
         if (!last) {
 #pragma unroll
           for (int half = 0; half < 2; ++half) {
-            uint32_t pk[16];
+            uint32_t pk[NP][16];
             uint32_t v[32];
             tc::tmem_ld_32x32b_x32(acc_t + lane_off + 32u * half, v);
             tc::wait_ld();
-            act_pack_32<ACT, H, NMASK, FOLD>(v, 32 * half, t.act_scale, t.bias[l], pk);
-            tc::tmem_st_32x32b_x16(a_t + lane_off + 16u * half, pk);
+            act_pack_32<ACT, H, NMASK, FOLD, NP>(v, 32 * half, t.act_scale, t.bias[l], pk);
+#pragma unroll
+            for (int part = 0; part < NP; ++part)
+              tc::tmem_st_32x32b_x16(a_t + 32u * part + lane_off + 16u * half, pk[part]);
           }
           tc::wait_st();
         } else {
@@ -228,11 +268,11 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
 
 namespace {
 
-template <int NG, int H, int MR, bool RT, int ACT, unsigned NMASK = 0u>
+template <int NG, int H, int MR, bool RT, int ACT, unsigned NMASK = 0u, int NP = 1>
 cudaError_t launch_tc_t(const RunParams& p, const TcParams& t, cudaStream_t st, int num_sms) {
-  auto kernel = ann_tc_step_kernel<NG, H, MR, RT, ACT, NMASK>;
+  auto kernel = ann_tc_step_kernel<NG, H, MR, RT, ACT, NMASK, NP>;
   const size_t hist = (p.has_stats && p.n_bins > 0) ? sizeof(uint32_t) * (size_t)(p.n_bins + 2) : 0;
-  const size_t smem = 1024 + (size_t)t.n_mma_hidden * kTcTileBytes + kTcOutBytes + hist;
+  const size_t smem = 1024 + (size_t)NP * ((size_t)t.n_mma_hidden * kTcTileBytes + kTcOutBytes) + hist;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const uint64_t tiles = (p.n_paths + kGroupThreads - 1) / kGroupThreads;
@@ -248,10 +288,19 @@ cudaError_t launch_tc_t(const RunParams& p, const TcParams& t, cudaStream_t st, 
 constexpr int kTcGroups = 4;
 constexpr unsigned kTanhNewtonMask = 0x55u;
 
+// SL7_PREC_SPLIT: three bf16 parts per operand (TMEM 64 + 3 x 32 = 160 columns per group -> 3 groups).
+constexpr int kTcGroupsSplit = 3;
+
 template <int ACT>
 cudaError_t launch_tc_act(const RunParams& p, const TcParams& t, cudaStream_t st, int num_sms) {
   constexpr int NG = kTcGroups;
   constexpr unsigned NM = (ACT == SL7_ACT_TANH) ? kTanhNewtonMask : 0u;
+  if (t.split) {
+    constexpr int NS = kTcGroupsSplit;
+    if (p.width == 50 && p.m == 5) return launch_tc_t<NS, 50, 5, false, ACT, NM, 3>(p, t, st, num_sms);
+    if (p.width == 50 && p.m == 7) return launch_tc_t<NS, 50, 7, false, ACT, NM, 3>(p, t, st, num_sms);
+    return launch_tc_t<NS, 64, kMaxM, true, ACT, NM, 3>(p, t, st, num_sms);
+  }
   if (p.width == 50 && p.m == 5) return launch_tc_t<NG, 50, 5, false, ACT, NM>(p, t, st, num_sms);
   if (p.width == 50 && p.m == 7) {
     if constexpr (ACT == SL7_ACT_TANH) {

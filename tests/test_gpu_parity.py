@@ -318,6 +318,24 @@ def test_ann_bf16_terminal_moments(gpu_lib, name):
                                                                            np.quantile(rel, 0.99), rel.max()))
 
 
+@pytest.mark.parametrize("name,gen", ANN_CASES, ids=[c[0] for c in ANN_CASES])
+def test_ann_split_tc_teacher_forced(gpu_lib, name, gen):
+    """SL7_PREC_SPLIT: bf16 tensor cores with three-part operands reach the fp32 bar (T-2, 1e-5 kappa)
+    against the plain float64 oracle O3."""
+    sl7 = gpu_lib
+    blob, m, dims, act, theta, y0, n_steps, dt = _ann_case(name, gen)
+    n_paths = 3 * 128 * 4 + 33
+    ctx = sl7.Context(m, dims, act)
+    ctx.load_weights(blob)
+    Yd, _ = _run(sl7, ctx, dict(y0=y0, dt=dt, n_steps=n_steps), n_paths, 31, sl7.OUT_FULL, sl7.COLLOC_ANN,
+                 prec=sl7.PREC_SPLIT, theta=theta)
+    Yd = Yd.reshape(n_steps + 1, n_paths)
+    spec = O.Spec(m, "ann", theta, y0, dt, n_steps, net=O.parse_blob(blob))
+    Z = O.normals(31, np.arange(n_paths, dtype=np.uint64), n_steps)
+    worst = _teacher_forced(spec, Yd, Z, tol=1e-5)
+    print("split teacher-forced worst |err|/kappa = %.3g" % worst)
+
+
 def test_ann_bf16_sharding_bitwise(gpu_lib):
     sl7 = gpu_lib
     w = workloads()["cfg0"]
