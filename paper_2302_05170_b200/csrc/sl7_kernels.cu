@@ -148,7 +148,8 @@ __global__ void __launch_bounds__(128) ann_f32_step_kernel(const __grid_constant
   __shared__ double red[8];
   const int L = p.n_hidden;
   const size_t nw = f32_weight_floats(H, HS, L, MR);
-  uint32_t* hist = reinterpret_cast<uint32_t*>(sw + ((nw + 3) & ~size_t(3)));
+  float* gs = sw + ((nw + 3) & ~size_t(3));                  // [H][blockDim] activation scratch
+  uint32_t* hist = reinterpret_cast<uint32_t*>(gs + (size_t)H * blockDim.x);
   for (size_t k = threadIdx.x; k < nw; k += blockDim.x) sw[k] = p.wdev[k];
   hist_init(p, hist);
   __syncthreads();
@@ -175,8 +176,10 @@ __global__ void __launch_bounds__(128) ann_f32_step_kernel(const __grid_constant
       for (int l = 0; l < L - 1; ++l) {
         const float* W = sw + (size_t)l * f32_layer_floats(H, HS);
         const float* b = W + H * HS;
-        float g[H];
-#pragma unroll
+        // output neurons in a rolled loop (a fully unrolled 50 x 50 body overflows the instruction
+        // cache: ncu showed "no_instructions" as the top stall); each neuron's activation goes to the
+        // thread's own column of a shared-memory scratch and is read back into registers afterwards
+#pragma unroll 2
         for (int j = 0; j < H; ++j) {
           const float4* row = reinterpret_cast<const float4*>(W + j * HS);
           float a0 = b[j], a1 = 0.f;
@@ -188,10 +191,10 @@ __global__ void __launch_bounds__(128) ann_f32_step_kernel(const __grid_constant
             if (4 * kk + 2 < H) a0 = fmaf(wv.z, h[4 * kk + 2], a0);
             if (4 * kk + 3 < H) a1 = fmaf(wv.w, h[4 * kk + 3], a1);
           }
-          g[j] = activate<ACT>(a0 + a1);
+          gs[j * blockDim.x + threadIdx.x] = activate<ACT>(a0 + a1);
         }
 #pragma unroll
-        for (int k = 0; k < H; ++k) h[k] = g[k];
+        for (int k = 0; k < H; ++k) h[k] = gs[k * blockDim.x + threadIdx.x];
       }
       float y[MR];
 #pragma unroll
@@ -312,7 +315,7 @@ cudaError_t launch_exact(const RunParams& p, cudaStream_t st, int num_sms) {
 template <int H, int HS, int MR, bool RT, int ACT>
 cudaError_t launch_ann_f32_t(const RunParams& p, cudaStream_t st, int num_sms) {
   const size_t nw = f32_weight_floats(H, HS, p.n_hidden, MR);
-  const size_t smem = ((nw + 3) & ~size_t(3)) * sizeof(float) + hist_bytes(p);
+  const size_t smem = (((nw + 3) & ~size_t(3)) + (size_t)H * 128) * sizeof(float) + hist_bytes(p);
   return launch_persistent(ann_f32_step_kernel<H, HS, MR, RT, ACT>, 128, smem, p, st, num_sms);
 }
 
