@@ -426,6 +426,57 @@ def simulate(spec: Spec, seed: int, paths) -> tuple[np.ndarray, np.ndarray]:
     return Y, Z
 
 
+# ----------------------------------------------------------------------------------------------
+# 7L-CDC ("a variant, the 7L-CDC scheme ... with more interpolations in Step 3";
+# PAPER.md:106-108 "a global interpolation technique which is based on the marginal collocation
+# points to compute the conditional collocation points for each random path ... only requires the
+# ANNs to compute a small number of marginal collocation points").  Readings R-18..R-20:
+# per step, the m marginal collocation points z_k are the empirical quantiles of the current states
+# of ALL paths at the levels Phi(x_k) (plotting position (k - 0.5)/M, linear interpolation); the table
+# row C[k] = H(z_k) is one predictor call per marginal point; each path's conditional points are the
+# Lagrange interpolant of k -> C[k][j] on the nodes z_k evaluated at its own state; repeated z_k
+# (e.g. step 0, all paths at Y0) fall back to the nearest row (ties: lowest k).  No sorting (R-6).
+# ----------------------------------------------------------------------------------------------
+
+
+def normal_cdf(x) -> np.ndarray:
+    """Phi(x) = erfc(-x / sqrt 2) / 2 (library: scipy.special.erfc)."""
+    from scipy.special import erfc
+    return 0.5 * erfc(-np.asarray(x, dtype=np.float64) / np.sqrt(2.0))
+
+
+def cdc_table(spec: Spec, Y):
+    """Marginal collocation points z (m,) of the current states Y (all paths) and the table C (m, m)."""
+    z = quantiles(Y, normal_cdf(spec.x))
+    return z, spec.points(z)
+
+
+def cdc_points(z, C, Y) -> np.ndarray:
+    """Conditional collocation points of every path: (P, m)."""
+    Y = np.asarray(Y, dtype=np.float64)
+    if np.any(np.diff(z) <= 0):
+        k = np.argmin(np.abs(Y[:, None] - z[None, :]), axis=1)     # first minimum = lowest k
+        return C[k]
+    return lagrange_basis(Y, z) @ C
+
+
+def simulate_cdc(spec: Spec, seed: int, paths) -> tuple[np.ndarray, np.ndarray]:
+    """7L-CDC over the FULL path set `paths` (the marginal points couple all paths)."""
+    paths = np.asarray(paths, dtype=np.uint64)
+    Z = normals(seed, paths, spec.n_steps)
+    Y = np.empty((spec.n_steps + 1, len(paths)))
+    Y[0] = spec.y0
+    for i in range(spec.n_steps):
+        Y[i + 1] = cdc_step(spec, Y[i], Z[i])
+    return Y, Z
+
+
+def cdc_step(spec: Spec, Y, Z) -> np.ndarray:
+    """One CDC step of every path from the states Y (all paths) with normals Z."""
+    z, C = cdc_table(spec, Y)
+    return lagrange_eval(Z, spec.x, cdc_points(z, C, Y))
+
+
 def exact_reference(process: str, theta, y0, dt, Z) -> np.ndarray:
     """Exact solution on the same normals (Eq. 6.6 'used to compute the reference
     value to the path-wise error').  GBM: Y_T = Y0 exp((mu - s^2/2) T + s sqrt(dt) sum_i Z_i);
