@@ -91,6 +91,15 @@ typedef enum { SL7_COLLOC_ANN = 0, SL7_COLLOC_EXACT_GBM = 1, SL7_COLLOC_EXACT_OU
  * ref_theta = (mu, s).  OU: the exact Eq. 6.6 transition per step, ref_theta = (Ybar, lam, s). */
 typedef enum { SL7_REF_NONE = 0, SL7_REF_GBM = 1, SL7_REF_OU = 2 } sl7_ref;
 
+/* Scheme.  7L: Algorithm I, the predictor runs for every path.
+ * CDC: the 7L-CDC variant: per step the predictor runs only at the m marginal
+ * collocation points z_k = empirical quantiles of the current states of ALL paths of the call at the
+ * levels Phi(x_k) (plotting position (k - 0.5)/M, linear interpolation; exact order statistics by radix
+ * select on the device), and each path's conditional points are the Lagrange interpolant of the table
+ * rows on the z_k at its own state; repeated z_k (step 0) use the nearest row.  The marginal points
+ * couple the paths, so a CDC call must hold the whole path set (no sharding; opts->ref must be NONE). */
+typedef enum { SL7_SCHEME_7L = 0, SL7_SCHEME_CDC = 1 } sl7_scheme;
+
 typedef struct {
   sl7_prec prec;            /* ANN arithmetic (ignored by the exact modes) */
   sl7_colloc colloc;        /* source of y_j */
@@ -103,6 +112,7 @@ typedef struct {
   sl7_ref ref;              /* strong-error reference (SL7_REF_NONE: E1 = E2 = 0) */
   double ref_theta[3];
   uint32_t flags;           /* SL7_FLAG_* below; 0 = defaults */
+  sl7_scheme scheme;        /* SL7_SCHEME_7L (Algorithm I) or SL7_SCHEME_CDC */
 } sl7_run_opts;
 
 /* opts->flags (exact-collocation modes only; ignored otherwise):

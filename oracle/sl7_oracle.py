@@ -471,6 +471,28 @@ def simulate_cdc(spec: Spec, seed: int, paths) -> tuple[np.ndarray, np.ndarray]:
     return Y, Z
 
 
+def cdc_step_error_scale(spec: Spec, Y, Z) -> np.ndarray:
+    """Forward-error scale of one CDC step (tolerance helper, not part of the method): the outer
+    interpolation's sum_j |l_j(Z)| A_j with A_j = sum_k |l_k(Y; z)| S_kj, S the size of the terms of
+    the table entries (as in step_error_scale)."""
+    Y = np.asarray(Y, dtype=np.float64)
+    z, C = cdc_table(spec, Y)
+    if spec.colloc == "ann":
+        S = mlp_abs_scale(spec.net, ann_features(z, spec.dt, spec.theta), spec.quant)
+    elif spec.colloc == "ou":
+        ybar, lam, sigma = spec.theta
+        e = np.exp(-lam * spec.dt)
+        _, std = ou_conditional_moments(z, spec.dt, ybar, lam, sigma)
+        S = (np.abs(z * e) + abs(ybar * (1 - e)))[:, None] + np.abs(std * spec.x)
+    else:
+        S = np.abs(C)
+    if np.any(np.diff(z) <= 0):
+        A = S[np.argmin(np.abs(Y[:, None] - z[None, :]), axis=1)]
+    else:
+        A = np.abs(lagrange_basis(Y, z)) @ S
+    return np.sum(np.abs(lagrange_basis(Z, spec.x)) * A, axis=-1)
+
+
 def cdc_step(spec: Spec, Y, Z) -> np.ndarray:
     """One CDC step of every path from the states Y (all paths) with normals Z."""
     z, C = cdc_table(spec, Y)

@@ -33,7 +33,11 @@ class sl7_run_opts(ctypes.Structure):
     _fields_ = [("prec", ctypes.c_int), ("colloc", ctypes.c_int), ("path_offset", ctypes.c_uint64),
                 ("stream", ctypes.c_void_p), ("hist_lo", ctypes.c_double), ("hist_hi", ctypes.c_double),
                 ("shift", ctypes.c_double), ("n_bins", ctypes.c_int32), ("accumulate", ctypes.c_int32),
-                ("ref", ctypes.c_int), ("ref_theta", ctypes.c_double * 3), ("flags", ctypes.c_uint32)]
+                ("ref", ctypes.c_int), ("ref_theta", ctypes.c_double * 3), ("flags", ctypes.c_uint32),
+                ("scheme", ctypes.c_int)]
+
+
+SCHEME_7L, SCHEME_CDC = 0, 1
 
 
 FLAG_FAST_NORMALS = 1
@@ -120,9 +124,9 @@ def _stream_ptr(stream):
 
 def make_opts(prec=PREC_FP32, colloc=COLLOC_ANN, path_offset=0, stream=None, hist_lo=0.0, hist_hi=0.0,
               shift=0.0, n_bins=0, accumulate=0, ref=REF_NONE, ref_theta=(0.0, 0.0, 0.0), raw_stream=None,
-              flags=0):
+              flags=0, scheme=SCHEME_7L):
     o = sl7_run_opts()
-    o.prec, o.colloc, o.path_offset, o.flags = prec, colloc, int(path_offset), int(flags)
+    o.prec, o.colloc, o.path_offset, o.flags, o.scheme = prec, colloc, int(path_offset), int(flags), int(scheme)
     o.stream = raw_stream if raw_stream is not None else (_stream_ptr(stream) if stream is not False else None)
     o.hist_lo, o.hist_hi, o.shift, o.n_bins, o.accumulate = hist_lo, hist_hi, shift, int(n_bins), int(accumulate)
     o.ref = ref

@@ -1,0 +1,334 @@
+// sl7_cdc.cu -- the 7L-CDC variant on sm_100a.
+//
+// Per large step i (readings R-18..R-20):
+//   1. marginal collocation points z_k = empirical quantiles of the current states of ALL paths at
+//      the levels Phi(x_k) (plotting position (k - 0.5)/M, linear interpolation between order
+//      statistics).  The 2m order statistics are found EXACTLY by a 4-pass radix select on the
+//      order-preserving 32-bit key of the fp32 state (8 bits per pass): each pass histograms the next
+//      digit of the elements whose higher digits match a target's prefix (shared-memory histograms,
+//      one per distinct prefix), then one small kernel walks the histograms to fix each target's digit.
+//   2. table C[k][.] = H(z_k): m predictor calls (exact closed forms, or the MLP in fp32);
+//   3. per path: y_j = Lagrange interpolant of k -> C[k][j] on the nodes z_k at the path's own state
+//      (normalised barycentric product form), then Y_{i+1} = g_m(X_hat) on the Gauss-Hermite grid.
+// Repeated z_k (step 0: every path at Y0) fall back to the nearest row (ties: lowest k).
+// The states live in HBM between steps (the quantiles couple all paths), so a CDC step is a short
+// sequence of launches on the caller's stream; HBM traffic per path-step: 4 selection reads + 1 read
+// + 1 write of 4 bytes.
+#include <cuda_runtime.h>
+
+#include <cstring>
+
+#include "sl7_device.cuh"
+
+namespace sl7 {
+
+constexpr int kCdcMaxT = 2 * kMaxM;   // targets: two order statistics per marginal point
+
+// Device-side scratch of the CDC pipeline (context-owned).
+struct CdcScratch {
+  unsigned long long hist[kCdcMaxT][256];   // per-slot digit histograms of the current pass
+  unsigned long long rank[kCdcMaxT];        // residual rank of each target within its prefix
+  uint32_t prefix[kCdcMaxT];                // key bits fixed so far (in the high bits)
+  int slot_of[kCdcMaxT];                    // target -> histogram slot
+  uint32_t slot_prefix[kCdcMaxT];           // distinct prefixes, ascending
+  int nslot;
+  unsigned long long M;                     // number of finite states
+  double frac[kMaxM];                       // interpolation weight of the upper order statistic
+  // the table the step kernel consumes
+  float z[kMaxM], v[kMaxM], C[kMaxM][kMaxM];
+  int degenerate;
+  double zd[kMaxM];
+};
+
+__device__ __forceinline__ uint32_t f2key(float f) {
+  const uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float key2f(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+
+// ---- pass p: histogram of digit p (bits [24 - 8p, 32 - 8p)) of the elements matching a slot prefix
+__global__ void __launch_bounds__(256) cdc_hist_kernel(const float* __restrict__ y, uint64_t n, int pass,
+                                                       CdcScratch* s) {
+  __shared__ uint32_t h[kCdcMaxT][256];
+  __shared__ uint32_t sp[kCdcMaxT];
+  const int nslot = s->nslot;
+  for (int i = threadIdx.x; i < nslot * 256; i += blockDim.x) h[i >> 8][i & 255] = 0u;
+  if (threadIdx.x < nslot) sp[threadIdx.x] = s->slot_prefix[threadIdx.x];
+  __syncthreads();
+  const int shift = 24 - 8 * pass;
+  const uint32_t lo = sp[0], hi = sp[nslot - 1];
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (uint64_t)gridDim.x * blockDim.x) {
+    const float v = y[q];
+    if (!isfinite(v)) continue;
+    const uint32_t key = f2key(v);
+    const uint32_t digit = (key >> shift) & 255u;
+    int slot = 0;
+    if (pass > 0) {
+      const uint32_t pre = key >> (shift + 8);
+      if (pre < lo || pre > hi) continue;
+      int a = 0, b = nslot - 1;   // binary search in the ascending slot prefixes
+      while (a < b) {
+        const int mid = (a + b) >> 1;
+        if (sp[mid] < pre) a = mid + 1; else b = mid;
+      }
+      if (sp[a] != pre) continue;
+      slot = a;
+    }
+    atomicAdd(&h[slot][digit], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nslot * 256; i += blockDim.x) {
+    const uint32_t c = h[i >> 8][i & 255];
+    if (c) atomicAdd(&s->hist[i >> 8][i & 255], (unsigned long long)c);
+  }
+}
+
+// ---- after pass p: fix each target's digit; set up the next pass (one block of 256 threads)
+__global__ void __launch_bounds__(256) cdc_scan_kernel(int pass, int m, CdcScratch* s, const __grid_constant__ CdcLevels lv) {
+  const int T = 2 * m;
+  if (threadIdx.x == 0) {
+    if (pass == 0) {
+      // M finite states; target order statistics (0-based) of the plotting-position quantiles
+      unsigned long long M = 0;
+      for (int b = 0; b < 256; ++b) M += s->hist[0][b];
+      s->M = M;
+      for (int k = 0; k < m && M == 0; ++k) {   // no finite state: every target at rank 0 (z = NaN below)
+        s->frac[k] = 0.0;
+        s->rank[2 * k] = s->rank[2 * k + 1] = 0ull;
+        s->prefix[2 * k] = s->prefix[2 * k + 1] = 0u;
+      }
+      for (int k = 0; k < m && M > 0; ++k) {
+        double pos = lv.p[k] * (double)M + 0.5;                  // 1-based fractional rank
+        if (pos < 1.0) pos = 1.0;
+        if (pos > (double)M) pos = (double)M;
+        const double kk = floor(pos);
+        s->frac[k] = pos - kk;
+        const unsigned long long r0 = (unsigned long long)kk - 1ull;
+        const unsigned long long r1 = ((unsigned long long)kk < M) ? (unsigned long long)kk : M - 1ull;
+        s->rank[2 * k] = r0;
+        s->rank[2 * k + 1] = r1;
+        s->prefix[2 * k] = s->prefix[2 * k + 1] = 0u;
+      }
+    }
+    // descend one digit per target
+    for (int t = 0; t < T; ++t) {
+      const int sl = (pass == 0) ? 0 : s->slot_of[t];
+      const unsigned long long r = s->rank[t];
+      int b = 0;
+      unsigned long long below = 0;   // elements of this prefix in bins < b
+      while (b < 255 && below + s->hist[sl][b] <= r) below += s->hist[sl][b++];
+      s->rank[t] = r - below;
+      s->prefix[t] = (s->prefix[t] << 8) | (uint32_t)b;
+    }
+    if (pass < 3) {
+      // distinct prefixes (targets are ordered by rank, so prefixes are non-decreasing)
+      int ns = 0;
+      for (int t = 0; t < T; ++t) {
+        if (ns == 0 || s->slot_prefix[ns - 1] != s->prefix[t]) s->slot_prefix[ns++] = s->prefix[t];
+        s->slot_of[t] = ns - 1;
+      }
+      s->nslot = ns;
+    } else {
+      // full keys known: marginal points in double (as the oracle: y_lo (1 - f) + y_hi f)
+      int degen = 0;
+      for (int k = 0; k < m; ++k) {
+        const double a = (double)key2f(s->prefix[2 * k]), b = (double)key2f(s->prefix[2 * k + 1]);
+        const double f = s->frac[k];
+        s->zd[k] = (s->M > 0) ? a * (1.0 - f) + b * f : __longlong_as_double(0x7FF8000000000000ll);
+        if (k > 0 && !(s->zd[k] > s->zd[k - 1])) degen = 1;   // repeated (or NaN) marginal points
+      }
+      s->degenerate = degen;
+      for (int k = 0; k < m; ++k) {
+        s->z[k] = (float)s->zd[k];
+        double w = 1.0;
+        if (!degen)
+          for (int l = 0; l < m; ++l)
+            if (l != k) w *= (s->zd[k] - s->zd[l]);
+        s->v[k] = degen ? 0.0f : (float)(1.0 / w);
+      }
+    }
+  }
+  __syncthreads();
+  // clear the histograms for the next pass
+  for (int i = threadIdx.x; i < kCdcMaxT * 256; i += blockDim.x) s->hist[i >> 8][i & 255] = 0ull;
+  if (pass == 3 && threadIdx.x == 0) {   // reset the selection for the next step
+    s->nslot = 1;
+    s->slot_prefix[0] = 0u;
+  }
+}
+
+// ---- table rows C[k][.] = H(z_k)
+__global__ void cdc_table_exact_kernel(const __grid_constant__ RunParams p, CdcScratch* s) {
+  const int k = threadIdx.x / kMaxM, j = threadIdx.x % kMaxM;
+  if (k >= p.m || j >= p.m) return;
+  const float zk = s->z[k];
+  s->C[k][j] = (p.colloc == kExactGbm) ? zk * p.c[j] : fmaf(p.ou_a, zk, p.ou_b) + p.c[j];
+}
+
+// MLP on the m marginal points, fp32 with the accurate activations of the FP32 kernel.  The weight
+// image is the FP32 kernel's (hidden layers W[H][HS] + b, then output rows).
+template <int ACT>
+__global__ void __launch_bounds__(256) cdc_table_mlp_kernel(const __grid_constant__ RunParams p, CdcScratch* s) {
+  __shared__ float h[kMaxM][kMaxW], g[kMaxM][kMaxW];
+  const int m = p.m, H = p.width, HS = (H == 50) ? 52 : 64, L = p.n_hidden;
+  const int MR = (H == 50) ? m : kMaxM;
+  for (int i = threadIdx.x; i < m * kMaxW; i += blockDim.x) {
+    const int k = i / kMaxW, u = i % kMaxW;
+    h[k][u] = (u < H) ? activate<ACT>(fmaf(p.l1w[u], s->z[k], p.l1b[u])) : 0.0f;
+  }
+  __syncthreads();
+  for (int l = 0; l < L - 1; ++l) {
+    const float* W = p.wdev + (size_t)l * f32_layer_floats(H, HS);
+    const float* b = W + (size_t)H * HS;
+    for (int i = threadIdx.x; i < m * kMaxW; i += blockDim.x) {
+      const int k = i / kMaxW, u = i % kMaxW;
+      float a = 0.0f;
+      if (u < H) {
+        a = b[u];
+        for (int v = 0; v < H; ++v) a = fmaf(W[(size_t)u * HS + v], h[k][v], a);
+        a = activate<ACT>(a);
+      }
+      g[k][u] = a;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < m * kMaxW; i += blockDim.x) h[i / kMaxW][i % kMaxW] = g[i / kMaxW][i % kMaxW];
+    __syncthreads();
+  }
+  const float* Wo = p.wdev + (size_t)(L - 1) * f32_layer_floats(H, HS);
+  const float* bo = Wo + (size_t)MR * HS;
+  for (int i = threadIdx.x; i < m * m; i += blockDim.x) {
+    const int k = i / m, j = i % m;
+    float a = bo[j];
+    for (int v = 0; v < H; ++v) a = fmaf(Wo[(size_t)j * HS + v], h[k][v], a);
+    s->C[k][j] = fmaf(a, p.out_scale[j], p.out_shift[j]);
+  }
+}
+
+// ---- per-path CDC step: conditional points by interpolation in the state, then g_m(X_hat)
+template <int MR, bool RT_M>
+__global__ void __launch_bounds__(256) cdc_step_kernel(const __grid_constant__ RunParams p, const CdcScratch* s,
+                                                       const float* yin, float* yout,   // may alias (in place)
+                                                       int step, int last) {
+  extern __shared__ uint32_t hist[];
+  __shared__ double red[8];
+  __shared__ float sz[kMaxM], sv[kMaxM], sC[kMaxM][kMaxM];
+  __shared__ int sdeg;
+  for (int i = threadIdx.x; i < kMaxM * kMaxM; i += blockDim.x) {
+    const int k = i / kMaxM, j = i % kMaxM;
+    sC[k][j] = (k < p.m && j < p.m) ? s->C[k][j] : 0.0f;
+  }
+  if (threadIdx.x < kMaxM) {
+    sz[threadIdx.x] = (threadIdx.x < p.m) ? s->z[threadIdx.x] : 0.0f;
+    sv[threadIdx.x] = (threadIdx.x < p.m) ? s->v[threadIdx.x] : 0.0f;
+  }
+  if (threadIdx.x == 0) sdeg = s->degenerate;
+  if (last) hist_init(p, hist);
+  __syncthreads();
+  const int m = p.m;
+  StatAcc acc;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < p.n_paths; q += stride) {
+    const float Y = yin[q];
+    float y[MR];
+    if (sdeg) {
+      int kb = 0;
+      float db = fabsf(Y - sz[0]);
+      for (int k = 1; k < m; ++k) {
+        const float d = fabsf(Y - sz[k]);
+        if (d < db) { db = d; kb = k; }
+      }
+#pragma unroll
+      for (int j = 0; j < MR; ++j) y[j] = sC[kb][j];
+    } else {
+      // Lagrange basis in the state on the marginal nodes (normalised barycentric product form)
+      float d[MR], pre[MR];
+#pragma unroll
+      for (int k = 0; k < MR; ++k) d[k] = (RT_M && k >= m) ? 1.0f : (Y - sz[k]);
+      pre[0] = 1.0f;
+#pragma unroll
+      for (int k = 1; k < MR; ++k) pre[k] = pre[k - 1] * d[k - 1];
+      float suf = 1.0f, den = 0.0f, lk[MR];
+#pragma unroll
+      for (int k = MR - 1; k >= 0; --k) {
+        lk[k] = sv[k] * (pre[k] * suf);
+        den += lk[k];
+        suf *= d[k];
+      }
+      const float rden = __fdividef(1.0f, den);
+#pragma unroll
+      for (int j = 0; j < MR; ++j) {
+        float a = 0.0f;
+#pragma unroll
+        for (int k = 0; k < MR; ++k) a = fmaf(lk[k], sC[k][j], a);
+        y[j] = a * rden;
+      }
+    }
+    // X_hat for (path, step) and g_m on the Gauss-Hermite grid
+    const uint64_t gp = p.path_offset + q;
+    float z4[4];
+    normals4_rk<false>(p, gp, (uint32_t)(step >> 2), z4[0], z4[1], z4[2], z4[3]);
+    const int r = step & 3;
+    const float Z = (r == 0) ? z4[0] : (r == 1) ? z4[1] : (r == 2) ? z4[2] : z4[3];
+    const float Yn = gm_eval<MR, RT_M>(p, Z, y);
+    yout[q] = Yn;
+    if (last && p.has_stats) stat_add(acc, p, Yn, 0.0, hist);
+  }
+  if (last && p.has_stats) stat_flush(acc, p, hist, red);
+}
+
+__global__ void fill_kernel(float* y, uint64_t n, float v) {
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (uint64_t)gridDim.x * blockDim.x)
+    y[q] = v;
+}
+
+// ------------------------------------------------------------------------------------------------
+size_t cdc_scratch_bytes() { return sizeof(CdcScratch); }
+
+int cdc_init_scratch(void* scratch, void* stream) {
+  CdcScratch h;
+  memset(&h, 0, sizeof h);
+  h.nslot = 1;
+  return (int)cudaMemcpyAsync(scratch, &h, sizeof h, cudaMemcpyHostToDevice, (cudaStream_t)stream);
+}
+
+// Runs all n_steps of the CDC scheme.  state: n_paths floats (may alias out rows, see host).
+int launch_cdc(const RunParams& p, const CdcLevels& lv, void* scratch, float* const* rows, int nrows, void* stream,
+               int num_sms) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CdcScratch* s = reinterpret_cast<CdcScratch*>(scratch);
+  const uint64_t n = p.n_paths;
+  const unsigned grid = (unsigned)(((n + 255) / 256) < (uint64_t)num_sms * 8 ? (n + 255) / 256 : (uint64_t)num_sms * 8);
+  // row 0 = Y0
+  fill_kernel<<<grid, 256, 0, st>>>(rows[0], n, p.y0);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return (int)e;
+  const size_t hist = (p.has_stats && p.n_bins > 0) ? sizeof(uint32_t) * (size_t)(p.n_bins + 2) : 0;
+  auto step_k = (p.m == 5) ? cdc_step_kernel<5, false> : (p.m == 7) ? cdc_step_kernel<7, false>
+                                                                    : cdc_step_kernel<kMaxM, true>;
+  if (hist > 48 * 1024) {
+    e = cudaFuncSetAttribute(step_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hist);
+    if (e != cudaSuccess) return (int)e;
+  }
+  for (int i = 0; i < p.n_steps; ++i) {
+    const float* yin = rows[(nrows == 1) ? 0 : i];
+    float* yout = rows[(nrows == 1) ? 0 : i + 1];
+    for (int pass = 0; pass < 4; ++pass) {
+      cdc_hist_kernel<<<grid, 256, 0, st>>>(yin, n, pass, s);
+      cdc_scan_kernel<<<1, 256, 0, st>>>(pass, p.m, s, lv);
+    }
+    if (p.colloc == kAnn) {
+      if (p.act == SL7_ACT_TANH) cdc_table_mlp_kernel<SL7_ACT_TANH><<<1, 256, 0, st>>>(p, s);
+      else cdc_table_mlp_kernel<SL7_ACT_SOFTPLUS><<<1, 256, 0, st>>>(p, s);
+    } else {
+      cdc_table_exact_kernel<<<1, kMaxM * kMaxM, 0, st>>>(p, s);
+    }
+    step_k<<<grid, 256, hist, st>>>(p, s, yin, yout, i, i == p.n_steps - 1 ? 1 : 0);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return (int)e;
+  }
+  return 0;
+}
+
+}  // namespace sl7

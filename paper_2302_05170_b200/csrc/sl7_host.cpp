@@ -53,6 +53,10 @@ struct sl7_ctx_s {
   size_t out_cap = 0;
   double* d_stats_scratch = nullptr;
   size_t stats_cap = 0;
+  // 7L-CDC scratch (selection histograms + table) and state buffer for STATS-only runs
+  void* d_cdc = nullptr;
+  float* d_state = nullptr;
+  size_t state_cap = 0;
   std::string err;
 };
 
@@ -435,6 +439,13 @@ sl7_status prepare(sl7_ctx c, double Y0, double dt, int32_t n_steps, const doubl
       return fail(c, SL7_EINVAL, "colloc");
   }
   if (o->flags & ~(SL7_FLAG_FAST_NORMALS | SL7_FLAG_SPECIALIZED)) return fail(c, SL7_EINVAL, "flags");
+  if (o->scheme != SL7_SCHEME_7L && o->scheme != SL7_SCHEME_CDC) return fail(c, SL7_EINVAL, "scheme");
+  if (o->scheme == SL7_SCHEME_CDC) {
+    if (o->ref != SL7_REF_NONE) return fail(c, SL7_EUNSUPPORTED, "scheme CDC: ref must be SL7_REF_NONE");
+    if (o->flags) return fail(c, SL7_EUNSUPPORTED, "scheme CDC: flags must be 0");
+    if (p.colloc == kAnn && o->prec != SL7_PREC_FP32)
+      return fail(c, SL7_EUNSUPPORTED, "scheme CDC: the m-row table runs in fp32 (prec must be SL7_PREC_FP32)");
+  }
   p.flags = (p.colloc == kAnn) ? 0u : o->flags;
   p.ref = (int)o->ref;
   if (o->ref == SL7_REF_GBM) {
@@ -464,7 +475,34 @@ sl7_status run(sl7_ctx c, RunParams& p, const sl7_run_opts* o, float* d_out, dou
     if (e) return cuda_fail(c, (cudaError_t)e, "zero stats");
   }
   int e;
-  if (p.colloc == kAnn && (o->prec == SL7_PREC_BF16 || o->prec == SL7_PREC_SPLIT)) {
+  if (o->scheme == SL7_SCHEME_CDC) {
+    // 7L-CDC: states in HBM between steps (FULL rows, the TERMINAL output, or context scratch)
+    if (!c->d_cdc) {
+      cudaError_t ce = cudaMalloc(&c->d_cdc, cdc_scratch_bytes());
+      if (ce != cudaSuccess) return cuda_fail(c, ce, "cudaMalloc(cdc scratch)");
+    }
+    e = cdc_init_scratch(c->d_cdc, o->stream);
+    if (e) return cuda_fail(c, (cudaError_t)e, "cdc scratch init");
+    std::vector<float*> rows;
+    if (p.out_mode == kFull) {
+      for (int i = 0; i <= p.n_steps; ++i) rows.push_back(d_out + (size_t)i * p.n_paths);
+    } else if (p.out_mode == kTerminal) {
+      rows.push_back(d_out);
+    } else {
+      if (c->state_cap < p.n_paths) {
+        if (c->d_state) cudaFree(c->d_state);
+        c->d_state = nullptr;
+        c->state_cap = 0;
+        cudaError_t ce = cudaMalloc(&c->d_state, p.n_paths * sizeof(float));
+        if (ce != cudaSuccess) return cuda_fail(c, ce, "cudaMalloc(cdc state)");
+        c->state_cap = p.n_paths;
+      }
+      rows.push_back(c->d_state);
+    }
+    CdcLevels lv;
+    for (int k = 0; k < kMaxM; ++k) lv.p[k] = (k < c->m) ? 0.5 * std::erfc(-c->x[k] / std::sqrt(2.0)) : 0.0;
+    e = launch_cdc(p, lv, c->d_cdc, rows.data(), (int)rows.size(), o->stream, c->num_sms);
+  } else if (p.colloc == kAnn && (o->prec == SL7_PREC_BF16 || o->prec == SL7_PREC_SPLIT)) {
     // per-run part of the TC parameters: layer 1 folded (as in RunParams) and pre-scaled in double
     TcParams t = c->tcp;
     const double sc = (c->act == SL7_ACT_TANH) ? 2.0 / std::log(2.0) : 1.0;
@@ -764,6 +802,8 @@ void sl7_destroy(sl7_ctx c) {
     if (c->d_wf32) cudaFree(c->d_wf32);
     if (c->d_wtc) cudaFree(c->d_wtc);
     if (c->d_wtc_split) cudaFree(c->d_wtc_split);
+    if (c->d_cdc) cudaFree(c->d_cdc);
+    if (c->d_state) cudaFree(c->d_state);
     if (c->d_out_scratch) cudaFree(c->d_out_scratch);
     if (c->d_stats_scratch) cudaFree(c->d_stats_scratch);
   }

@@ -97,6 +97,16 @@ struct TcParams {
   int split;          // 1: SL7_PREC_SPLIT
 };
 
+// 7L-CDC: quantile levels Phi(x_k) of the marginal collocation points (host, double).
+struct CdcLevels {
+  double p[kMaxM];
+};
+size_t cdc_scratch_bytes();
+int cdc_init_scratch(void* scratch, void* stream);
+// rows: nrows == 1 -> one in-place state buffer; nrows == n_steps + 1 -> FULL output rows.
+int launch_cdc(const RunParams& p, const CdcLevels& lv, void* scratch, float* const* rows, int nrows, void* stream,
+               int num_sms);
+
 // launchers (sl7_kernels.cu / sl7_tc.cu); return cudaError_t as int
 int launch_step_kernel(const RunParams& p, int prec, void* stream, int num_sms);
 int launch_tc_kernel(const RunParams& p, const TcParams& t, void* stream, int num_sms);
