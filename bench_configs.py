@@ -110,16 +110,20 @@ def main():
             ctx.load_weights(load_golden_blob(w.blob))
             lo, hi = (-3.0, 3.0) if w.process == "ou" else (0.0, 0.6)
             modes = [("ann_bf16_tcgen05", ctx, sl7.COLLOC_ANN, sl7.PREC_BF16, 0, w.theta, N),
-                     ("ann_fp32", ctx, sl7.COLLOC_ANN, sl7.PREC_FP32, 0, w.theta, N // 10)]
+                     ("ann_split_bf16x3_tcgen05", ctx, sl7.COLLOC_ANN, sl7.PREC_SPLIT, 0, w.theta, N),
+                     ("ann_fp32", ctx, sl7.COLLOC_ANN, sl7.PREC_FP32, 0, w.theta, N // 10),
+                     ("cdc_ann_fp32_table", ctx, sl7.COLLOC_ANN, sl7.PREC_FP32, -1, w.theta, N)]
             if w.process == "ou":
                 ex = sl7.Context(w.m, device=0)
                 modes += [("exact_ou_general", ex, sl7.COLLOC_EXACT_OU, sl7.PREC_FP32, 0, w.theta, N),
                           ("exact_ou_fast_specialized", ex, sl7.COLLOC_EXACT_OU, sl7.PREC_FP32,
                            sl7.FLAG_FAST_NORMALS | sl7.FLAG_SPECIALIZED, w.theta, N)]
             for label, c, colloc, prec, flags, theta, n_paths in modes:
-                ref = sl7.REF_OU if w.process == "ou" else sl7.REF_NONE
-                opts = sl7.make_opts(prec=prec, colloc=colloc, stream=stream, flags=flags, n_bins=4096,
-                                     hist_lo=lo, hist_hi=hi, shift=w.y0, ref=ref, ref_theta=w.theta)
+                cdc = flags == -1            # marker: 7L-CDC scheme
+                ref = sl7.REF_OU if (w.process == "ou" and not cdc) else sl7.REF_NONE
+                opts = sl7.make_opts(prec=prec, colloc=colloc, stream=stream, flags=0 if cdc else flags, n_bins=4096,
+                                     hist_lo=lo, hist_hi=hi, shift=w.y0, ref=ref, ref_theta=w.theta,
+                                     scheme=sl7.SCHEME_CDC if cdc else sl7.SCHEME_7L)
                 fn = (lambda c=c, theta=theta, opts=opts, n_paths=n_paths:
                       c.simulate(w.y0, w.dt, w.n_steps, theta, n_paths, w.seed, sl7.OUT_STATS, opts, stats=stats))
                 clk = ClockSampler(0)
