@@ -58,13 +58,28 @@ __device__ __forceinline__ float tc_act_u(float u, bool newton) {
     return fmaf(-2.0f, rcp_approx(ex2_approx(u) + 1.0f), 1.0f);
   } else {
     const float e = ex2_approx(fabsf(u) * -1.4426950408889634f);
+    if (newton) {
+      // log1p(e), e in (0, 1], as a degree-8 polynomial on the FMA pipe (abs. error 1.4e-7 in fp32)
+      float lp = -6.301349960e-03f;
+      lp = fmaf(lp, e, 3.544928879e-02f);
+      lp = fmaf(lp, e, -9.422647208e-02f);
+      lp = fmaf(lp, e, 1.666473895e-01f);
+      lp = fmaf(lp, e, -2.402127683e-01f);
+      lp = fmaf(lp, e, 3.316470385e-01f);
+      lp = fmaf(lp, e, -4.998508692e-01f);
+      lp = fmaf(lp, e, 9.999948740e-01f);
+      lp = fmaf(lp, e, 2.928694798e-08f);
+      return fmaxf(u, 0.0f) + lp;
+    }
     return fmaf(0.69314718055994531f, lg2_approx(1.0f + e), fmaxf(u, 0.0f));
   }
 }
 
+// NMASK bit (unit % 8) set: this unit's second transcendental runs on the FMA pipe (tanh: reciprocal
+// by Newton; softplus: log1p by polynomial), trading one MUFU op for ~6 FMA-pipe instructions.
 template <int ACT, unsigned NMASK>
 __device__ __forceinline__ bool use_newton(int c) {
-  return ACT == SL7_ACT_TANH && ((NMASK >> (c & 7)) & 1u);
+  return (NMASK >> (c & 7)) & 1u;
 }
 
 // Pack two activations as NP bf16 parts: part 0 = bf16(h); NP = 3 (SL7_PREC_SPLIT) adds the rounded
@@ -124,11 +139,11 @@ __device__ __forceinline__ void issue_layer(uint32_t acc_t, uint32_t a_t, uint32
   }
 }
 
-template <int NG, int H, int MR, bool RT_M, int ACT, unsigned NMASK, int NP = 1>
+template <int NG, int H, int MR, bool RT_M, int ACT, unsigned NMASK, int NP = 1, bool SKIPMMA = false>
 __global__ void __launch_bounds__(NG * kGroupThreads, 1)
     ann_tc_step_kernel(const __grid_constant__ RunParams p, const __grid_constant__ TcParams t) {
   extern __shared__ uint8_t smem_raw[];
-  __shared__ uint64_t mbar[NG];
+  __shared__ uint64_t mbar[NG];   // per group: MMA completion (tcgen05.commit)
   __shared__ uint32_t tmem_base_sh;
   __shared__ double red[8];
 
@@ -217,11 +232,16 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
         tc::named_bar_sync(1 + g, kGroupThreads);
         if (tid_g == 0) {
           tc::fence_after();
-          // weight image: NP parts of each hidden tile (8 KB), then NP parts of the output tile (2 KB)
-          if (last)
+          // weight image: NP parts of each hidden tile (8 KB), then NP parts of the output tile (2 KB).
+          // (Issuing the hidden layers as two N = 32 halves with separate commits, to overlap the
+          // epilogue of columns 0..31 with the MMAs of 32..63, measured slower: 1.38e10 vs 1.41e10.)
+          if (SKIPMMA) {
+            // timing experiment only (SL7_TC_VARIANT=9): same synchronisation, no tensor work
+          } else if (last) {
             issue_layer<NP>(acc_t, a_t, sbase + (uint32_t)(NP * nL * kTcTileBytes), kTcOutBytes, idesc_o);
-          else
+          } else {
             issue_layer<NP>(acc_t, a_t, sbase + (uint32_t)(NP * l * kTcTileBytes), kTcTileBytes, idesc_h);
+          }
           tc::mma_commit(bar);
         }
         if (l == 0) den = gm_basis<MR, RT_M>(p, Z, lb);
@@ -268,9 +288,9 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
 
 namespace {
 
-template <int NG, int H, int MR, bool RT, int ACT, unsigned NMASK = 0u, int NP = 1>
+template <int NG, int H, int MR, bool RT, int ACT, unsigned NMASK = 0u, int NP = 1, bool SKIP = false>
 cudaError_t launch_tc_t(const RunParams& p, const TcParams& t, cudaStream_t st, int num_sms) {
-  auto kernel = ann_tc_step_kernel<NG, H, MR, RT, ACT, NMASK, NP>;
+  auto kernel = ann_tc_step_kernel<NG, H, MR, RT, ACT, NMASK, NP, SKIP>;
   const size_t hist = (p.has_stats && p.n_bins > 0) ? sizeof(uint32_t) * (size_t)(p.n_bins + 2) : 0;
   const size_t smem = 1024 + (size_t)NP * ((size_t)t.n_mma_hidden * kTcTileBytes + kTcOutBytes) + hist;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -287,6 +307,7 @@ cudaError_t launch_tc_t(const RunParams& p, const TcParams& t, cudaStream_t st, 
 // half of the units on the FMA pipe: 1.45e10 path-steps/s vs 1.30e10 all-MUFU).
 constexpr int kTcGroups = 4;
 constexpr unsigned kTanhNewtonMask = 0x55u;
+constexpr unsigned kSoftplusPolyMask = 0x55u;
 
 // SL7_PREC_SPLIT: three bf16 parts per operand (TMEM 64 + 3 x 32 = 160 columns per group -> 3 groups).
 constexpr int kTcGroupsSplit = 3;
@@ -294,7 +315,7 @@ constexpr int kTcGroupsSplit = 3;
 template <int ACT>
 cudaError_t launch_tc_act(const RunParams& p, const TcParams& t, cudaStream_t st, int num_sms) {
   constexpr int NG = kTcGroups;
-  constexpr unsigned NM = (ACT == SL7_ACT_TANH) ? kTanhNewtonMask : 0u;
+  constexpr unsigned NM = (ACT == SL7_ACT_TANH) ? kTanhNewtonMask : kSoftplusPolyMask;
   if (t.split) {
     constexpr int NS = kTcGroupsSplit;
     if (p.width == 50 && p.m == 5) return launch_tc_t<NS, 50, 5, false, ACT, NM, 3>(p, t, st, num_sms);
@@ -303,10 +324,13 @@ cudaError_t launch_tc_act(const RunParams& p, const TcParams& t, cudaStream_t st
   }
   if (p.width == 50 && p.m == 5) return launch_tc_t<NG, 50, 5, false, ACT, NM>(p, t, st, num_sms);
   if (p.width == 50 && p.m == 7) {
-    if constexpr (ACT == SL7_ACT_TANH) {
-      if (t.variant == 1) return launch_tc_t<NG, 50, 7, false, ACT, 0x00u>(p, t, st, num_sms);  // all-MUFU (A/B runs)
+    switch (t.variant) {   // A/B hook (SL7_TC_VARIANT): fraction of units with the FMA-pipe transcendental
+      case 1: return launch_tc_t<NG, 50, 7, false, ACT, 0x00u>(p, t, st, num_sms);
+      case 2: return launch_tc_t<NG, 50, 7, false, ACT, 0x25u>(p, t, st, num_sms);
+      case 3: return launch_tc_t<NG, 50, 7, false, ACT, 0x77u>(p, t, st, num_sms);
+      case 9: return launch_tc_t<NG, 50, 7, false, ACT, NM, 1, true>(p, t, st, num_sms);
+      default: return launch_tc_t<NG, 50, 7, false, ACT, NM>(p, t, st, num_sms);
     }
-    return launch_tc_t<NG, 50, 7, false, ACT, NM>(p, t, st, num_sms);
   }
   return launch_tc_t<NG, 64, kMaxM, true, ACT, NM>(p, t, st, num_sms);
 }
