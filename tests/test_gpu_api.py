@@ -1,0 +1,114 @@
+"""C-ABI behaviour on the GPU: argument validation, chunked (resumed) runs, host-buffer entry point,
+degenerate sizes for every kernel family."""
+import numpy as np
+import pytest
+
+from oracle import sl7_oracle as O
+from sl7_inputs import load_golden_blob, workloads
+
+pytestmark = pytest.mark.gpu
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def test_validation_errors(gpu_lib):
+    sl7 = gpu_lib
+    torch = _torch()
+    ctx = sl7.Context(5)
+    out = torch.empty(10, dtype=torch.float32, device="cuda")
+    st = torch.zeros(sl7.stats_elems(8), dtype=torch.float64, device="cuda")
+
+    def call(dt=0.5, n_steps=2, n_paths=10, theta=(0.05, 0.2), mode=None, **kw):
+        o = sl7.make_opts(colloc=sl7.COLLOC_EXACT_GBM, **kw)
+        return ctx.simulate(1.0, dt, n_steps, theta, n_paths, 1, sl7.OUT_TERMINAL if mode is None else mode, o,
+                            out=out, stats=st)
+
+    for kw, msg in [(dict(dt=0.0), "dt"), (dict(dt=float("nan")), "dt"), (dict(n_steps=0), "n_steps"),
+                    (dict(n_paths=0), "n_paths"), (dict(theta=(0.05,)), "EXACT_GBM"),
+                    (dict(theta=(0.05, -0.2)), "sigma"), (dict(n_bins=20000, hist_lo=0, hist_hi=1), "n_bins"),
+                    (dict(n_bins=8, hist_lo=1, hist_hi=1), "hist_lo"), (dict(flags=8), "flags"),
+                    (dict(scheme=5), "scheme"), (dict(path_offset=(1 << 64) - 5), "overflows")]:
+        with pytest.raises(sl7.Sl7Error, match=msg):
+            call(**kw)
+    import ctypes
+    th = (ctypes.c_double * 2)(0.05, 0.2)
+    o = sl7.make_opts(colloc=sl7.COLLOC_EXACT_GBM)
+    st_ = sl7._lib.sl7_simulate(ctx._h, 1.0, 0.5, 2, th, 2, 10, 1, sl7.OUT_FULL, ctypes.byref(o), None, None)
+    assert st_ == sl7.EINVAL and b"d_out" in sl7._lib.sl7_last_error(ctx._h)
+    with pytest.raises(sl7.Sl7Error, match="ESTATE"):
+        ctx.simulate(1.0, 0.5, 2, (), 10, 1, sl7.OUT_TERMINAL, sl7.make_opts(colloc=sl7.COLLOC_ANN), out=out)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16", "split"])
+def test_chunked_accumulate_equals_single_run(gpu_lib, prec):
+    """Checkpoint/resume semantics: the counter-based RNG makes any path range recomputable, and
+    opts.accumulate sums chunk statistics into one vector."""
+    sl7 = gpu_lib
+    torch = _torch()
+    p = {"fp32": sl7.PREC_FP32, "bf16": sl7.PREC_BF16, "split": sl7.PREC_SPLIT}[prec]
+    w = workloads()["cfg2_ou"]
+    ctx = sl7.Context(w.m, list(w.dims), w.act)
+    ctx.load_weights(load_golden_blob(w.blob))
+    N = 40_001
+    kw = dict(prec=p, colloc=sl7.COLLOC_ANN, n_bins=256, hist_lo=-3, hist_hi=3, shift=0.0)
+    full = torch.zeros(sl7.stats_elems(256), dtype=torch.float64, device="cuda")
+    ctx.simulate(w.y0, w.dt, 8, w.theta, N, 7, sl7.OUT_STATS, sl7.make_opts(**kw), stats=full)
+    acc = torch.zeros_like(full)
+    for lo, n in [(0, 10_000), (10_000, 1), (10_001, 30_000)]:
+        ctx.simulate(w.y0, w.dt, 8, w.theta, n, 7, sl7.OUT_STATS, sl7.make_opts(path_offset=lo, accumulate=1, **kw),
+                     stats=acc)
+    torch.cuda.synchronize()
+    a, f = acc.cpu().numpy(), full.cpu().numpy()
+    assert a[0] == f[0] == N and np.array_equal(a[8:], f[8:])
+    np.testing.assert_allclose(a[2:6], f[2:6], rtol=1e-12)
+
+
+def test_host_entry_stats_only(gpu_lib):
+    sl7 = gpu_lib
+    torch = _torch()
+    ctx = sl7.Context(7)
+    opts = sl7.make_opts(colloc=sl7.COLLOC_EXACT_OU, n_bins=64, hist_lo=-2, hist_hi=3, shift=1.0,
+                         ref=sl7.REF_OU, ref_theta=(0.0, 1.0, 0.5))
+    h = np.empty(sl7.stats_elems(64))
+    _, _, up, down = ctx.simulate_host(1.0, 0.125, 16, (0.0, 1.0, 0.5), 100_000, 3, sl7.OUT_STATS, opts, None, h)
+    d = torch.zeros(sl7.stats_elems(64), dtype=torch.float64, device="cuda")
+    ctx.simulate(1.0, 0.125, 16, (0.0, 1.0, 0.5), 100_000, 3, sl7.OUT_STATS, opts, stats=d)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(h, d.cpu().numpy(), rtol=1e-12)
+    assert down == h.nbytes and h[0] == 100_000
+    s = sl7.stats_summary(h, opts)
+    assert s["strong_err"] < 1e-6      # exact OU collocation = Eq. 6.6 on the same normals
+
+
+@pytest.mark.parametrize("kind", ["exact", "fp32", "bf16", "split", "cdc"])
+def test_single_path_and_single_step(gpu_lib, kind):
+    sl7 = gpu_lib
+    torch = _torch()
+    w = workloads()["cfg0"]
+    blob = load_golden_blob(w.blob)
+    if kind == "exact":
+        ctx, colloc, theta, prec = sl7.Context(5), sl7.COLLOC_EXACT_GBM, w.theta, sl7.PREC_FP32
+    else:
+        ctx = sl7.Context(w.m, list(w.dims), w.act)
+        ctx.load_weights(blob)
+        colloc, theta = sl7.COLLOC_ANN, ()
+        prec = {"fp32": sl7.PREC_FP32, "bf16": sl7.PREC_BF16, "split": sl7.PREC_SPLIT, "cdc": sl7.PREC_FP32}[kind]
+    scheme = sl7.SCHEME_CDC if kind == "cdc" else sl7.SCHEME_7L
+    for n_paths, n_steps in [(1, 1), (1, 5), (129, 1)]:
+        o = sl7.make_opts(prec=prec, colloc=colloc, scheme=scheme)
+        out, _ = ctx.simulate(1.0, 0.5, n_steps, theta, n_paths, 5, sl7.OUT_FULL, o)
+        torch.cuda.synchronize()
+        Yd = out.double().cpu().numpy().reshape(n_steps + 1, n_paths)
+        spec = O.Spec(5, "gbm" if kind == "exact" else "ann", theta, 1.0, 0.5, n_steps, net=O.parse_blob(blob),
+                      quant="bf16" if kind == "bf16" else None)
+        Z = O.normals(5, np.arange(n_paths, dtype=np.uint64), n_steps)
+        tol = 5e-3 if kind == "bf16" else 1e-5
+        for i in range(n_steps):
+            if kind == "cdc":
+                ref, kap = O.cdc_step(spec, Yd[i], Z[i]), O.cdc_step_error_scale(spec, Yd[i], Z[i])
+            else:
+                ref, kap = O.step(spec, Yd[i], Z[i]), O.step_error_scale(spec, Yd[i], Z[i])
+            assert np.all(np.abs(Yd[i + 1] - ref) <= tol * kap), (kind, n_paths, n_steps, i)
