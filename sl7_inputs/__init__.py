@@ -140,6 +140,26 @@ def load_golden_blob(name: str) -> bytes:
         return f.read()
 
 
+# Training-set feature ranges (SPEC.md:180 for OU; GBM / CIR chosen to cover configs 0-4).  Row layout
+# (y_start, dt, theta...) with the SL7 theta order: GBM (mu, sigma), OU (Ybar, lam, sigma),
+# CIR (kappa, Ybar, sigma).
+FEATURE_RANGES = {
+    "gbm": ((0.2, 5.0), (1.0 / 64, 1.0), (0.0, 0.1), (0.1, 0.4)),
+    "ou": ((-2.0, 2.0), (0.05, 2.0), (-1.0, 1.0), (0.1, 2.0), (0.1, 1.0)),
+    "cir": ((0.01, 0.3), (1.0 / 64, 1.0), (0.5, 2.0), (0.05, 0.2), (0.1, 0.4)),
+}
+
+
+def sample_features(model: str, n_rows: int, seed: int = 0, dt_range=None) -> np.ndarray:
+    """Uniform feature rows over FEATURE_RANGES[model], float64 [n_rows][2 + n_theta].
+    dt_range overrides the dt column's range (small horizons keep oracle runs short)."""
+    rng = np.random.default_rng(seed)
+    rg = list(FEATURE_RANGES[model])
+    if dt_range is not None:
+        rg[1] = dt_range
+    return np.stack([rng.uniform(lo, hi, size=n_rows) for lo, hi in rg], axis=1)
+
+
 def path_ids(n_paths: int, offset: int = 0, stride: int = 1) -> np.ndarray:
     """Global path indices (uint64) of a contiguous or strided subset."""
     return (np.uint64(offset) + np.arange(n_paths, dtype=np.uint64) * np.uint64(stride)).astype(np.uint64)
