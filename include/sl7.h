@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define SL7_ABI_VERSION 1
+#define SL7_ABI_VERSION 2
 #define SL7_MAX_M 16          /* nodes per collocation grid */
 #define SL7_MAX_WIDTH 64      /* hidden width of the MLP */
 #define SL7_MAX_HIDDEN 6      /* hidden layers of the MLP */
@@ -202,6 +202,52 @@ sl7_status sl7_philox_u32(uint64_t seed, uint64_t path_offset, uint64_t n_paths,
  * = the fast variant the exact kernels use under that flag. */
 sl7_status sl7_normals(uint64_t seed, uint64_t path_offset, uint64_t n_paths, int32_t n_steps,
                        uint32_t flags, float* d_out, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * Euler-Maruyama comparator and offline training-set generation.
+ * --------------------------------------------------------------------------------------------- */
+
+/* SDE models of Eq. 6.1 with their Euler-Maruyama coefficients (Eq. 6.2):
+ *  GBM: a = mu Y,              b = sigma Y;            theta = (mu, sigma), sigma >= 0
+ *  OU:  a = lam (Ybar - Y),    b = sigma;              theta = (Ybar, lam, sigma), lam, sigma >= 0
+ *  CIR: a = kappa (Ybar - Y+), b = sigma sqrt(Y+);     theta = (kappa, Ybar, sigma), kappa, sigma >= 0,
+ *       Y+ = max(Y, 0) ("full truncation"; the plain scheme is undefined for Y < 0, R-22). */
+typedef enum { SL7_MODEL_GBM = 1, SL7_MODEL_OU = 2, SL7_MODEL_CIR = 3 } sl7_model;
+
+/* Euler-Maruyama paths on the path generator's RNG, the classical comparator of the 7L scheme
+ * (PAPER.md:32 Eq. 6.2; strong convergence contrast PAPER.md:16, :110).  Each large step dt is taken
+ * as `substeps` (K >= 1) equal sub-steps dtau = dt / K:
+ *     Y <- Y + a(Y) dtau + b(Y) sqrt(dtau) X,
+ * fine step k = i K + s of path p consuming normal Z_{4b + (k & 3)}, b = k >> 2, of the same Philox
+ * stream as sl7_simulate (so K = 1 shares the 7L scheme's normals step for step).  Outputs, d_out /
+ * d_stats layouts, path_offset sharding and asynchrony are those of sl7_simulate (FULL records the
+ * large steps).  opts: path_offset, stream, hist_lo/hi, shift, n_bins, accumulate, ref/ref_theta
+ * (the reference runs on the FINE normals: GBM exact, OU exact Eq. 6.6 transition per sub-step) and
+ * flags (SL7_FLAG_FAST_NORMALS only); prec, colloc and scheme are ignored.
+ * Errors: SL7_EINVAL (model, theta, substeps, n_steps * substeps > 2^31, as sl7_simulate), SL7_ECUDA. */
+sl7_status sl7_simulate_em(sl7_ctx ctx, sl7_model model, double Y0, double dt, int32_t n_steps,
+                           int32_t substeps, const double* theta, int32_t n_theta, uint64_t n_paths,
+                           uint64_t seed, sl7_out out_mode, const sl7_run_opts* opts, float* d_out,
+                           double* d_stats);
+
+/* Offline training-set generation (Algorithm I step 1; "the Euler-Maruyama scheme will
+ * be used to generate the training data set ... tiny time steps").
+ * h_features : HOST float64 rows [n_rows][2 + n_theta] = (y_start, dt, theta...) (theta order of
+ *              sl7_model; dt > 0).
+ * n_inner    : M >= m inner Monte Carlo paths per row.   dtau : target fine step, > 0.
+ * Row r runs K_r = ceil(dt_r / dtau) Euler sub-steps of dt_r / K_r on M paths with
+ * global ids path_offset + r M + q (q < M), each fine step k on Z_{p,k} as in sl7_simulate_em; its
+ * labels are the empirical quantiles of the M terminal values at the levels Phi(x_j) of the context's
+ * m Gauss-Hermite nodes (plotting position (k - 0.5)/M, linear interpolation between order statistics;
+ * non-finite values excluded; NaN labels if none is finite).
+ * d_terminal : device fp32 [n_rows][M] terminal values, or NULL (context scratch, processed in chunks).
+ * d_labels   : device fp64 [n_rows][m], ascending per row.
+ * opts: path_offset, stream, flags (SL7_FLAG_FAST_NORMALS only); the rest is ignored.
+ * Asynchronous on opts->stream (the feature rows are copied before return).  Errors: SL7_EINVAL
+ * (model, features, M, dtau, K_r > 2^31, path-id overflow), SL7_ENOMEM, SL7_ECUDA. */
+sl7_status sl7_training_set(sl7_ctx ctx, sl7_model model, const double* h_features, uint64_t n_rows,
+                            uint32_t n_inner, double dtau, uint64_t seed, const sl7_run_opts* opts,
+                            float* d_terminal, double* d_labels);
 
 /* Host setup introspection (no device needed): the context-independent grid of m nodes in
  * double (x[m], ascending) and barycentric weights w[m] = 1 / prod_{k != j}(x_j - x_k). */

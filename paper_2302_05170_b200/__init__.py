@@ -24,6 +24,7 @@ OUT_FULL, OUT_TERMINAL, OUT_STATS = 0, 1, 2
 PREC_FP32, PREC_TF32, PREC_BF16, PREC_SPLIT = 0, 1, 2, 3
 COLLOC_ANN, COLLOC_EXACT_GBM, COLLOC_EXACT_OU = 0, 1, 2
 REF_NONE, REF_GBM, REF_OU = 0, 1, 2
+MODEL_GBM, MODEL_OU, MODEL_CIR = 1, 2, 3
 STATS_HEAD = 8
 MAX_M = 16
 HAS_TC = True   # libsl7 has the tcgen05 (SL7_PREC_BF16) ANN kernel
@@ -61,7 +62,8 @@ class Sl7Error(RuntimeError):
 STATUS_NAMES = {0: "SL7_OK", 1: "SL7_EINVAL", 2: "SL7_ESTATE", 3: "SL7_EFORMAT", 4: "SL7_ENOMEM",
                 5: "SL7_ECUDA", 6: "SL7_ENONFINITE", 7: "SL7_EUNSUPPORTED"}
 
-EXPORTS = ["sl7_create", "sl7_load_weights", "sl7_simulate", "sl7_simulate_host", "sl7_stats",
+EXPORTS = ["sl7_create", "sl7_load_weights", "sl7_simulate", "sl7_simulate_host", "sl7_simulate_em",
+           "sl7_training_set", "sl7_stats",
            "sl7_philox_u32", "sl7_normals", "sl7_gh_grid", "sl7_out_elems", "sl7_stats_elems",
            "sl7_last_error", "sl7_status_str", "sl7_abi_version", "sl7_destroy"]
 
@@ -84,6 +86,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                c.POINTER(sl7_run_opts), fp, fp]
     L.sl7_simulate_host.argtypes = [vp, c.c_double, c.c_double, i32, dp, i32, u64, u64, c.c_int,
                                     c.POINTER(sl7_run_opts), fp, fp, c.POINTER(u64), c.POINTER(u64)]
+    L.sl7_simulate_em.argtypes = [vp, c.c_int, c.c_double, c.c_double, i32, i32, dp, i32, u64, u64, c.c_int,
+                                  c.POINTER(sl7_run_opts), fp, fp]
+    L.sl7_training_set.argtypes = [vp, c.c_int, dp, u64, c.c_uint32, c.c_double, u64, c.POINTER(sl7_run_opts),
+                                   fp, fp]
     L.sl7_stats.argtypes = [dp, c.POINTER(sl7_run_opts), c.POINTER(sl7_summary)]
     L.sl7_philox_u32.argtypes = [u64, u64, u64, c.c_uint32, vp, vp]
     L.sl7_normals.argtypes = [u64, u64, u64, i32, c.c_uint32, vp, vp]
@@ -99,7 +105,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L.sl7_abi_version.restype = i32
     L.sl7_destroy.argtypes = [vp]
     L.sl7_destroy.restype = None
-    for name in ("sl7_create", "sl7_load_weights", "sl7_simulate", "sl7_simulate_host", "sl7_stats",
+    for name in ("sl7_create", "sl7_load_weights", "sl7_simulate", "sl7_simulate_host", "sl7_simulate_em",
+                 "sl7_training_set", "sl7_stats",
                  "sl7_philox_u32", "sl7_normals", "sl7_gh_grid"):
         getattr(L, name).restype = c.c_int
     _lib = L
@@ -229,3 +236,30 @@ class Context:
                                       int(seed), out_mode, ctypes.byref(opts), po, ps, ctypes.byref(up),
                                       ctypes.byref(down)), self._h)
         return h_out, h_stats, up.value, down.value
+
+    def simulate_em(self, model, y0, dt, n_steps, substeps, theta, n_paths, seed, out_mode, opts, out=None,
+                    stats=None):
+        """sl7_simulate_em (Euler-Maruyama comparator) on torch device tensors; allocates out if None."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        if out is None and out_mode != OUT_STATS:
+            out = torch.empty(out_elems(n_steps, n_paths, out_mode), dtype=torch.float32, device=dev)
+        th = (ctypes.c_double * max(1, len(theta)))(*theta)
+        _check(_lib.sl7_simulate_em(self._h, int(model), float(y0), float(dt), int(n_steps), int(substeps), th,
+                                    len(theta), int(n_paths), int(seed), out_mode, ctypes.byref(opts), _dptr(out),
+                                    _dptr(stats)), self._h)
+        return out, stats
+
+    def training_set(self, model, features, n_inner, dtau, seed, opts, terminal=None, labels=None):
+        """sl7_training_set: features = host float64 [n_rows][2 + n_theta]; returns (terminal, labels) device
+        tensors (terminal None unless passed in: the library then uses its own scratch)."""
+        import numpy as np
+        import torch
+        F = np.ascontiguousarray(np.asarray(features, dtype=np.float64))
+        n_rows = F.shape[0]
+        if labels is None:
+            labels = torch.empty((n_rows, self.m), dtype=torch.float64, device=torch.device("cuda", self.device))
+        _check(_lib.sl7_training_set(self._h, int(model), F.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                     int(n_rows), int(n_inner), float(dtau), int(seed), ctypes.byref(opts),
+                                     _dptr(terminal), _dptr(labels)), self._h)
+        return terminal, labels

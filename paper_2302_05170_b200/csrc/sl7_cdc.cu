@@ -22,8 +22,6 @@
 
 namespace sl7 {
 
-constexpr int kCdcMaxT = 2 * kMaxM;   // targets: two order statistics per marginal point
-
 // Device-side scratch of the CDC pipeline (context-owned).
 struct CdcScratch {
   unsigned long long hist[kCdcMaxT][256];   // per-slot digit histograms of the current pass
@@ -39,14 +37,6 @@ struct CdcScratch {
   int degenerate;
   double zd[kMaxM];
 };
-
-__device__ __forceinline__ uint32_t f2key(float f) {
-  const uint32_t b = __float_as_uint(f);
-  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-}
-__device__ __forceinline__ float key2f(uint32_t k) {
-  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
-}
 
 // ---- pass p: histogram of digit p (bits [24 - 8p, 32 - 8p)) of the elements matching a slot prefix
 __global__ void __launch_bounds__(256) cdc_hist_kernel(const float* __restrict__ y, uint64_t n, int pass,

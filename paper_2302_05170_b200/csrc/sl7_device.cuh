@@ -303,6 +303,21 @@ __device__ __forceinline__ void hist_init(const RunParams& p, uint32_t* hist) {
     for (int b = threadIdx.x; b < p.n_bins + 2; b += blockDim.x) hist[b] = 0u;
 }
 
+// ------------------------------------------------------------------------------------------------
+// Order statistics by radix select (7L-CDC marginal points, training-set labels): the order-preserving
+// 32-bit key of an fp32 value (negative: all bits flipped; non-negative: sign bit set), so unsigned key
+// order = float order (-0 < +0; NaNs are excluded by the callers).  Two targets per quantile level.
+// ------------------------------------------------------------------------------------------------
+constexpr int kCdcMaxT = 2 * kMaxM;
+
+__device__ __forceinline__ uint32_t f2key(float f) {
+  const uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float key2f(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+
 // Path-wise exact reference state on the same normals.
 struct RefState {
   double r;   // GBM: sum of Z; OU: exact state

@@ -53,6 +53,11 @@ struct sl7_ctx_s {
   size_t out_cap = 0;
   double* d_stats_scratch = nullptr;
   size_t stats_cap = 0;
+  // training-set generator: feature rows and terminal-value scratch
+  EmRow* d_rows = nullptr;
+  size_t rows_cap = 0;
+  float* d_term_scratch = nullptr;
+  size_t term_cap = 0;
   // 7L-CDC scratch (selection histograms + table) and state buffer for STATS-only runs
   void* d_cdc = nullptr;
   float* d_state = nullptr;
@@ -300,19 +305,14 @@ sl7_status build_tc_image(sl7_ctx c) {
   return SL7_OK;
 }
 
-// Fill RunParams for one call; all validation happens here (synchronously, before any launch).
-sl7_status prepare(sl7_ctx c, double Y0, double dt, int32_t n_steps, const double* theta, int32_t n_theta,
-                   uint64_t n_paths, uint64_t seed, sl7_out out_mode, const sl7_run_opts* o, RunParams& p,
-                   bool have_out, bool have_stats) {
-  if (!c) return fail(c, SL7_EINVAL, "ctx is NULL");
-  if (!o) return fail(c, SL7_EINVAL, "opts is NULL");
-  if (!(dt > 0.0) || !std::isfinite(dt)) return fail(c, SL7_EINVAL, "dt must be finite and > 0");
-  if (n_steps < 1) return fail(c, SL7_EINVAL, "n_steps must be >= 1");
+// Part of RunParams common to every path kernel (7L, CDC, Euler-Maruyama): RNG, grid, outputs,
+// statistics and the strong-error reference (evaluated on steps of ref_dt, ref_steps of them).
+// Validates the arguments it consumes; the caller has validated dt and n_steps.
+sl7_status prepare_base(sl7_ctx c, double Y0, int32_t n_steps, double ref_dt, int64_t ref_steps, uint64_t n_paths, uint64_t seed,
+                        sl7_out out_mode, const sl7_run_opts* o, RunParams& p, bool have_out, bool have_stats) {
   if (n_paths < 1) return fail(c, SL7_EINVAL, "n_paths must be >= 1");
   if (o->path_offset + (n_paths - 1) < o->path_offset) return fail(c, SL7_EINVAL, "path_offset + n_paths - 1 overflows 2^64");
   if (!std::isfinite(Y0)) return fail(c, SL7_EINVAL, "Y0 must be finite");
-  if (n_theta < 0 || n_theta > SL7_MAX_THETA || (n_theta > 0 && !theta)) return fail(c, SL7_EINVAL, "theta/n_theta");
-  if (n_theta > 0 && !finite_all(theta, n_theta)) return fail(c, SL7_EINVAL, "theta must be finite");
   if (out_mode != SL7_OUT_FULL && out_mode != SL7_OUT_TERMINAL && out_mode != SL7_OUT_STATS)
     return fail(c, SL7_EINVAL, "out_mode");
   if (out_mode != SL7_OUT_STATS && !have_out) return fail(c, SL7_EINVAL, "d_out is NULL for a FULL/TERMINAL run");
@@ -351,6 +351,38 @@ sl7_status prepare(sl7_ctx c, double Y0, double dt, int32_t n_steps, const doubl
       p.xhi[j] = p.xlo[j] = p.w[j] = 0.0f;   // padded slot: w = 0 (no contribution)
     }
   }
+  p.ref = (int)o->ref;
+  if (o->ref == SL7_REF_GBM) {
+    const double mu = o->ref_theta[0], s = o->ref_theta[1];
+    p.ref_drift_T = (mu - 0.5 * s * s) * ref_dt * (double)ref_steps;
+    p.ref_vol = s * std::sqrt(ref_dt);
+  } else if (o->ref == SL7_REF_OU) {
+    const double ybar = o->ref_theta[0], lam = o->ref_theta[1], s = o->ref_theta[2];
+    const double e = std::exp(-lam * ref_dt);
+    p.ref_a = e;
+    p.ref_b = ybar * (1.0 - e);
+    p.ref_s = ou_std(lam, s, ref_dt);
+  }
+  p.has_stats = have_stats ? 1 : 0;
+  p.n_bins = have_stats ? o->n_bins : 0;
+  p.shift = o->shift;
+  p.hist_lo = o->hist_lo;
+  p.hist_scale = (p.n_bins > 0) ? (double)p.n_bins / (o->hist_hi - o->hist_lo) : 0.0;
+  return SL7_OK;
+}
+
+// Fill RunParams for one sl7_simulate call; all validation happens here (synchronously, before any launch).
+sl7_status prepare(sl7_ctx c, double Y0, double dt, int32_t n_steps, const double* theta, int32_t n_theta,
+                   uint64_t n_paths, uint64_t seed, sl7_out out_mode, const sl7_run_opts* o, RunParams& p,
+                   bool have_out, bool have_stats) {
+  if (!c) return fail(c, SL7_EINVAL, "ctx is NULL");
+  if (!o) return fail(c, SL7_EINVAL, "opts is NULL");
+  if (!(dt > 0.0) || !std::isfinite(dt)) return fail(c, SL7_EINVAL, "dt must be finite and > 0");
+  if (n_steps < 1) return fail(c, SL7_EINVAL, "n_steps must be >= 1");
+  if (n_theta < 0 || n_theta > SL7_MAX_THETA || (n_theta > 0 && !theta)) return fail(c, SL7_EINVAL, "theta/n_theta");
+  if (n_theta > 0 && !finite_all(theta, n_theta)) return fail(c, SL7_EINVAL, "theta must be finite");
+  sl7_status st = prepare_base(c, Y0, n_steps, dt, n_steps, n_paths, seed, out_mode, o, p, have_out, have_stats);
+  if (st != SL7_OK) return st;
   switch (o->colloc) {
     case SL7_COLLOC_EXACT_GBM: {
       if (n_theta != 2) return fail(c, SL7_EINVAL, "EXACT_GBM needs theta = (mu, sigma)");
@@ -447,23 +479,58 @@ sl7_status prepare(sl7_ctx c, double Y0, double dt, int32_t n_steps, const doubl
       return fail(c, SL7_EUNSUPPORTED, "scheme CDC: the m-row table runs in fp32 (prec must be SL7_PREC_FP32)");
   }
   p.flags = (p.colloc == kAnn) ? 0u : o->flags;
-  p.ref = (int)o->ref;
-  if (o->ref == SL7_REF_GBM) {
-    const double mu = o->ref_theta[0], s = o->ref_theta[1];
-    p.ref_drift_T = (mu - 0.5 * s * s) * dt * n_steps;
-    p.ref_vol = s * std::sqrt(dt);
-  } else if (o->ref == SL7_REF_OU) {
-    const double ybar = o->ref_theta[0], lam = o->ref_theta[1], s = o->ref_theta[2];
-    const double e = std::exp(-lam * dt);
-    p.ref_a = e;
-    p.ref_b = ybar * (1.0 - e);
-    p.ref_s = ou_std(lam, s, dt);
+  return SL7_OK;
+}
+
+// Euler-Maruyama constants of one (model, theta, dtau); shared by sl7_simulate_em and sl7_training_set so
+// that a training row and the equivalent EM call use bit-identical coefficients.
+sl7_status em_constants(sl7_ctx c, int model, const double* theta, int32_t n_theta, double dtau, float& a, float& s,
+                        float& ybar) {
+  if (model != SL7_MODEL_GBM && model != SL7_MODEL_OU && model != SL7_MODEL_CIR) return fail(c, SL7_EINVAL, "model");
+  const int need = (model == SL7_MODEL_GBM) ? 2 : 3;
+  if (n_theta != need || !theta) return fail(c, SL7_EINVAL, "theta: model %d needs %d parameters", model, need);
+  if (!finite_all(theta, need)) return fail(c, SL7_EINVAL, "theta must be finite");
+  const double sq = std::sqrt(dtau);
+  if (model == SL7_MODEL_GBM) {
+    if (theta[1] < 0) return fail(c, SL7_EINVAL, "theta: sigma >= 0");
+    a = (float)(theta[0] * dtau);
+    s = (float)(theta[1] * sq);
+    ybar = 0.0f;
+  } else {
+    // OU (Ybar, lam, sigma); CIR (kappa, Ybar, sigma)
+    const double rate = (model == SL7_MODEL_OU) ? theta[1] : theta[0];
+    const double mean = (model == SL7_MODEL_OU) ? theta[0] : theta[1];
+    if (rate < 0 || theta[2] < 0) return fail(c, SL7_EINVAL, "theta: rate >= 0 and sigma >= 0");
+    a = (float)(rate * dtau);
+    s = (float)(theta[2] * sq);
+    ybar = (float)mean;
   }
-  p.has_stats = have_stats ? 1 : 0;
-  p.n_bins = have_stats ? o->n_bins : 0;
-  p.shift = o->shift;
-  p.hist_lo = o->hist_lo;
-  p.hist_scale = (p.n_bins > 0) ? (double)p.n_bins / (o->hist_hi - o->hist_lo) : 0.0;
+  return SL7_OK;
+}
+
+sl7_status prepare_em(sl7_ctx c, int model, double Y0, double dt, int32_t n_steps, int32_t substeps, const double* theta,
+                      int32_t n_theta, uint64_t n_paths, uint64_t seed, sl7_out out_mode, const sl7_run_opts* o,
+                      RunParams& p, bool have_out, bool have_stats) {
+  if (!c) return fail(c, SL7_EINVAL, "ctx is NULL");
+  if (!o) return fail(c, SL7_EINVAL, "opts is NULL");
+  if (!(dt > 0.0) || !std::isfinite(dt)) return fail(c, SL7_EINVAL, "dt must be finite and > 0");
+  if (n_steps < 1) return fail(c, SL7_EINVAL, "n_steps must be >= 1");
+  if (substeps < 1) return fail(c, SL7_EINVAL, "substeps must be >= 1");
+  if ((int64_t)n_steps * substeps > (int64_t)1 << 31) return fail(c, SL7_EINVAL, "n_steps * substeps > 2^31");
+  if (o->flags & ~SL7_FLAG_FAST_NORMALS) return fail(c, SL7_EINVAL, "flags (EM: SL7_FLAG_FAST_NORMALS only)");
+  const double dtau = dt / substeps;
+  float a, s, yb;
+  sl7_status st = em_constants(c, model, theta, n_theta, dtau, a, s, yb);
+  if (st != SL7_OK) return st;
+  st = prepare_base(c, Y0, n_steps, dtau, (int64_t)n_steps * substeps, n_paths, seed, out_mode, o, p, have_out, have_stats);
+  if (st != SL7_OK) return st;
+  p.em_model = model;
+  p.em_K = substeps;
+  p.em_a = a;
+  p.em_s = s;
+  p.em_ybar = yb;
+  p.flags = o->flags;
+  p.colloc = -1;
   return SL7_OK;
 }
 
@@ -475,7 +542,9 @@ sl7_status run(sl7_ctx c, RunParams& p, const sl7_run_opts* o, float* d_out, dou
     if (e) return cuda_fail(c, (cudaError_t)e, "zero stats");
   }
   int e;
-  if (o->scheme == SL7_SCHEME_CDC) {
+  if (p.em_model != 0) {
+    e = launch_em(p, o->stream, c->num_sms);
+  } else if (o->scheme == SL7_SCHEME_CDC) {
     // 7L-CDC: states in HBM between steps (FULL rows, the TERMINAL output, or context scratch)
     if (!c->d_cdc) {
       cudaError_t ce = cudaMalloc(&c->d_cdc, cdc_scratch_bytes());
@@ -677,6 +746,100 @@ sl7_status sl7_simulate(sl7_ctx c, double Y0, double dt, int32_t n_steps, const 
   return run(c, p, opts, out_mode == SL7_OUT_STATS ? nullptr : d_out, d_stats);
 }
 
+sl7_status sl7_simulate_em(sl7_ctx c, sl7_model model, double Y0, double dt, int32_t n_steps, int32_t substeps,
+                           const double* theta, int32_t n_theta, uint64_t n_paths, uint64_t seed, sl7_out out_mode,
+                           const sl7_run_opts* opts, float* d_out, double* d_stats) {
+  RunParams p;
+  sl7_status s = prepare_em(c, (int)model, Y0, dt, n_steps, substeps, theta, n_theta, n_paths, seed, out_mode, opts, p,
+                            d_out != nullptr, d_stats != nullptr);
+  if (s != SL7_OK) return s;
+  DeviceGuard g(c->device);
+  if (!g.ok) return fail(c, SL7_ECUDA, "cudaSetDevice(%d)", c->device);
+  return run(c, p, opts, out_mode == SL7_OUT_STATS ? nullptr : d_out, d_stats);
+}
+
+sl7_status sl7_training_set(sl7_ctx c, sl7_model model, const double* F, uint64_t n_rows, uint32_t M, double dtau,
+                            uint64_t seed, const sl7_run_opts* o, float* d_term, double* d_labels) {
+  if (!c) return fail(c, SL7_EINVAL, "ctx is NULL");
+  if (!o) return fail(c, SL7_EINVAL, "opts is NULL");
+  if (model != SL7_MODEL_GBM && model != SL7_MODEL_OU && model != SL7_MODEL_CIR) return fail(c, SL7_EINVAL, "model");
+  if (!F) return fail(c, SL7_EINVAL, "h_features is NULL");
+  if (n_rows < 1) return fail(c, SL7_EINVAL, "n_rows must be >= 1");
+  if (M < (uint32_t)c->m) return fail(c, SL7_EINVAL, "n_inner must be >= m");
+  if (!(dtau > 0.0) || !std::isfinite(dtau)) return fail(c, SL7_EINVAL, "dtau must be finite and > 0");
+  if (!d_labels) return fail(c, SL7_EINVAL, "d_labels is NULL");
+  if (o->flags & ~SL7_FLAG_FAST_NORMALS) return fail(c, SL7_EINVAL, "flags (SL7_FLAG_FAST_NORMALS only)");
+  if (n_rows > UINT64_MAX / M || o->path_offset + (n_rows * M - 1) < o->path_offset)
+    return fail(c, SL7_EINVAL, "path_offset + n_rows * n_inner - 1 overflows 2^64");
+  const int nt = (model == SL7_MODEL_GBM) ? 2 : 3, nf = 2 + nt;
+  std::vector<EmRow> rows(n_rows);
+  for (uint64_t r = 0; r < n_rows; ++r) {
+    const double* f = F + r * nf;
+    if (!std::isfinite(f[0])) return fail(c, SL7_EINVAL, "features[%llu]: y_start must be finite", (unsigned long long)r);
+    if (!(f[1] > 0.0) || !std::isfinite(f[1])) return fail(c, SL7_EINVAL, "features[%llu]: dt must be finite and > 0", (unsigned long long)r);
+    const double K = std::max(1.0, std::ceil(f[1] / dtau));
+    if (K > 2147483648.0) return fail(c, SL7_EINVAL, "features[%llu]: ceil(dt / dtau) > 2^31", (unsigned long long)r);
+    EmRow& er = rows[r];
+    sl7_status st = em_constants(c, (int)model, f + 2, nt, f[1] / K, er.a, er.s, er.ybar);
+    if (st != SL7_OK) return fail(c, st, "features[%llu]: %s", (unsigned long long)r, c->err.c_str());
+    er.y0 = (float)f[0];
+    er.K = (int32_t)K;
+  }
+  DeviceGuard g(c->device);
+  if (!g.ok) return fail(c, SL7_ECUDA, "cudaSetDevice(%d)", c->device);
+  RunParams p;
+  std::memset(&p, 0, sizeof p);
+  p.key0 = (uint32_t)seed;
+  p.key1 = (uint32_t)(seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    p.rk0[r] = p.key0 + (uint32_t)r * 0x9E3779B9u;
+    p.rk1[r] = p.key1 + (uint32_t)r * 0xBB67AE85u;
+  }
+  p.path_offset = o->path_offset;
+  p.em_model = (int)model;
+  p.flags = o->flags;
+  CdcLevels lv;
+  for (int k = 0; k < kMaxM; ++k) lv.p[k] = (k < c->m) ? 0.5 * std::erfc(-c->x[k] / std::sqrt(2.0)) : 0.0;
+  // rows per chunk: all of them into d_terminal, else a 1 GiB scratch; at most 2^31 - 1 blocks per launch
+  const uint64_t tpr = (M + 255u) / 256u;
+  uint64_t chunk = d_term ? n_rows : std::max<uint64_t>(1, std::min<uint64_t>(n_rows, (256ull << 20) / M));
+  chunk = std::min<uint64_t>(chunk, 0x7FFFFFFFull / tpr);
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(o->stream);
+  cudaError_t e;
+  if (c->rows_cap < chunk) {
+    if (c->d_rows) cudaFree(c->d_rows);
+    c->d_rows = nullptr;
+    c->rows_cap = 0;
+    e = cudaMalloc(&c->d_rows, chunk * sizeof(EmRow));
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaMalloc(feature rows)");
+    c->rows_cap = chunk;
+  }
+  if (!d_term && c->term_cap < chunk * M) {
+    if (c->d_term_scratch) cudaFree(c->d_term_scratch);
+    c->d_term_scratch = nullptr;
+    c->term_cap = 0;
+    e = cudaMalloc(&c->d_term_scratch, chunk * M * sizeof(float));
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaMalloc(terminal scratch)");
+    c->term_cap = chunk * M;
+  }
+  std::vector<EmRow> part;
+  for (uint64_t start = 0; start < n_rows; start += chunk) {
+    const uint64_t nr = std::min(chunk, n_rows - start);
+    part.assign(rows.begin() + start, rows.begin() + start + nr);
+    for (uint64_t r = 0; r < nr; ++r) part[r].row = (uint32_t)r;
+    // longest rows first: the block scheduler then fills the tail with short rows
+    std::stable_sort(part.begin(), part.end(), [](const EmRow& a, const EmRow& b) { return a.K > b.K; });
+    e = cudaMemcpyAsync(c->d_rows, part.data(), nr * sizeof(EmRow), cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, "H2D feature rows");
+    float* term = d_term ? d_term + start * M : c->d_term_scratch;
+    int k = launch_em_rows(p, c->d_rows, (uint32_t)nr, M, start, term, o->stream);
+    if (k) return cuda_fail(c, (cudaError_t)k, "training-set EM kernel");
+    k = launch_row_quantiles(term, (uint32_t)nr, M, c->m, lv, d_labels + start * c->m, o->stream);
+    if (k) return cuda_fail(c, (cudaError_t)k, "training-set quantile kernel");
+  }
+  return SL7_OK;
+}
+
 sl7_status sl7_simulate_host(sl7_ctx c, double Y0, double dt, int32_t n_steps, const double* theta, int32_t n_theta,
                              uint64_t n_paths, uint64_t seed, sl7_out out_mode, const sl7_run_opts* opts, float* h_out,
                              double* h_stats, uint64_t* h2d_bytes, uint64_t* d2h_bytes) {
@@ -806,6 +969,8 @@ void sl7_destroy(sl7_ctx c) {
     if (c->d_state) cudaFree(c->d_state);
     if (c->d_out_scratch) cudaFree(c->d_out_scratch);
     if (c->d_stats_scratch) cudaFree(c->d_stats_scratch);
+    if (c->d_rows) cudaFree(c->d_rows);
+    if (c->d_term_scratch) cudaFree(c->d_term_scratch);
   }
   delete c;
 }

@@ -62,6 +62,17 @@ struct RunParams {
   const float* wdev;     // FP32 kernel: hidden + output weights (layout: WeightLayoutF32)
   const void* wtc;       // TC kernel: packed bf16 operand images (layout: sl7_tc.cu)
   const float* btc;      // TC kernel: fp32 biases [(L-1)][64] + out bias [16]
+  // ---- Euler-Maruyama (sl7_simulate_em): Y <- Y + a(Y) dtau + b(Y) sqrt(dtau) Z, K sub-steps per step
+  int em_model;          // sl7_model
+  int em_K;
+  float em_a, em_s, em_ybar;   // GBM: a = mu dtau, s = sigma sqrt(dtau); OU / CIR: a = lam dtau, s, ybar
+};
+
+// One feature row of the training-set generator (sl7_training_set), constants as in RunParams.
+struct EmRow {
+  float y0, a, s, ybar;
+  int32_t K;      // Euler sub-steps of dt / K
+  uint32_t row;   // output row within the chunk
 };
 
 // FP32-kernel weight image: for hidden layer l = 1..L-1: W[H][HS] then b[H] padded to a multiple of 4
@@ -113,5 +124,11 @@ int launch_tc_kernel(const RunParams& p, const TcParams& t, void* stream, int nu
 int launch_philox_u32(uint64_t seed, uint64_t off, uint64_t n, uint32_t block, uint32_t* out, void* stream);
 int launch_normals(uint64_t seed, uint64_t off, uint64_t n, int n_steps, bool fast, float* out, void* stream);
 int launch_zero_stats(double* stats, size_t n, void* stream);
+// sl7_em.cu
+int launch_em(const RunParams& p, void* stream, int num_sms);
+int launch_em_rows(const RunParams& p, const EmRow* d_rows, uint32_t n_rows, uint32_t M, uint64_t row_base,
+                   float* term, void* stream);
+int launch_row_quantiles(const float* term, uint32_t n_rows, uint32_t M, int m, const CdcLevels& lv,
+                         double* labels, void* stream);
 
 }  // namespace sl7

@@ -48,7 +48,7 @@ def test_library_is_sm100a(lib):
 
 
 def test_abi_version_and_sizes(lib):
-    assert lib.sl7_abi_version() == 1
+    assert lib.sl7_abi_version() == 2
     assert lib.sl7_out_elems(64, 1000, sl7.OUT_FULL) == 65 * 1000
     assert lib.sl7_out_elems(64, 1000, sl7.OUT_TERMINAL) == 1000
     assert lib.sl7_out_elems(64, 1000, sl7.OUT_STATS) == 0
