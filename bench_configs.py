@@ -7,6 +7,11 @@ launch, CUDA events on the launch stream, NVML clocks sampled during the timed r
 cfg2: OU (Ybar=0, lam=1, sigma=0.5, Y0=1) and CIR (kappa=1, Ybar=0.1, sigma=0.3, Y0=0.1), T=2, 16 steps,
       m=7, [5,50,50,50,50,7] softplus (theta as network input), 1e8 paths, STATS (moments + 4096-bin
       histogram).  Modes: ANN-BF16 (tcgen05), ANN-FP32, exact OU (general / specialised).
+em:   Euler-Maruyama comparator on cfg2's OU and CIR, 16 large steps of 0.125 with
+      K = 1, 8, 125 sub-steps (dtau = 1e-3 at K = 125), STATS + strong error vs the exact OU solution on
+      the same fine normals; the 7L lines of cfg2 give the contrast.  Unit: fine path-steps/s.
+train: training-set generation (§8(f) row 2): 4096 OU feature rows over SPEC.md:180's ranges
+      (dt in [0.05, 2]), M = 1e5 inner paths, dtau = 1e-3 (K_r = ceil(dt/dtau) <= 2000), labels at m = 7.
 cfg3: GBM, T=1, 64 steps, m=5, 2e8 paths, FULL step-major path tensor (65 x 2e8 fp32 = 52 GB in HBM).
       Modes: exact GBM with fast normals + closed-form g_m (HBM-store-bound), exact GBM general,
       ANN-BF16 (tcgen05).  Roofline: bound "hbm", algorithmic bytes = 4 (n+1) N_P per launch.
@@ -46,11 +51,13 @@ def timed_launches(fn, steps, warmup, flush, stream):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--config", default="all", choices=["cfg2", "cfg3", "all"])
+    ap.add_argument("--config", default="all", choices=["cfg2", "cfg3", "em", "train", "all"])
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--cfg3-paths", type=int, default=200_000_000)
     ap.add_argument("--cfg2-paths", type=int, default=100_000_000)
+    ap.add_argument("--train-rows", type=int, default=4096)
+    ap.add_argument("--train-inner", type=int, default=100_000)
     a = ap.parse_args()
 
     import torch
@@ -100,6 +107,75 @@ def main():
                   "clocks": clk.summary()})
         del out
         torch.cuda.empty_cache()
+
+    # issue roofline of the RNG-bound kernels: thread-instructions/s = SMs x 4 schedulers x 32 lanes x clock;
+    # instructions per fine path-step with the fast normals, counted in the SASS of em_rows_kernel's
+    # unrolled OU loop body: 156 per Philox block of 4 fine steps (Philox4x32-10 ~56, two fast
+    # Box-Muller pairs ~80, four Euler updates 12, loop 8) = 39.  frac is then the issue-slot utilisation.
+    issue_peak = n_sms * 4 * 32 * sm_max * 1e6
+    em_instr = 39.0
+
+    if a.config in ("em", "all"):
+        from sl7_inputs import CIR_THETA, OU_THETA
+        stats = torch.zeros(sl7.stats_elems(4096), dtype=torch.float64, device=dev)
+        ctx = sl7.Context(7, device=0)
+        for proc, theta, y0, model, lo, hi in [("ou", OU_THETA, 1.0, sl7.MODEL_OU, -3.0, 3.0),
+                                               ("cir", CIR_THETA, 0.1, sl7.MODEL_CIR, 0.0, 0.6)]:
+            for K, N in [(1, 100_000_000), (8, 25_000_000), (125, 2_000_000)]:
+                for fast in (False, True):
+                    flags = sl7.FLAG_FAST_NORMALS if fast else 0
+                    ref = sl7.REF_OU if proc == "ou" else sl7.REF_NONE
+                    opts = sl7.make_opts(stream=stream, n_bins=4096, hist_lo=lo, hist_hi=hi, shift=y0, ref=ref,
+                                         ref_theta=theta, flags=flags)
+                    fn = (lambda opts=opts, K=K, N=N, model=model, theta=theta, y0=y0:
+                          ctx.simulate_em(model, y0, 0.125, 16, K, theta, N, 2302051702, sl7.OUT_STATS, opts,
+                                          stats=stats))
+                    clk = ClockSampler(0)
+                    clk.start()
+                    ms, ms_min = timed_launches(fn, a.steps, a.warmup, flush, stream)
+                    clk.stop()
+                    s = sl7.stats_summary(stats.cpu().numpy(), opts)
+                    rate = N * 16 * K / (ms * 1e-3)
+                    line = {"config": "em_" + proc, "mode": "euler_maruyama_K%d%s" % (K, "_fast" if fast else ""),
+                            "metric": "Euler-Maruyama fine path-steps/sec (device-timed)", "value": rate,
+                            "unit": "fine path-steps/s", "ms_per_launch": ms, "paths": N, "n_steps": 16,
+                            "substeps": K, "dtau": 0.125 / K,
+                            "terminal": {k: s[k] for k in ("mean", "var", "strong_err")}, "clocks": clk.summary()}
+                    if fast:
+                        ach = rate * em_instr
+                        line["roofline"] = {"bound": "alu", "pipe": "issue", "achieved": ach / 1e12,
+                                            "peak": issue_peak / 1e12, "unit": "T thread-instr/s",
+                                            "frac": ach / issue_peak,
+                                            "algorithmic": "%.0f instructions per fine path-step" % em_instr}
+                    emit(line)
+
+    if a.config in ("train", "all"):
+        import numpy as np
+        from sl7_inputs import sample_features
+        R, M, dtau, m = a.train_rows, a.train_inner, 1e-3, 7
+        F = sample_features("ou", R, seed=2302051705)
+        K = np.maximum(1, np.ceil(F[:, 1] / dtau))
+        fine = float(K.sum()) * M
+        ctx = sl7.Context(m, device=0)
+        labels = torch.empty((R, m), dtype=torch.float64, device=dev)
+        for fast in (False, True):
+            opts = sl7.make_opts(stream=stream, flags=sl7.FLAG_FAST_NORMALS if fast else 0)
+            fn = (lambda opts=opts: ctx.training_set(sl7.MODEL_OU, F, M, dtau, 2302051705, opts, labels=labels))
+            clk = ClockSampler(0)
+            clk.start()
+            ms, ms_min = timed_launches(fn, a.steps, a.warmup, flush, stream)
+            clk.stop()
+            rate = fine / (ms * 1e-3)
+            line = {"config": "train_ou", "mode": "training_set%s" % ("_fast" if fast else ""),
+                    "metric": "training rows/sec (device-timed)", "value": R / (ms * 1e-3), "unit": "rows/s",
+                    "fine_path_steps_per_s": rate, "ms_per_launch": ms, "rows": R, "inner_paths": M, "dtau": dtau,
+                    "mean_substeps": float(K.mean()), "m": m, "clocks": clk.summary()}
+            if fast:
+                ach = rate * em_instr
+                line["roofline"] = {"bound": "alu", "pipe": "issue", "achieved": ach / 1e12, "peak": issue_peak / 1e12,
+                                    "unit": "T thread-instr/s", "frac": ach / issue_peak,
+                                    "algorithmic": "%.0f instructions per fine path-step" % em_instr}
+            emit(line)
 
     if a.config in ("cfg2", "all"):
         N = a.cfg2_paths

@@ -50,19 +50,39 @@ __global__ void __launch_bounds__(256) em_kernel(const __grid_constant__ RunPara
     if (full) *o = Y;
     RefState rs;
     if (REF_ON) ref_init(rs, p);
-    float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
-    uint32_t j = 0;   // fine step
-    for (int i = 0; i < p.n_steps; ++i) {
-      for (int k = 0; k < p.em_K; ++k, ++j) {
-        if ((j & 3u) == 0u) normals4_rk<FAST>(p, gp, j >> 2, z0, z1, z2, z3);
-        const float Z = z0;
-        z0 = z1; z1 = z2; z2 = z3;
-        Y = em_step<MODEL>(Y, Z, p.em_a, p.em_s, p.em_ybar);
-        if (REF_ON) ref_step(rs, p, Z);
+    if ((p.em_K & 3) == 0) {
+      // K a multiple of 4: each large step is K/4 whole Philox blocks (no per-step rotation)
+      uint32_t blk = 0;
+      for (int i = 0; i < p.n_steps; ++i) {
+        for (int b = 0; b < (p.em_K >> 2); ++b, ++blk) {
+          float z[4];
+          normals4_rk<FAST>(p, gp, blk, z[0], z[1], z[2], z[3]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            Y = em_step<MODEL>(Y, z[u], p.em_a, p.em_s, p.em_ybar);
+            if (REF_ON) ref_step(rs, p, z[u]);
+          }
+        }
+        if (full) {
+          o += p.n_paths;
+          *o = Y;
+        }
       }
-      if (full) {
-        o += p.n_paths;
-        *o = Y;
+    } else {
+      float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
+      uint32_t j = 0;   // fine step
+      for (int i = 0; i < p.n_steps; ++i) {
+        for (int k = 0; k < p.em_K; ++k, ++j) {
+          if ((j & 3u) == 0u) normals4_rk<FAST>(p, gp, j >> 2, z0, z1, z2, z3);
+          const float Z = z0;
+          z0 = z1; z1 = z2; z2 = z3;
+          Y = em_step<MODEL>(Y, Z, p.em_a, p.em_s, p.em_ybar);
+          if (REF_ON) ref_step(rs, p, Z);
+        }
+        if (full) {
+          o += p.n_paths;
+          *o = Y;
+        }
       }
     }
     if (p.out_mode == kTerminal) p.out[q] = Y;
@@ -81,12 +101,19 @@ __global__ void __launch_bounds__(256) em_rows_kernel(const __grid_constant__ Ru
   if (q >= M) return;
   const uint64_t gp = p.path_offset + (row_base + r.row) * (uint64_t)M + q;
   float Y = r.y0;
-  float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
-  for (uint32_t j = 0; j < (uint32_t)r.K; ++j) {
-    if ((j & 3u) == 0u) normals4_rk<FAST>(p, gp, j >> 2, z0, z1, z2, z3);
-    const float Z = z0;
-    z0 = z1; z1 = z2; z2 = z3;
-    Y = em_step<MODEL>(Y, Z, r.a, r.s, r.ybar);
+  // fine steps in Philox blocks of four (no per-step buffer rotation or block test), then the remainder
+  const uint32_t nb = (uint32_t)r.K >> 2, rem = (uint32_t)r.K & 3u;
+  float z[4];
+  for (uint32_t b = 0; b < nb; ++b) {
+    normals4_rk<FAST>(p, gp, b, z[0], z[1], z[2], z[3]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) Y = em_step<MODEL>(Y, z[u], r.a, r.s, r.ybar);
+  }
+  if (rem) {
+    normals4_rk<FAST>(p, gp, nb, z[0], z[1], z[2], z[3]);
+#pragma unroll
+    for (int u = 0; u < 3; ++u)
+      if ((uint32_t)u < rem) Y = em_step<MODEL>(Y, z[u], r.a, r.s, r.ybar);
   }
   term[(size_t)r.row * M + q] = Y;
 }
