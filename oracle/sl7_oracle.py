@@ -218,6 +218,13 @@ def cir_collocation(Y, dt, kappa, ybar, sigma, x) -> np.ndarray:
     return c * ncx2.ppf(q, d, lam_nc)
 
 
+def cir_exact_points(Y, dt, kappa, ybar, sigma, x) -> np.ndarray:
+    """Exact-collocation CIR: the conditional quantiles of cir_collocation at the
+    path's state Y+ = max(Y, 0) (reading R-24: g_m's polynomial extrapolation can leave the state
+    slightly negative; the CIR transition from a state <= 0 is the one from 0, a central chi-square)."""
+    return cir_collocation(np.maximum(np.asarray(Y, dtype=np.float64), 0.0), dt, kappa, ybar, sigma, x)
+
+
 # ---- the ANN H_hat (Eq. 6.4, PAPER.md:56-62; architecture PAPER.md:85) -----------------------
 
 ACT_TANH = 0
@@ -367,7 +374,7 @@ def ann_collocation(net: Mlp, Y, dt, theta, quant=None) -> np.ndarray:
 
 
 class Spec:
-    """What to simulate.  colloc in {'ann', 'gbm', 'ou'}; theta in the orders of reading R-10."""
+    """What to simulate.  colloc in {'ann', 'gbm', 'ou', 'cir'}; theta in the orders of reading R-10."""
 
     def __init__(self, m, colloc, theta, y0, dt, n_steps, net=None, quant=None):
         self.m = int(m)
@@ -390,6 +397,9 @@ class Spec:
         if self.colloc == "ou":
             ybar, lam, sigma = self.theta
             return ou_collocation(Y, self.dt, ybar, lam, sigma, self.x)
+        if self.colloc == "cir":
+            kappa, ybar, sigma = self.theta
+            return cir_exact_points(Y, self.dt, kappa, ybar, sigma, self.x)
         raise ValueError(self.colloc)
 
 

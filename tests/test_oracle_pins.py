@@ -470,3 +470,59 @@ def test_quantiles_hazen():
     y = rng.normal(size=1001)
     lv = np.array([0.0005, 0.01, 0.25, 0.5, 0.75, 0.99, 0.9995])
     np.testing.assert_allclose(O.quantiles(y, lv), np.quantile(y, lv, method="hazen"), rtol=1e-14, atol=1e-14)
+
+
+# ------------------------------------------------------- exact CIR collocation
+
+def _ncx2_cdf_mp(x, d, lam):
+    """Definition: Poisson(lam/2) mixture of regularised lower incomplete gammas, 30 digits."""
+    import mpmath
+    mpmath.mp.dps = 30
+    x, d, mu = mpmath.mpf(x), mpmath.mpf(d), mpmath.mpf(lam) / 2
+    s, i = mpmath.mpf(0), 0
+    while True:
+        w = mpmath.exp(-mu + i * mpmath.log(mu) - mpmath.loggamma(i + 1)) if mu > 0 else (1 if i == 0 else 0)
+        s += w * mpmath.gammainc(d / 2 + i, 0, x / 2, regularized=True)
+        i += 1
+        if i > mu + 40 * mpmath.sqrt(mu + 1) + 40:
+            return s
+
+
+@pytest.mark.parametrize("Y", [0.1, 0.02, 0.35, 0.0])
+def test_cir_exact_points_vs_definition(Y):
+    """y_j = c F^{-1}(Phi(x_j)) with F the noncentral chi-square CDF written out as its Poisson mixture
+    and inverted at 30 digits (mpmath), independently of scipy's ncx2."""
+    import mpmath
+    k, ybar, s, dt = 1.0, 0.1, 0.3, 0.125
+    c = s * s * (1 - math.exp(-k * dt)) / (4 * k)
+    d = 4 * k * ybar / (s * s)
+    lam = Y * math.exp(-k * dt) / c
+    x = O.gauss_hermite_nodes(7)
+    y = O.cir_exact_points(np.array([Y]), dt, k, ybar, s, x)[0]
+    for j in (0, 2, 3, 6):
+        p = mpmath.ncdf(x[j])
+        q = mpmath.findroot(lambda t: _ncx2_cdf_mp(t, d, lam) - p, y[j] / c)
+        assert abs(y[j] - c * float(q)) <= 1e-11 * y[j]
+
+
+def test_cir_exact_points_negative_state_is_zero_state():
+    x = O.gauss_hermite_nodes(5)
+    a = O.cir_exact_points(np.array([-0.01, 0.0]), 0.25, 1.0, 0.1, 0.3, x)
+    np.testing.assert_array_equal(a[0], a[1])
+    c = 0.09 * (1 - math.exp(-0.25)) / 4
+    np.testing.assert_allclose(a[1], c * scipy.stats.chi2.ppf(scipy.stats.norm.cdf(x), 4 * 0.1 / 0.09), rtol=1e-12)
+
+
+def test_cir_exact_collocation_paths_match_cir_moments():
+    """7L with exact CIR collocation over 4 large steps reproduces the CIR law's closed-form mean and
+    variance (E[Y_T] = Ybar + (Y0 - Ybar) e^{-kT}; Var as below) within 4 standard errors."""
+    k, ybar, s, y0, T, n, P = 1.0, 0.1, 0.3, 0.3, 1.0, 4, 3000
+    spec = O.Spec(7, "cir", (k, ybar, s), y0, T / n, n)
+    Y, _ = O.simulate(spec, 9, np.arange(P, dtype=np.uint64))
+    YT = Y[-1]
+    y0f = float(np.float32(y0))
+    e = math.exp(-k * T)
+    mean = ybar + (y0f - ybar) * e
+    var = y0f * s * s / k * (e - e * e) + ybar * s * s / (2 * k) * (1 - e) ** 2
+    assert abs(YT.mean() - mean) < 4 * math.sqrt(var / P)
+    assert abs(YT.var() - var) < 4 * var * math.sqrt(2.0 / P) * 1.5
