@@ -6,7 +6,8 @@ launch, CUDA events on the launch stream, NVML clocks sampled during the timed r
 
 cfg2: OU (Ybar=0, lam=1, sigma=0.5, Y0=1) and CIR (kappa=1, Ybar=0.1, sigma=0.3, Y0=0.1), T=2, 16 steps,
       m=7, [5,50,50,50,50,7] softplus (theta as network input), 1e8 paths, STATS (moments + 4096-bin
-      histogram).  Modes: ANN-BF16 (tcgen05), ANN-FP32, exact OU (general / specialised).
+      histogram).  Modes: ANN-BF16 (tcgen05), ANN-SPLIT, ANN-FP32, 7L-CDC, exact OU (general / specialised),
+      exact CIR (float64 noncentral chi-square quantiles, 1e6 paths).
 em:   Euler-Maruyama comparator on cfg2's OU and CIR, 16 large steps of 0.125 with
       K = 1, 8, 125 sub-steps (dtau = 1e-3 at K = 125), STATS + strong error vs the exact OU solution on
       the same fine normals; the 7L lines of cfg2 give the contrast.  Unit: fine path-steps/s.
@@ -189,6 +190,9 @@ def main():
                      ("ann_split_bf16x3_tcgen05", ctx, sl7.COLLOC_ANN, sl7.PREC_SPLIT, 0, w.theta, N),
                      ("ann_fp32", ctx, sl7.COLLOC_ANN, sl7.PREC_FP32, 0, w.theta, N // 10),
                      ("cdc_ann_fp32_table", ctx, sl7.COLLOC_ANN, sl7.PREC_FP32, -1, w.theta, N)]
+            if w.process == "cir":
+                ex = sl7.Context(w.m, device=0)
+                modes += [("exact_cir_ncx2_fp64", ex, sl7.COLLOC_EXACT_CIR, sl7.PREC_FP32, 0, w.theta, N // 100)]
             if w.process == "ou":
                 ex = sl7.Context(w.m, device=0)
                 modes += [("exact_ou_general", ex, sl7.COLLOC_EXACT_OU, sl7.PREC_FP32, 0, w.theta, N),

@@ -83,8 +83,15 @@ typedef enum { SL7_PREC_FP32 = 0, SL7_PREC_TF32 = 1, SL7_PREC_BF16 = 2, SL7_PREC
  *  ANN:        the loaded MLP, input (Y, dt, theta...) (Eq. 6.4).
  *  EXACT_GBM:  y_j = Y exp((mu - sigma^2/2) dt + sigma sqrt(dt) x_j), theta = (mu, sigma).
  *  EXACT_OU:   y_j = Y e^{-lam dt} + Ybar (1 - e^{-lam dt}) + sigma sqrt((1-e^{-2 lam dt})/(2 lam)) x_j
- *              (Eq. 6.6), theta = (Ybar, lam, sigma); series form when lam*dt < 1e-6. */
-typedef enum { SL7_COLLOC_ANN = 0, SL7_COLLOC_EXACT_GBM = 1, SL7_COLLOC_EXACT_OU = 2 } sl7_colloc;
+ *              (Eq. 6.6), theta = (Ybar, lam, sigma); series form when lam*dt < 1e-6.
+ *  EXACT_CIR:  y_j = c F^{-1}(Phi(x_j)), F the noncentral chi-square CDF with d = 4 kappa Ybar / sigma^2
+ *              degrees of freedom and noncentrality Y+ e^{-kappa dt} / c, c = sigma^2 (1 - e^{-kappa dt})
+ *              / (4 kappa), Y+ = max(Y, 0) (the CIR transition law, Eq. 6.3); theta = (kappa, Ybar,
+ *              sigma), all > 0.  Evaluated per path and step in float64 (Poisson mixture of incomplete
+ *              gammas, bracketed Newton): a reference generator, ~100x slower than the other modes.
+ *              Scheme 7L only; SL7_FLAG_SPECIALIZED is not available. */
+typedef enum { SL7_COLLOC_ANN = 0, SL7_COLLOC_EXACT_GBM = 1, SL7_COLLOC_EXACT_OU = 2,
+               SL7_COLLOC_EXACT_CIR = 3 } sl7_colloc;
 
 /* Path-wise reference evaluated on the SAME normals, for the strong error E|Y_T - Y(T)|
  * (PAPER.md:81, :16, :110).  GBM: Y(T) = Y0 exp((mu - s^2/2) T + s sqrt(dt) sum_i X_i),

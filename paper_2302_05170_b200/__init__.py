@@ -22,7 +22,7 @@ OK, EINVAL, ESTATE, EFORMAT, ENOMEM, ECUDA, ENONFINITE, EUNSUPPORTED = range(8)
 ACT_TANH, ACT_SOFTPLUS = 0, 1
 OUT_FULL, OUT_TERMINAL, OUT_STATS = 0, 1, 2
 PREC_FP32, PREC_TF32, PREC_BF16, PREC_SPLIT = 0, 1, 2, 3
-COLLOC_ANN, COLLOC_EXACT_GBM, COLLOC_EXACT_OU = 0, 1, 2
+COLLOC_ANN, COLLOC_EXACT_GBM, COLLOC_EXACT_OU, COLLOC_EXACT_CIR = 0, 1, 2, 3
 REF_NONE, REF_GBM, REF_OU = 0, 1, 2
 MODEL_GBM, MODEL_OU, MODEL_CIR = 1, 2, 3
 STATS_HEAD = 8

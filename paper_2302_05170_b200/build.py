@@ -14,7 +14,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsl7.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["sl7_host.cpp", "sl7_kernels.cu", "sl7_tc.cu", "sl7_cdc.cu", "sl7_em.cu"]
+SOURCES = ["sl7_host.cpp", "sl7_kernels.cu", "sl7_tc.cu", "sl7_cdc.cu", "sl7_em.cu", "sl7_cir.cu"]
 HEADERS = ["sl7_internal.h", "sl7_device.cuh", "sl7_tc.cuh"]
 
 

@@ -1,0 +1,208 @@
+// sl7_cir.cu -- exact-collocation CIR on sm_100a: the 7L step with the
+// conditional collocation points of the CIR transition itself instead of the ANN.
+//
+// The CIR transition Y(t + dt) | Y(t) = c * chi'^2(d, lam) with c = sigma^2 (1 - e^{-kappa dt}) / (4 kappa),
+// d = 4 kappa Ybar / sigma^2, lam = Y+ e^{-kappa dt} / c (Y+ = max(Y, 0), reading R-24), so
+//     y_j = c * F^{-1}_{d,lam}(Phi(x_j))                                         (Eq. 6.3)
+// per path and step, then Y_{i+1} = g_m(X_hat) exactly as in the other exact modes.
+//
+// F is evaluated in float64 as its Poisson mixture F(x) = sum_k w_k P(d/2 + k, x/2),
+// w_k = e^{-mu} mu^k / k!, mu = lam/2, P the regularised lower incomplete gamma: P is computed once at
+// the Poisson mode (series for y < a + 1, Lentz continued fraction otherwise) and carried to the other
+// k by the exact recurrences P(a+1, y) = P(a, y) - G(a), G(a) = y^a e^{-y} / Gamma(a+1) (forward) and
+// P(a, y) = P(a+1, y) + G(a) (backward), the weights by w_{k+1} = w_k mu / (k+1); the density comes
+// from the same terms.  The quantile is a bracketed Newton iteration from the Patnaik (scaled central
+// chi-square) + Wilson-Hilferty starting point, which takes the normal quantile x_j directly.
+// The work is float64 special-function evaluation (~4 Newton steps x ~2 (sqrt(mu) + ...) terms x m nodes
+// per path-step): a reference generator, not a throughput path.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include "sl7_device.cuh"
+
+namespace sl7 {
+
+namespace {
+
+struct Ncx2 {
+  double a_m;    // d/2 + k_mode
+  double lg_m;   // lgamma(a_m + 1)
+  double mu;     // lam / 2
+  double w_m;    // Poisson weight at the mode
+  int k_m;       // Poisson mode floor(mu)
+};
+
+// regularised lower incomplete gamma P(a, y), y > 0, given lgamma(a + 1)
+__device__ double gamma_p(double a, double y, double lg_a1) {
+  const double lpre = a * log(y) - y - lg_a1;   // log(y^a e^{-y} / Gamma(a + 1))
+  if (y < a + 1.0) {
+    double term = 1.0, sum = 1.0, ap = a;
+    for (int n = 0; n < 2000; ++n) {
+      ap += 1.0;
+      term *= y / ap;
+      sum += term;
+      if (term < sum * 1e-17) break;
+    }
+    return exp(lpre) * sum;
+  }
+  // Q(a, y) = e^{-y} y^a / Gamma(a) * CF  (modified Lentz)
+  const double tiny = 1e-300;
+  double b = y + 1.0 - a, cc = 1.0 / tiny, dd = 1.0 / b, h = dd;
+  for (int i = 1; i < 2000; ++i) {
+    const double an = -i * (i - a);
+    b += 2.0;
+    dd = fma(an, dd, b);
+    if (fabs(dd) < tiny) dd = tiny;
+    cc = b + an / cc;
+    if (fabs(cc) < tiny) cc = tiny;
+    dd = 1.0 / dd;
+    const double del = dd * cc;
+    h *= del;
+    if (fabs(del - 1.0) < 1e-16) break;
+  }
+  return 1.0 - exp(lpre + log(a)) * h;
+}
+
+// F(x) and dF/dx of the noncentral chi-square
+__device__ void ncx2_cdf_pdf(const Ncx2& n, double x, double& F, double& f) {
+  const double y = 0.5 * x;
+  if (!(y > 0.0)) {
+    F = 0.0;
+    f = 0.0;
+    return;
+  }
+  const double P = gamma_p(n.a_m, y, n.lg_m);
+  const double G = exp(n.a_m * log(y) - y - n.lg_m);
+  double Fs = n.w_m * P, fs = n.w_m * G * n.a_m;   // density term: w y^{a-1} e^{-y} / Gamma(a) = w G a / y
+  {
+    double Pk = P, Gk = G, wk = n.w_m, ak = n.a_m;
+    for (int k = n.k_m + 1; k < n.k_m + 100000; ++k) {
+      Pk = fmax(Pk - Gk, 0.0);
+      Gk *= y / (ak + 1.0);
+      ak += 1.0;
+      wk *= n.mu / (double)k;
+      Fs += wk * Pk;
+      fs += wk * Gk * ak;
+      if (wk < 1e-18) break;
+    }
+  }
+  {
+    double Pk = P, Gk = G, wk = n.w_m, ak = n.a_m;
+    for (int k = n.k_m - 1; k >= 0; --k) {
+      Gk *= ak / y;
+      ak -= 1.0;
+      Pk += Gk;
+      wk *= (double)(k + 1) / n.mu;
+      Fs += wk * Pk;
+      fs += wk * Gk * ak;
+      if (wk < 1e-18) break;
+    }
+  }
+  F = Fs;
+  f = 0.5 * fs / y;
+}
+
+// F^{-1}(p) with z = Phi^{-1}(p) for the starting point; lo: a known lower bracket (F(lo) <= p)
+__device__ double ncx2_quantile(const Ncx2& n, double p, double z, double d, double lam, double lo) {
+  const double h = d + lam, r = d + 2.0 * lam;
+  const double nu = h * h / r, rho = r / h, t = 2.0 / (9.0 * nu);
+  double w = 1.0 - t + z * sqrt(t);
+  w = fmax(w, 0.05);
+  double x = fmax(rho * nu * w * w * w, lo);
+  double hi = CUDART_INF;
+  for (int it = 0; it < 100; ++it) {
+    double F, f;
+    ncx2_cdf_pdf(n, x, F, f);
+    const double g = F - p;
+    if (g < 0.0) lo = x; else hi = x;
+    if (g == 0.0) break;
+    double xn = x - g / f;
+    if (!(f > 0.0) || !(xn > lo && xn < hi)) xn = (hi < CUDART_INF) ? 0.5 * (lo + hi) : 2.0 * x + 1.0;
+    const bool done = fabs(xn - x) <= 1e-14 * xn;
+    x = xn;
+    if (done) break;
+  }
+  return x;
+}
+
+template <int MR, bool RT_M, bool FAST>
+__global__ void __launch_bounds__(256) exact_cir_kernel(const __grid_constant__ RunParams p) {
+  extern __shared__ uint32_t hist[];
+  __shared__ double red[8];
+  hist_init(p, hist);
+  __syncthreads();
+  StatAcc acc;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const int m = RT_M ? p.m : MR;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < p.n_paths; q += stride) {
+    const uint64_t gp = p.path_offset + q;
+    float Y = p.y0;
+    if (p.out_mode == kFull) p.out[q] = Y;
+    float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
+    for (int i = 0; i < p.n_steps; ++i) {
+      if ((i & 3) == 0) normals4<FAST>(p.key0, p.key1, gp, (uint32_t)(i >> 2), z0, z1, z2, z3);
+      const float Z = z0;
+      z0 = z1; z1 = z2; z2 = z3;
+      // conditional law of the step: c chi'^2(d, lam(Y+))
+      const double lam = fmax((double)Y, 0.0) * p.cir_lscale;
+      Ncx2 n;
+      n.mu = 0.5 * lam;
+      n.k_m = (int)floor(n.mu);
+      n.a_m = 0.5 * p.cir_d + (double)n.k_m;
+      n.lg_m = lgamma(n.a_m + 1.0);
+      n.w_m = (n.mu > 0.0) ? exp(-n.mu + (double)n.k_m * log(n.mu) - lgamma((double)n.k_m + 1.0)) : 1.0;
+      float y[MR];
+      double lo = 0.0;
+#pragma unroll 1
+      for (int j = 0; j < m; ++j) {
+        const double xq = ncx2_quantile(n, p.cir_p[j], p.cir_x[j], p.cir_d, lam, lo);
+        lo = xq;   // quantiles increase with j
+        y[j] = (float)(p.cir_c * xq);
+      }
+      if (RT_M)
+        for (int j = m; j < MR; ++j) y[j] = 0.0f;
+      Y = gm_eval<MR, RT_M>(p, Z, y);
+      if (p.out_mode == kFull) p.out[(uint64_t)(i + 1) * p.n_paths + q] = Y;
+    }
+    if (p.out_mode == kTerminal) p.out[q] = Y;
+    if (p.has_stats) stat_add(acc, p, Y, 0.0, hist);
+  }
+  if (p.has_stats) stat_flush(acc, p, hist, red);
+}
+
+template <int MR, bool RT_M, bool FAST>
+cudaError_t launch_cir_t(const RunParams& p, cudaStream_t st, int num_sms) {
+  auto kernel = exact_cir_kernel<MR, RT_M, FAST>;
+  const size_t smem = (p.has_stats && p.n_bins > 0) ? sizeof(uint32_t) * (size_t)(p.n_bins + 2) : 0;
+  cudaError_t e;
+  if (smem > 48 * 1024) {
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  const uint64_t need = (p.n_paths + 255) / 256, full = (uint64_t)per_sm * (uint64_t)num_sms;
+  kernel<<<(unsigned)(need < full ? need : full), 256, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <bool FAST>
+cudaError_t launch_cir_f(const RunParams& p, cudaStream_t st, int num_sms) {
+  switch (p.m) {
+    case 5: return launch_cir_t<5, false, FAST>(p, st, num_sms);
+    case 7: return launch_cir_t<7, false, FAST>(p, st, num_sms);
+    default: return launch_cir_t<kMaxM, true, FAST>(p, st, num_sms);
+  }
+}
+
+}  // namespace
+
+int launch_exact_cir(const RunParams& p, void* stream, int num_sms) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  return (int)((p.flags & SL7_FLAG_FAST_NORMALS) ? launch_cir_f<true>(p, st, num_sms)
+                                                 : launch_cir_f<false>(p, st, num_sms));
+}
+
+}  // namespace sl7

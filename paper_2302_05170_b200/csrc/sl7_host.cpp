@@ -431,6 +431,22 @@ sl7_status prepare(sl7_ctx c, double Y0, double dt, int32_t n_steps, const doubl
       p.colloc = kExactOu;
       break;
     }
+    case SL7_COLLOC_EXACT_CIR: {
+      if (n_theta != 3) return fail(c, SL7_EINVAL, "EXACT_CIR needs theta = (kappa, Ybar, sigma)");
+      const double kappa = theta[0], ybar = theta[1], s = theta[2];
+      if (!(kappa > 0) || !(ybar > 0) || !(s > 0)) return fail(c, SL7_EINVAL, "theta: kappa, Ybar, sigma > 0");
+      if (o->flags & SL7_FLAG_SPECIALIZED) return fail(c, SL7_EUNSUPPORTED, "EXACT_CIR: SL7_FLAG_SPECIALIZED");
+      if (o->scheme == SL7_SCHEME_CDC) return fail(c, SL7_EUNSUPPORTED, "EXACT_CIR: scheme CDC");
+      p.cir_c = s * s * (-std::expm1(-kappa * dt)) / (4.0 * kappa);
+      p.cir_d = 4.0 * kappa * ybar / (s * s);
+      p.cir_lscale = std::exp(-kappa * dt) / p.cir_c;
+      for (int j = 0; j < kMaxM; ++j) {
+        p.cir_x[j] = (j < c->m) ? c->x[j] : 0.0;
+        p.cir_p[j] = (j < c->m) ? 0.5 * std::erfc(-c->x[j] / std::sqrt(2.0)) : 0.0;
+      }
+      p.colloc = kExactCir;
+      break;
+    }
     case SL7_COLLOC_ANN: {
       if (c->dims.empty()) return fail(c, SL7_ESTATE, "ANN mode on a context created without layer_dims");
       if (!c->has_net) return fail(c, SL7_ESTATE, "ANN mode before sl7_load_weights");

@@ -13,7 +13,7 @@ constexpr int kMaxW = SL7_MAX_WIDTH;
 constexpr int kMaxHidden = SL7_MAX_HIDDEN;
 constexpr int kStatsHead = SL7_STATS_HEAD;
 
-enum Colloc : int { kAnn = 0, kExactGbm = 1, kExactOu = 2 };
+enum Colloc : int { kAnn = 0, kExactGbm = 1, kExactOu = 2, kExactCir = 3 };
 enum Ref : int { kRefNone = 0, kRefGbm = 1, kRefOu = 2 };
 enum OutMode : int { kFull = 0, kTerminal = 1, kStatsOnly = 2 };
 
@@ -40,6 +40,9 @@ struct RunParams {
   float q[8];
   float ou_s;
   uint32_t flags;
+  // ---- exact CIR: Y' | Y = cir_c chi'^2(cir_d, Y+ cir_lscale); quantile levels cir_p[j] = Phi(cir_x[j])
+  double cir_c, cir_d, cir_lscale;
+  double cir_p[kMaxM], cir_x[kMaxM];
   // ---- strong-error reference on the same normals ----
   int ref;               // Ref
   double ref_drift_T;    // GBM: (mu - s^2/2) T
@@ -124,6 +127,8 @@ int launch_tc_kernel(const RunParams& p, const TcParams& t, void* stream, int nu
 int launch_philox_u32(uint64_t seed, uint64_t off, uint64_t n, uint32_t block, uint32_t* out, void* stream);
 int launch_normals(uint64_t seed, uint64_t off, uint64_t n, int n_steps, bool fast, float* out, void* stream);
 int launch_zero_stats(double* stats, size_t n, void* stream);
+// sl7_cir.cu
+int launch_exact_cir(const RunParams& p, void* stream, int num_sms);
 // sl7_em.cu
 int launch_em(const RunParams& p, void* stream, int num_sms);
 int launch_em_rows(const RunParams& p, const EmRow* d_rows, uint32_t n_rows, uint32_t M, uint64_t row_base,

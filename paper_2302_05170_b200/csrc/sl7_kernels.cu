@@ -335,6 +335,7 @@ int launch_step_kernel(const RunParams& p, int prec, void* stream, int num_sms) 
   switch (p.colloc) {
     case kExactGbm: return (int)launch_exact<kExactGbm>(p, st, num_sms);
     case kExactOu: return (int)launch_exact<kExactOu>(p, st, num_sms);
+    case kExactCir: return launch_exact_cir(p, stream, num_sms);
     default:
       return (int)(p.act == SL7_ACT_TANH ? launch_ann_f32<SL7_ACT_TANH>(p, st, num_sms)
                                          : launch_ann_f32<SL7_ACT_SOFTPLUS>(p, st, num_sms));
