@@ -224,6 +224,27 @@ def main():
                                         "unit": "Top/s", "frac": ach / pk,
                                         "algorithmic": "%d softplus activations per path-step" % trans}
                 emit(line)
+            # the sharded-CDC driver (sl7_cdc_* + dist.cdc_run) on one rank: the cost of driving the per-pass
+            # exchange from the host, against the single-call CDC line above
+            from paper_2302_05170_b200.dist import CdcShard, cdc_run
+            opts = sl7.make_opts(prec=sl7.PREC_FP32, colloc=sl7.COLLOC_ANN, stream=stream, n_bins=4096, hist_lo=lo,
+                                 hist_hi=hi, shift=w.y0, scheme=sl7.SCHEME_CDC)
+
+            def sharded(opts=opts, ctx=ctx, w=w):
+                stats.zero_()
+                cdc_run([CdcShard(ctx, w.y0, w.dt, w.n_steps, w.theta, N, w.seed, opts, stats)], w.n_steps,
+                        allreduce=lambda t: None)
+            clk = ClockSampler(0)
+            clk.start()
+            ms, ms_min = timed_launches(sharded, a.steps, a.warmup, flush, stream)
+            clk.stop()
+            s = sl7.stats_summary(stats.cpu().numpy(), opts, q_levels=[0.01, 0.5, 0.99])
+            emit({"config": key, "mode": "cdc_sharded_driver_1rank", "metric": "7L path-steps/sec (device-timed)",
+                  "value": N * w.n_steps / (ms * 1e-3), "unit": UNIT, "ms_per_launch": ms, "paths": N,
+                  "n_steps": w.n_steps, "m": w.m, "exchange": "4 x %d-byte histogram all-reduces per step" % (
+                      8 * sl7.cdc_hist_elems()),
+                  "terminal": {k: s[k] for k in ("mean", "var", "skew", "exkurt", "strong_err")},
+                  "clocks": clk.summary()})
 
 
 if __name__ == "__main__":

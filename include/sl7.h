@@ -211,6 +211,35 @@ sl7_status sl7_normals(uint64_t seed, uint64_t path_offset, uint64_t n_paths, in
                        uint32_t flags, float* d_out, void* stream);
 
 /* ---------------------------------------------------------------------------------------------
+ * Sharded 7L-CDC (PAPER.md:48, :106-108 on several GPUs).  The marginal collocation points z_k are
+ * quantiles of ALL paths, so a run whose paths are split over ranks exchanges, per large step, the four
+ * radix-select digit histograms.  The caller drives the step loop and owns the reduction:
+ *
+ *   sl7_cdc_init(ctx, ..., n_local, ..., opts{path_offset = first global path of this rank}, d_state)
+ *   for step i in 0..n_steps-1:
+ *     for pass in 0..3:
+ *       sl7_cdc_hist(ctx, d_state, pass, d_hist)      local digit counts of this pass
+ *       all-reduce(SUM) d_hist over the ranks           (e.g. torch.distributed / NCCL, same stream)
+ *       sl7_cdc_select(ctx, pass, d_hist)               every rank fixes the same digits
+ *     sl7_cdc_step(ctx, i, d_state, d_state, last ? d_stats : NULL)
+ *   all-reduce(SUM) d_stats
+ *
+ * With one rank this is exactly sl7_simulate(scheme = CDC) (bit for bit); with several, every path's
+ * states equal those of the single-rank run over the union of the paths.
+ * d_hist: device u64[sl7_cdc_hist_elems()] ([2 SL7_MAX_M slots][256 digits]); d_state: device fp32
+ * [n_local], updated in place (d_in == d_out allowed).  opts as for sl7_simulate with scheme CDC (the
+ * histogram/shift fields describe the statistics sl7_cdc_step adds into d_stats; d_stats is NOT zeroed).
+ * All calls are asynchronous on opts->stream of sl7_cdc_init.  Errors: as sl7_simulate; SL7_ESTATE if
+ * sl7_cdc_init has not succeeded; SL7_EINVAL for pass outside 0..3 or step outside 0..n_steps-1. */
+size_t sl7_cdc_hist_elems(void);
+sl7_status sl7_cdc_init(sl7_ctx ctx, double Y0, double dt, int32_t n_steps, const double* theta,
+                        int32_t n_theta, uint64_t n_paths, uint64_t seed, const sl7_run_opts* opts,
+                        float* d_state);
+sl7_status sl7_cdc_hist(sl7_ctx ctx, const float* d_state, int32_t pass, uint64_t* d_hist);
+sl7_status sl7_cdc_select(sl7_ctx ctx, int32_t pass, const uint64_t* d_hist);
+sl7_status sl7_cdc_step(sl7_ctx ctx, int32_t step, const float* d_in, float* d_out, double* d_stats);
+
+/* ---------------------------------------------------------------------------------------------
  * Euler-Maruyama comparator and offline training-set generation.
  * --------------------------------------------------------------------------------------------- */
 

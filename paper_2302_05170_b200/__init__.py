@@ -63,7 +63,8 @@ STATUS_NAMES = {0: "SL7_OK", 1: "SL7_EINVAL", 2: "SL7_ESTATE", 3: "SL7_EFORMAT",
                 5: "SL7_ECUDA", 6: "SL7_ENONFINITE", 7: "SL7_EUNSUPPORTED"}
 
 EXPORTS = ["sl7_create", "sl7_load_weights", "sl7_simulate", "sl7_simulate_host", "sl7_simulate_em",
-           "sl7_training_set", "sl7_stats",
+           "sl7_training_set", "sl7_cdc_hist_elems", "sl7_cdc_init", "sl7_cdc_hist", "sl7_cdc_select",
+           "sl7_cdc_step", "sl7_stats",
            "sl7_philox_u32", "sl7_normals", "sl7_gh_grid", "sl7_out_elems", "sl7_stats_elems",
            "sl7_last_error", "sl7_status_str", "sl7_abi_version", "sl7_destroy"]
 
@@ -90,6 +91,12 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                   c.POINTER(sl7_run_opts), fp, fp]
     L.sl7_training_set.argtypes = [vp, c.c_int, dp, u64, c.c_uint32, c.c_double, u64, c.POINTER(sl7_run_opts),
                                    fp, fp]
+    L.sl7_cdc_hist_elems.argtypes = []
+    L.sl7_cdc_hist_elems.restype = c.c_size_t
+    L.sl7_cdc_init.argtypes = [vp, c.c_double, c.c_double, i32, dp, i32, u64, u64, c.POINTER(sl7_run_opts), fp]
+    L.sl7_cdc_hist.argtypes = [vp, fp, i32, fp]
+    L.sl7_cdc_select.argtypes = [vp, i32, fp]
+    L.sl7_cdc_step.argtypes = [vp, i32, fp, fp, fp]
     L.sl7_stats.argtypes = [dp, c.POINTER(sl7_run_opts), c.POINTER(sl7_summary)]
     L.sl7_philox_u32.argtypes = [u64, u64, u64, c.c_uint32, vp, vp]
     L.sl7_normals.argtypes = [u64, u64, u64, i32, c.c_uint32, vp, vp]
@@ -106,7 +113,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L.sl7_destroy.argtypes = [vp]
     L.sl7_destroy.restype = None
     for name in ("sl7_create", "sl7_load_weights", "sl7_simulate", "sl7_simulate_host", "sl7_simulate_em",
-                 "sl7_training_set", "sl7_stats",
+                 "sl7_training_set", "sl7_cdc_init", "sl7_cdc_hist", "sl7_cdc_select", "sl7_cdc_step", "sl7_stats",
                  "sl7_philox_u32", "sl7_normals", "sl7_gh_grid"):
         getattr(L, name).restype = c.c_int
     _lib = L
@@ -263,3 +270,22 @@ class Context:
                                      int(n_rows), int(n_inner), float(dtau), int(seed), ctypes.byref(opts),
                                      _dptr(terminal), _dptr(labels)), self._h)
         return terminal, labels
+
+    # ---- sharded 7L-CDC (include/sl7.h, "Sharded 7L-CDC"): the caller drives the loop -------------
+    def cdc_init(self, y0, dt, n_steps, theta, n_paths, seed, opts, state):
+        th = (ctypes.c_double * max(1, len(theta)))(*theta)
+        _check(_lib.sl7_cdc_init(self._h, float(y0), float(dt), int(n_steps), th, len(theta), int(n_paths), int(seed),
+                                 ctypes.byref(opts), _dptr(state)), self._h)
+
+    def cdc_hist(self, state, pass_, hist):
+        _check(_lib.sl7_cdc_hist(self._h, _dptr(state), int(pass_), _dptr(hist)), self._h)
+
+    def cdc_select(self, pass_, hist):
+        _check(_lib.sl7_cdc_select(self._h, int(pass_), _dptr(hist)), self._h)
+
+    def cdc_step(self, step, state_in, state_out, stats=None):
+        _check(_lib.sl7_cdc_step(self._h, int(step), _dptr(state_in), _dptr(state_out), _dptr(stats)), self._h)
+
+
+def cdc_hist_elems():
+    return load_library().sl7_cdc_hist_elems()

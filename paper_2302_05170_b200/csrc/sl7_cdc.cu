@@ -40,7 +40,7 @@ struct CdcScratch {
 
 // ---- pass p: histogram of digit p (bits [24 - 8p, 32 - 8p)) of the elements matching a slot prefix
 __global__ void __launch_bounds__(256) cdc_hist_kernel(const float* __restrict__ y, uint64_t n, int pass,
-                                                       CdcScratch* s) {
+                                                       const CdcScratch* s, unsigned long long* __restrict__ hist) {
   __shared__ uint32_t h[kCdcMaxT][256];
   __shared__ uint32_t sp[kCdcMaxT];
   const int nslot = s->nslot;
@@ -71,18 +71,21 @@ __global__ void __launch_bounds__(256) cdc_hist_kernel(const float* __restrict__
   __syncthreads();
   for (int i = threadIdx.x; i < nslot * 256; i += blockDim.x) {
     const uint32_t c = h[i >> 8][i & 255];
-    if (c) atomicAdd(&s->hist[i >> 8][i & 255], (unsigned long long)c);
+    if (c) atomicAdd(&hist[i], (unsigned long long)c);
   }
 }
 
 // ---- after pass p: fix each target's digit; set up the next pass (one block of 256 threads)
-__global__ void __launch_bounds__(256) cdc_scan_kernel(int pass, int m, CdcScratch* s, const __grid_constant__ CdcLevels lv) {
+// hist: [slot][256] counts of this pass over ALL paths of the run (summed over ranks for a sharded run);
+// clear: zero it afterwards (the single-call path reuses the scratch histogram).
+__global__ void __launch_bounds__(256) cdc_scan_kernel(int pass, int m, CdcScratch* s, const __grid_constant__ CdcLevels lv,
+                                                       unsigned long long* hist, int clear) {
   const int T = 2 * m;
   if (threadIdx.x == 0) {
     if (pass == 0) {
       // M finite states; target order statistics (0-based) of the plotting-position quantiles
       unsigned long long M = 0;
-      for (int b = 0; b < 256; ++b) M += s->hist[0][b];
+      for (int b = 0; b < 256; ++b) M += hist[b];
       s->M = M;
       for (int k = 0; k < m && M == 0; ++k) {   // no finite state: every target at rank 0 (z = NaN below)
         s->frac[k] = 0.0;
@@ -108,7 +111,8 @@ __global__ void __launch_bounds__(256) cdc_scan_kernel(int pass, int m, CdcScrat
       const unsigned long long r = s->rank[t];
       int b = 0;
       unsigned long long below = 0;   // elements of this prefix in bins < b
-      while (b < 255 && below + s->hist[sl][b] <= r) below += s->hist[sl][b++];
+      const unsigned long long* h = hist + 256 * sl;
+      while (b < 255 && below + h[b] <= r) below += h[b++];
       s->rank[t] = r - below;
       s->prefix[t] = (s->prefix[t] << 8) | (uint32_t)b;
     }
@@ -142,7 +146,8 @@ __global__ void __launch_bounds__(256) cdc_scan_kernel(int pass, int m, CdcScrat
   }
   __syncthreads();
   // clear the histograms for the next pass
-  for (int i = threadIdx.x; i < kCdcMaxT * 256; i += blockDim.x) s->hist[i >> 8][i & 255] = 0ull;
+  if (clear)
+    for (int i = threadIdx.x; i < kCdcMaxT * 256; i += blockDim.x) hist[i] = 0ull;
   if (pass == 3 && threadIdx.x == 0) {   // reset the selection for the next step
     s->nslot = 1;
     s->slot_prefix[0] = 0u;
@@ -283,40 +288,77 @@ int cdc_init_scratch(void* scratch, void* stream) {
   return (int)cudaMemcpyAsync(scratch, &h, sizeof h, cudaMemcpyHostToDevice, (cudaStream_t)stream);
 }
 
-// Runs all n_steps of the CDC scheme.  state: n_paths floats (may alias out rows, see host).
-int launch_cdc(const RunParams& p, const CdcLevels& lv, void* scratch, float* const* rows, int nrows, void* stream,
-               int num_sms) {
+namespace {
+
+unsigned cdc_grid(uint64_t n, int num_sms) {
+  return (unsigned)(((n + 255) / 256) < (uint64_t)num_sms * 8 ? (n + 255) / 256 : (uint64_t)num_sms * 8);
+}
+
+}  // namespace
+
+int cdc_fill(float* y, uint64_t n, float v, void* stream, int num_sms) {
+  fill_kernel<<<cdc_grid(n, num_sms), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(y, n, v);
+  return (int)cudaGetLastError();
+}
+
+int cdc_hist(const RunParams& p, void* scratch, const float* y, int pass, unsigned long long* hist, bool zero,
+             void* stream, int num_sms) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (zero) {
+    const cudaError_t e = cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * kCdcMaxT * 256, st);
+    if (e != cudaSuccess) return (int)e;
+  }
+  cdc_hist_kernel<<<cdc_grid(p.n_paths, num_sms), 256, 0, st>>>(y, p.n_paths, pass,
+                                                                 reinterpret_cast<const CdcScratch*>(scratch), hist);
+  return (int)cudaGetLastError();
+}
+
+int cdc_select(const RunParams& p, const CdcLevels& lv, void* scratch, int pass, unsigned long long* hist, bool clear,
+               void* stream) {
+  cdc_scan_kernel<<<1, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(pass, p.m, reinterpret_cast<CdcScratch*>(scratch),
+                                                                          lv, hist, clear ? 1 : 0);
+  return (int)cudaGetLastError();
+}
+
+int cdc_advance(const RunParams& p, void* scratch, const float* yin, float* yout, int step, bool stats, void* stream,
+                int num_sms) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   CdcScratch* s = reinterpret_cast<CdcScratch*>(scratch);
-  const uint64_t n = p.n_paths;
-  const unsigned grid = (unsigned)(((n + 255) / 256) < (uint64_t)num_sms * 8 ? (n + 255) / 256 : (uint64_t)num_sms * 8);
-  // row 0 = Y0
-  fill_kernel<<<grid, 256, 0, st>>>(rows[0], n, p.y0);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return (int)e;
-  const size_t hist = (p.has_stats && p.n_bins > 0) ? sizeof(uint32_t) * (size_t)(p.n_bins + 2) : 0;
+  if (p.colloc == kAnn) {
+    if (p.act == SL7_ACT_TANH) cdc_table_mlp_kernel<SL7_ACT_TANH><<<1, 256, 0, st>>>(p, s);
+    else cdc_table_mlp_kernel<SL7_ACT_SOFTPLUS><<<1, 256, 0, st>>>(p, s);
+  } else {
+    cdc_table_exact_kernel<<<1, kMaxM * kMaxM, 0, st>>>(p, s);
+  }
+  const size_t hist = (stats && p.has_stats && p.n_bins > 0) ? sizeof(uint32_t) * (size_t)(p.n_bins + 2) : 0;
   auto step_k = (p.m == 5) ? cdc_step_kernel<5, false> : (p.m == 7) ? cdc_step_kernel<7, false>
                                                                     : cdc_step_kernel<kMaxM, true>;
   if (hist > 48 * 1024) {
-    e = cudaFuncSetAttribute(step_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hist);
+    const cudaError_t e = cudaFuncSetAttribute(step_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hist);
     if (e != cudaSuccess) return (int)e;
   }
+  step_k<<<cdc_grid(p.n_paths, num_sms), 256, hist, st>>>(p, s, yin, yout, step, stats ? 1 : 0);
+  return (int)cudaGetLastError();
+}
+
+// Runs all n_steps of the CDC scheme on one device (the selection histograms live in the scratch).
+int launch_cdc(const RunParams& p, const CdcLevels& lv, void* scratch, float* const* rows, int nrows, void* stream,
+               int num_sms) {
+  CdcScratch* s = reinterpret_cast<CdcScratch*>(scratch);
+  unsigned long long* hist = &s->hist[0][0];
+  int e = cdc_fill(rows[0], p.n_paths, p.y0, stream, num_sms);   // row 0 = Y0
+  if (e) return e;
   for (int i = 0; i < p.n_steps; ++i) {
     const float* yin = rows[(nrows == 1) ? 0 : i];
     float* yout = rows[(nrows == 1) ? 0 : i + 1];
     for (int pass = 0; pass < 4; ++pass) {
-      cdc_hist_kernel<<<grid, 256, 0, st>>>(yin, n, pass, s);
-      cdc_scan_kernel<<<1, 256, 0, st>>>(pass, p.m, s, lv);
+      e = cdc_hist(p, scratch, yin, pass, hist, false, stream, num_sms);
+      if (e) return e;
+      e = cdc_select(p, lv, scratch, pass, hist, true, stream);
+      if (e) return e;
     }
-    if (p.colloc == kAnn) {
-      if (p.act == SL7_ACT_TANH) cdc_table_mlp_kernel<SL7_ACT_TANH><<<1, 256, 0, st>>>(p, s);
-      else cdc_table_mlp_kernel<SL7_ACT_SOFTPLUS><<<1, 256, 0, st>>>(p, s);
-    } else {
-      cdc_table_exact_kernel<<<1, kMaxM * kMaxM, 0, st>>>(p, s);
-    }
-    step_k<<<grid, 256, hist, st>>>(p, s, yin, yout, i, i == p.n_steps - 1 ? 1 : 0);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return (int)e;
+    e = cdc_advance(p, scratch, yin, yout, i, i == p.n_steps - 1 && p.has_stats, stream, num_sms);
+    if (e) return e;
   }
   return 0;
 }

@@ -58,6 +58,11 @@ struct sl7_ctx_s {
   size_t rows_cap = 0;
   float* d_term_scratch = nullptr;
   size_t term_cap = 0;
+  // sharded 7L-CDC run in progress (sl7_cdc_*)
+  RunParams cdc_p;
+  CdcLevels cdc_lv;
+  void* cdc_stream = nullptr;
+  bool cdc_ready = false;
   // 7L-CDC scratch (selection histograms + table) and state buffer for STATS-only runs
   void* d_cdc = nullptr;
   float* d_state = nullptr;
@@ -854,6 +859,77 @@ sl7_status sl7_training_set(sl7_ctx c, sl7_model model, const double* F, uint64_
     if (k) return cuda_fail(c, (cudaError_t)k, "training-set quantile kernel");
   }
   return SL7_OK;
+}
+
+size_t sl7_cdc_hist_elems(void) { return (size_t)2 * kMaxM * 256; }
+
+sl7_status sl7_cdc_init(sl7_ctx c, double Y0, double dt, int32_t n_steps, const double* theta, int32_t n_theta,
+                        uint64_t n_paths, uint64_t seed, const sl7_run_opts* opts, float* d_state) {
+  if (!c) return fail(c, SL7_EINVAL, "ctx is NULL");
+  if (!opts) return fail(c, SL7_EINVAL, "opts is NULL");
+  if (!d_state) return fail(c, SL7_EINVAL, "d_state is NULL");
+  c->cdc_ready = false;
+  sl7_run_opts o = *opts;
+  o.scheme = SL7_SCHEME_CDC;
+  RunParams p;
+  sl7_status s = prepare(c, Y0, dt, n_steps, theta, n_theta, n_paths, seed, SL7_OUT_STATS, &o, p, false, true);
+  if (s != SL7_OK) return s;
+  DeviceGuard g(c->device);
+  if (!g.ok) return fail(c, SL7_ECUDA, "cudaSetDevice(%d)", c->device);
+  if (!c->d_cdc) {
+    cudaError_t ce = cudaMalloc(&c->d_cdc, cdc_scratch_bytes());
+    if (ce != cudaSuccess) return cuda_fail(c, ce, "cudaMalloc(cdc scratch)");
+  }
+  int e = cdc_init_scratch(c->d_cdc, o.stream);
+  if (e) return cuda_fail(c, (cudaError_t)e, "cdc scratch init");
+  e = cdc_fill(d_state, n_paths, p.y0, o.stream, c->num_sms);
+  if (e) return cuda_fail(c, (cudaError_t)e, "cdc state init");
+  for (int k = 0; k < kMaxM; ++k) c->cdc_lv.p[k] = (k < c->m) ? 0.5 * std::erfc(-c->x[k] / std::sqrt(2.0)) : 0.0;
+  p.out_mode = kStatsOnly;
+  c->cdc_p = p;
+  c->cdc_stream = o.stream;
+  c->cdc_ready = true;
+  return SL7_OK;
+}
+
+sl7_status sl7_cdc_hist(sl7_ctx c, const float* d_state, int32_t pass, uint64_t* d_hist) {
+  if (!c) return fail(c, SL7_EINVAL, "ctx is NULL");
+  if (!c->cdc_ready) return fail(c, SL7_ESTATE, "sl7_cdc_hist before sl7_cdc_init");
+  if (!d_state || !d_hist) return fail(c, SL7_EINVAL, "d_state/d_hist is NULL");
+  if (pass < 0 || pass > 3) return fail(c, SL7_EINVAL, "pass must be 0..3");
+  DeviceGuard g(c->device);
+  if (!g.ok) return fail(c, SL7_ECUDA, "cudaSetDevice(%d)", c->device);
+  const int e = cdc_hist(c->cdc_p, c->d_cdc, d_state, pass, reinterpret_cast<unsigned long long*>(d_hist), true,
+                         c->cdc_stream, c->num_sms);
+  return e ? cuda_fail(c, (cudaError_t)e, "cdc histogram") : SL7_OK;
+}
+
+sl7_status sl7_cdc_select(sl7_ctx c, int32_t pass, const uint64_t* d_hist) {
+  if (!c) return fail(c, SL7_EINVAL, "ctx is NULL");
+  if (!c->cdc_ready) return fail(c, SL7_ESTATE, "sl7_cdc_select before sl7_cdc_init");
+  if (!d_hist) return fail(c, SL7_EINVAL, "d_hist is NULL");
+  if (pass < 0 || pass > 3) return fail(c, SL7_EINVAL, "pass must be 0..3");
+  DeviceGuard g(c->device);
+  if (!g.ok) return fail(c, SL7_ECUDA, "cudaSetDevice(%d)", c->device);
+  const int e = cdc_select(c->cdc_p, c->cdc_lv, c->d_cdc, pass,
+                           const_cast<unsigned long long*>(reinterpret_cast<const unsigned long long*>(d_hist)), false,
+                           c->cdc_stream);
+  return e ? cuda_fail(c, (cudaError_t)e, "cdc select") : SL7_OK;
+}
+
+sl7_status sl7_cdc_step(sl7_ctx c, int32_t step, const float* d_in, float* d_out, double* d_stats) {
+  if (!c) return fail(c, SL7_EINVAL, "ctx is NULL");
+  if (!c->cdc_ready) return fail(c, SL7_ESTATE, "sl7_cdc_step before sl7_cdc_init");
+  if (!d_in || !d_out) return fail(c, SL7_EINVAL, "d_in/d_out is NULL");
+  if (step < 0 || step >= c->cdc_p.n_steps) return fail(c, SL7_EINVAL, "step must be in 0..n_steps-1");
+  DeviceGuard g(c->device);
+  if (!g.ok) return fail(c, SL7_ECUDA, "cudaSetDevice(%d)", c->device);
+  RunParams p = c->cdc_p;
+  p.stats = d_stats;
+  p.has_stats = d_stats ? 1 : 0;
+  const int e = cdc_advance(p, c->d_cdc, d_in, d_out, step, d_stats != nullptr, c->cdc_stream,
+                            c->num_sms);
+  return e ? cuda_fail(c, (cudaError_t)e, "cdc step") : SL7_OK;
 }
 
 sl7_status sl7_simulate_host(sl7_ctx c, double Y0, double dt, int32_t n_steps, const double* theta, int32_t n_theta,

@@ -120,6 +120,15 @@ int cdc_init_scratch(void* scratch, void* stream);
 // rows: nrows == 1 -> one in-place state buffer; nrows == n_steps + 1 -> FULL output rows.
 int launch_cdc(const RunParams& p, const CdcLevels& lv, void* scratch, float* const* rows, int nrows, void* stream,
                int num_sms);
+// the pieces of one CDC step, for runs whose paths are sharded over ranks (sl7_cdc_*): the caller sums the
+// pass histograms ([2 SL7_MAX_M][256] u64) over ranks between cdc_hist and cdc_select.
+int cdc_fill(float* y, uint64_t n, float v, void* stream, int num_sms);
+int cdc_hist(const RunParams& p, void* scratch, const float* y, int pass, unsigned long long* hist, bool zero,
+             void* stream, int num_sms);
+int cdc_select(const RunParams& p, const CdcLevels& lv, void* scratch, int pass, unsigned long long* hist, bool clear,
+               void* stream);
+int cdc_advance(const RunParams& p, void* scratch, const float* yin, float* yout, int step, bool stats, void* stream,
+                int num_sms);
 
 // launchers (sl7_kernels.cu / sl7_tc.cu); return cudaError_t as int
 int launch_step_kernel(const RunParams& p, int prec, void* stream, int num_sms);
