@@ -312,10 +312,11 @@ def main():
                 "frac": achieved / peak,
                 # dram__bytes_read.sum + dram__bytes_write.sum of the n=64 launch (ncu --set full, recorded in
                 # profiles/r01_ann_tc_ncu.md): weights + stats only; the kernel reads no HBM per path-step
-                "traffic": 140288 + 69632, "traffic_note": "bytes per n=64 launch (1e7 paths x 64 steps)",
+                "traffic": 70656 + 149504, "traffic_note": "bytes per n=64 launch (1e7 paths x 64 steps)",
                 "peak_basis": "148 SM x 16 MUFU op/clk x %g MHz (max SM clock)" % sm_max,
                 "algorithmic": "%d transcendental activations per path-step (one per hidden unit); the kernel "
-                               "spends 2 MUFU ops per activation (ex2 + rcp / ex2 + lg2) for ~2e-7 accuracy" % trans_ps,
+                               "spends one MUFU op per tanh (MUFU.TANH, measured max error 9.9e-6 relative) and "
+                               "1.5 per softplus (ex2 + lg2, half of the log1p on the FMA pipe)" % trans_ps,
                 "tensor": {"achieved": tens, "peak": bf16, "unit": "TFLOP/s", "frac": tens / bf16,
                            "basis": "%d MMA FLOP per path-step vs MEASURED_PEAKS.json bf16_tflops (burst)" % mma_flops_ps,
                            "issued_per_algorithmic": 6 if prec == sl7.PREC_SPLIT else 1}}

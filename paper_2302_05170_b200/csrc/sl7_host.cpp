@@ -595,7 +595,12 @@ sl7_status run(sl7_ctx c, RunParams& p, const sl7_run_opts* o, float* d_out, dou
   } else if (p.colloc == kAnn && (o->prec == SL7_PREC_BF16 || o->prec == SL7_PREC_SPLIT)) {
     // per-run part of the TC parameters: layer 1 folded (as in RunParams) and pre-scaled in double
     TcParams t = c->tcp;
-    const double sc = (c->act == SL7_ACT_TANH) ? 2.0 / std::log(2.0) : 1.0;
+    const char* v = std::getenv("SL7_TC_VARIANT");
+    t.variant = v ? std::atoi(v) : 0;
+    t.split = (o->prec == SL7_PREC_SPLIT) ? 1 : 0;
+    // tanh on MUFU.TANH by default (variants 1..9 select the older ex2 + rcp epilogues for A/B timing)
+    t.tanh_mufu = (c->act == SL7_ACT_TANH && !t.split && (t.variant == 0 || t.variant >= 20)) ? 1 : 0;
+    const double sc = (c->act == SL7_ACT_TANH && !t.tanh_mufu) ? 2.0 / std::log(2.0) : 1.0;
     t.act_scale = (float)sc;
     for (int k = 0; k < kTcN; ++k) {
       t.l1w[k] = (float)(p.l1w_d[k] * sc);
@@ -603,9 +608,6 @@ sl7_status run(sl7_ctx c, RunParams& p, const sl7_run_opts* o, float* d_out, dou
     }
     for (int l = 0; l < t.n_mma_hidden; ++l)
       for (int k = 0; k < kTcN; ++k) t.bias[l][k] = (float)((double)c->tcp.bias[l][k] * sc);
-    const char* v = std::getenv("SL7_TC_VARIANT");
-    t.variant = v ? std::atoi(v) : 0;
-    t.split = (o->prec == SL7_PREC_SPLIT) ? 1 : 0;
     e = launch_tc_kernel(p, t, o->stream, c->num_sms);
   } else {
     e = launch_step_kernel(p, (int)o->prec, o->stream, c->num_sms);

@@ -109,6 +109,7 @@ struct TcParams {
   int n_mma_hidden;   // L - 1
   int variant;        // activation variant (experiment hook, SL7_TC_VARIANT)
   int split;          // 1: SL7_PREC_SPLIT
+  int tanh_mufu;      // tanh on MUFU.TANH (argument unscaled: act_scale = 1)
 };
 
 // 7L-CDC: quantile levels Phi(x_k) of the marginal collocation points (host, double).

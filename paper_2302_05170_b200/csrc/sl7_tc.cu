@@ -4,7 +4,8 @@
 //   layer 1 (rank 1 in Y after folding dt, theta)     : FFMA + activation, fp32, CUDA cores
 //   hidden layers 2..L and the output layer            : tcgen05.mma kind::f16, bf16 x bf16 -> fp32
 //                                                        [128 paths x 64] x [64 x 64] (output: x 16)
-//   bias + activation epilogue                         : tcgen05.ld -> FADD + MUFU -> bf16 -> tcgen05.st
+//   bias + activation epilogue                         : tcgen05.ld -> MUFU.TANH (tanh) or ex2 + lg2
+//                                                        (softplus) -> bf16 -> tcgen05.st
 //   Philox/Box-Muller normal, barycentric g_m, store   : CUDA cores, as in the fp32 kernels
 //
 // CTA = NG independent "tile groups" of 4 warps (128 threads).  Thread t of a group owns path t of
@@ -40,6 +41,34 @@ __device__ __forceinline__ float rcp12_newton(float s) {
   return r;
 }
 
+// Internal activation code of the TC kernel: tanh on the MUFU.TANH unit (tanh.approx.f32, max. relative
+// error ~2^-11, below the bf16 rounding of the activation that follows), argument unscaled (act_scale 1).
+constexpr int kActTanhX = 2;
+// softplus with one MUFU op per unit: e^{-|z|} on MUFU.EX2, log1p(e) by a minimax polynomial on the FMA pipe
+// (degree 8, abs. error 1.4e-7 on [0, 1]; degree 6 (1.3e-6) for the NMASK units).  A degree-5 polynomial
+// (8.8e-6) biased the terminal mean of cfg2 by 2e-3 relative (all 200 units err with the same sign).
+constexpr int kActSoftplusX = 3;
+
+__device__ __forceinline__ float tanh_mufu(float z) {
+  float r;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(r) : "f"(z));
+  return r;
+}
+
+// 2^v for v <= 0 on the FMA/ALU pipes: v = n + f (n = rint(v) by the 1.5 * 2^23 trick, f in [-1/2, 1/2]),
+// 2^f by its degree-4 Taylor polynomial (relative error <= 4.2e-5), 2^n added into the exponent field.
+__device__ __forceinline__ float exp2_fma(float v) {
+  v = fmaxf(v, -126.0f);
+  const float t = v + 12582912.0f;
+  const float f = v - (t - 12582912.0f);
+  const float p = fmaf(fmaf(fmaf(fmaf(9.6181291e-3f, f, 5.5504109e-2f), f, 2.4022651e-1f), f, 6.9314718e-1f), f, 1.0f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+}
+
+// tanh with no MUFU op: tanh|z| = (1 - e) / (1 + e), e = 2^(-2 log2(e) |z|) from exp2_fma, the reciprocal of
+// 1 + e in [1, 2] by rcp12_newton.  Absolute error <= ~1e-4 (2^-13).
+__device__ __forceinline__ float tanh_fma(float z);
+
 // Activation of the TC epilogue.  The argument is u = z * scale with scale = 2 log2(e) (tanh) or 1
 // (softplus), folded on the host into layer 1 and into the biases.
 //   tanh, 2 MUFU:      tanh = 1 - 2 / (2^u + 1)          (2^u -> 0 / inf gives -1 / 1 exactly)
@@ -47,9 +76,40 @@ __device__ __forceinline__ float rcp12_newton(float s) {
 //                      so its reciprocal is rcp12_newton on the FMA pipe; sign restored by copysign
 //   softplus, 2 MUFU:  max(z, 0) + ln2 log2(1 + 2^(-|z| log2 e))
 // Absolute error <= ~2e-7 in every variant.
+__device__ __forceinline__ float tanh_fma(float z) {
+  const float e = exp2_fma(fabsf(z) * -2.8853900817779268f);
+  const float r = rcp12_newton(1.0f + e);
+  return copysignf(fmaf(-e, r, r), z);
+}
+
 template <int ACT>
 __device__ __forceinline__ float tc_act_u(float u, bool newton) {
-  if constexpr (ACT == SL7_ACT_TANH) {
+  if constexpr (ACT == kActTanhX) {
+    return newton ? tanh_fma(u) : tanh_mufu(u);
+  } else if constexpr (ACT == kActSoftplusX) {
+    const float e = ex2_approx(fabsf(u) * -1.4426950408889634f);
+    float lp;
+    if (newton) {   // degree 6: abs. error 1.3e-6
+      lp = -1.7807194e-02f;
+      lp = fmaf(lp, e, 8.3869926e-02f);
+      lp = fmaf(lp, e, -1.9167948e-01f);
+      lp = fmaf(lp, e, 3.1643384e-01f);
+      lp = fmaf(lp, e, -4.9753391e-01f);
+      lp = fmaf(lp, e, 9.9986143e-01f);
+      lp = fmaf(lp, e, 1.2839006e-06f);
+    } else {        // degree 8: abs. error 1.4e-7
+      lp = -6.301349960e-03f;
+      lp = fmaf(lp, e, 3.544928879e-02f);
+      lp = fmaf(lp, e, -9.422647208e-02f);
+      lp = fmaf(lp, e, 1.666473895e-01f);
+      lp = fmaf(lp, e, -2.402127683e-01f);
+      lp = fmaf(lp, e, 3.316470385e-01f);
+      lp = fmaf(lp, e, -4.998508692e-01f);
+      lp = fmaf(lp, e, 9.999948740e-01f);
+      lp = fmaf(lp, e, 2.928694798e-08f);
+    }
+    return fmaxf(u, 0.0f) + lp;
+  } else if constexpr (ACT == SL7_ACT_TANH) {
     if (newton) {   // compile-time after unrolling
       const float e = ex2_approx(-fabsf(u));
       const float r = rcp12_newton(1.0f + e);
@@ -110,7 +170,7 @@ __device__ __forceinline__ void act_pack_32(const uint32_t (&v)[32], int col0, f
       const int c = col0 + 2 * k + q;
       if (c < H) {
         const float acc = __uint_as_float(v[2 * k + q]);
-        const float u = FOLD ? acc * scale : fmaf(acc, scale, bs[c]);
+        const float u = FOLD ? ((ACT == kActTanhX || ACT == kActSoftplusX) ? acc : acc * scale) : fmaf(acc, scale, bs[c]);
         h[q] = tc_act_u<ACT>(u, use_newton<ACT, NMASK>(c));
       } else {
         h[q] = (FOLD && c < H + 3) ? 1.0f : 0.0f;
@@ -162,6 +222,13 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
   const int nL = t.n_mma_hidden;
   const int wbytes = NP * (nL * kTcTileBytes + kTcOutBytes);
   uint32_t* hist = reinterpret_cast<uint32_t*>(wsm + wbytes);
+  // per-thread running sums of the statistics live in shared memory ([8][threads], SoA), not in registers:
+  // they change once per tile, and the 12 registers they would pin are worth more to the epilogue
+  const int hist_words = (p.has_stats && p.n_bins > 0) ? ((p.n_bins + 2 + 1) & ~1) : 0;
+  double* sst = reinterpret_cast<double*>(hist + hist_words);
+  constexpr int kThreads = NG * kGroupThreads;
+  if (p.has_stats)
+    for (int k = 0; k < 8; ++k) sst[k * kThreads + threadIdx.x] = 0.0;
   {
     const uint4* src = reinterpret_cast<const uint4*>(NP == 1 ? t.wimg : t.wimg_split);
     uint4* dst = reinterpret_cast<uint4*>(wsm);
@@ -187,7 +254,6 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
   uint64_t* bar = &mbar[g];
   uint32_t phase = 0;
 
-  StatAcc acc;
   const uint64_t n_tiles = (p.n_paths + kGroupThreads - 1) / kGroupThreads;
   for (uint64_t tile = (uint64_t)blockIdx.x * NG + g; tile < n_tiles; tile += (uint64_t)gridDim.x * NG) {
     const uint64_t q = tile * kGroupThreads + tid_g;
@@ -277,10 +343,27 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
     }
     if (valid) {
       if (p.out_mode == kTerminal) p.out[q] = Y;
-      if (p.has_stats) stat_add(acc, p, Y, ref_final(rs, p), hist);
+      if (p.has_stats) {
+        StatAcc a;
+        stat_add(a, p, Y, ref_final(rs, p), hist);
+        const double v[8] = {a.s1, a.s2, a.s3, a.s4, a.e1, a.e2, (double)a.n, (double)a.nnf};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) sst[k * kThreads + threadIdx.x] += v[k];
+      }
     }
   }
-  if (p.has_stats) stat_flush(acc, p, hist, red);
+  if (p.has_stats) {
+    StatAcc acc;
+    acc.s1 = sst[0 * kThreads + threadIdx.x];
+    acc.s2 = sst[1 * kThreads + threadIdx.x];
+    acc.s3 = sst[2 * kThreads + threadIdx.x];
+    acc.s4 = sst[3 * kThreads + threadIdx.x];
+    acc.e1 = sst[4 * kThreads + threadIdx.x];
+    acc.e2 = sst[5 * kThreads + threadIdx.x];
+    acc.n = (uint32_t)sst[6 * kThreads + threadIdx.x];
+    acc.nnf = (uint32_t)sst[7 * kThreads + threadIdx.x];
+    stat_flush(acc, p, hist, red);
+  }
   tc::fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc(tbase, kTmemCols);
@@ -291,8 +374,9 @@ namespace {
 template <int NG, int H, int MR, bool RT, int ACT, unsigned NMASK = 0u, int NP = 1, bool SKIP = false>
 cudaError_t launch_tc_t(const RunParams& p, const TcParams& t, cudaStream_t st, int num_sms) {
   auto kernel = ann_tc_step_kernel<NG, H, MR, RT, ACT, NMASK, NP, SKIP>;
-  const size_t hist = (p.has_stats && p.n_bins > 0) ? sizeof(uint32_t) * (size_t)(p.n_bins + 2) : 0;
-  const size_t smem = 1024 + (size_t)NP * ((size_t)t.n_mma_hidden * kTcTileBytes + kTcOutBytes) + hist;
+  const size_t hist = (p.has_stats && p.n_bins > 0) ? sizeof(uint32_t) * (size_t)((p.n_bins + 2 + 1) & ~1) : 0;
+  const size_t sst = p.has_stats ? sizeof(double) * 8 * NG * kGroupThreads : 0;
+  const size_t smem = 1024 + (size_t)NP * ((size_t)t.n_mma_hidden * kTcTileBytes + kTcOutBytes) + hist + sst;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const uint64_t tiles = (p.n_paths + kGroupThreads - 1) / kGroupThreads;
@@ -312,9 +396,12 @@ constexpr unsigned kSoftplusPolyMask = 0x55u;
 // SL7_PREC_SPLIT: three bf16 parts per operand (TMEM 64 + 3 x 32 = 160 columns per group -> 3 groups).
 constexpr int kTcGroupsSplit = 3;
 
+// softplus (2 MUFU ops per unit on half of the units): 5 groups per SM, as for tanh (cfg2: 1.03e10 vs 9.4e9)
+constexpr int kTcGroupsSoftplus = 5;
+
 template <int ACT>
 cudaError_t launch_tc_act(const RunParams& p, const TcParams& t, cudaStream_t st, int num_sms) {
-  constexpr int NG = kTcGroups;
+  constexpr int NG = (ACT == SL7_ACT_SOFTPLUS) ? kTcGroupsSoftplus : kTcGroups;
   constexpr unsigned NM = (ACT == SL7_ACT_TANH) ? kTanhNewtonMask : kSoftplusPolyMask;
   if (t.split) {
     constexpr int NS = kTcGroupsSplit;
@@ -335,10 +422,51 @@ cudaError_t launch_tc_act(const RunParams& p, const TcParams& t, cudaStream_t st
   return launch_tc_t<NG, 64, kMaxM, true, ACT, NM>(p, t, st, num_sms);
 }
 
+// tanh on MUFU.TANH (kActTanhX): all units on the MUFU unit.  The epilogue is short, so the share of time
+// a group waits for its MMA grows; 5 groups per SM (480 of 512 TMEM columns, <= 96 registers) keep the MUFU
+// unit fed better than 4 (cfg1: 2.28e10 vs 2.18e10 path-steps/s).
+constexpr int kTcGroupsTanhX = 5;
+
+cudaError_t launch_tc_act_x(const RunParams& p, const TcParams& t, cudaStream_t st, int num_sms) {
+  constexpr int NG = kTcGroupsTanhX;
+  constexpr unsigned NM = 0x00u;
+  if (t.split) {
+    constexpr int NS = kTcGroupsSplit;
+    if (p.width == 50 && p.m == 5) return launch_tc_t<NS, 50, 5, false, kActTanhX, NM, 3>(p, t, st, num_sms);
+    if (p.width == 50 && p.m == 7) return launch_tc_t<NS, 50, 7, false, kActTanhX, NM, 3>(p, t, st, num_sms);
+    return launch_tc_t<NS, 64, kMaxM, true, kActTanhX, NM, 3>(p, t, st, num_sms);
+  }
+  if (p.width == 50 && p.m == 5) return launch_tc_t<NG, 50, 5, false, kActTanhX, NM>(p, t, st, num_sms);
+  if (p.width == 50 && p.m == 7) return launch_tc_t<NG, 50, 7, false, kActTanhX, NM>(p, t, st, num_sms);
+  return launch_tc_t<NG, 64, kMaxM, true, kActTanhX, NM>(p, t, st, num_sms);
+}
+
 }  // namespace
 
 int launch_tc_kernel(const RunParams& p, const TcParams& t, void* stream, int num_sms) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (p.act == SL7_ACT_SOFTPLUS && !t.split && t.variant >= 30 && p.width == 50 && p.m == 7) {
+    switch (t.variant) {   // A/B hooks: one-MUFU softplus, group count, FMA-pipe share
+      case 30: return (int)launch_tc_t<5, 50, 7, false, kActSoftplusX, 0x00u>(p, t, st, num_sms);
+      case 32: return (int)launch_tc_t<5, 50, 7, false, kActSoftplusX, 0xFFu>(p, t, st, num_sms);
+      case 34: return (int)launch_tc_t<5, 50, 7, false, SL7_ACT_SOFTPLUS, 0x77u>(p, t, st, num_sms);
+      case 35: return (int)launch_tc_t<4, 50, 7, false, SL7_ACT_SOFTPLUS, 0x55u>(p, t, st, num_sms);
+      default: break;
+    }
+  }
+  if (p.act == SL7_ACT_TANH && t.tanh_mufu) {
+    if (p.width == 50 && p.m == 7 && !t.split) {
+      switch (t.variant) {   // A/B hook: units on the FMA-pipe tanh (mask over unit % 8)
+        case 21: return (int)launch_tc_t<kTcGroups, 50, 7, false, kActTanhX, 0x01u>(p, t, st, num_sms);
+        case 22: return (int)launch_tc_t<kTcGroups, 50, 7, false, kActTanhX, 0x11u>(p, t, st, num_sms);
+        case 23: return (int)launch_tc_t<kTcGroups, 50, 7, false, kActTanhX, 0x25u>(p, t, st, num_sms);
+        case 24: return (int)launch_tc_t<kTcGroups, 50, 7, false, kActTanhX, 0x55u>(p, t, st, num_sms);
+        case 25: return (int)launch_tc_t<4, 50, 7, false, kActTanhX, 0x00u>(p, t, st, num_sms);
+        default: break;
+      }
+    }
+    return (int)launch_tc_act_x(p, t, st, num_sms);
+  }
   return (int)(p.act == SL7_ACT_TANH ? launch_tc_act<SL7_ACT_TANH>(p, t, st, num_sms)
                                      : launch_tc_act<SL7_ACT_SOFTPLUS>(p, t, st, num_sms));
 }

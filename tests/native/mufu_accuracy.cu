@@ -2,9 +2,19 @@
 //   lg2.approx.f32 on u = 1 - j 2^-24 (the relative accuracy of log near 1 decides the tail normals)
 //   lg2.approx.f32 on (0, 1) (absolute error)
 //   sin.approx / cos.approx on (-pi, pi) (absolute error)
+//   tanh.approx.f32 (MUFU.TANH) on (-12, 12) (absolute and relative error; the TC kernel's tanh)
 #include <cmath>
 #include <cstdio>
 #include <cuda_runtime.h>
+
+__global__ void probe_tanh(int n, float* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float z = -12.0f + 24.0f * ((float)i + 0.5f) / (float)n;
+  float r;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(r) : "f"(z));
+  out[i] = r;
+}
 
 __global__ void probe(int n, float* lg_near1, float* lg_any, float* s, float* c) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -44,6 +54,20 @@ int main() {
   }
   printf("{\"lg2_near1_max_rel\": %.3g, \"worst_j\": %d, \"lg2_abs_any\": %.3g, \"sin_abs\": %.3g, \"cos_abs\": %.3g}\n",
          m_rel_near1, worst_j, m_abs_any, m_sin, m_cos);
+  {
+    probe_tanh<<<(n + 255) / 256, 256>>>(n, d[0]);
+    cudaMemcpy(h, d[0], sizeof(float) * n, cudaMemcpyDeviceToHost);
+    double m_abs = 0, m_rel = 0, z_abs = 0, z_rel = 0, sum_err = 0;
+    for (int i = 0; i < n; ++i) {
+      const double z = (double)(-12.0f + 24.0f * ((float)i + 0.5f) / (float)n);
+      const double ref = std::tanh(z), e = (double)h[i] - ref;
+      sum_err += e;
+      if (std::fabs(e) > m_abs) { m_abs = std::fabs(e); z_abs = z; }
+      if (ref != 0 && std::fabs(e / ref) > m_rel) { m_rel = std::fabs(e / ref); z_rel = z; }
+    }
+    printf("{\"tanh_approx_max_abs\": %.3g, \"at\": %.4g, \"max_rel\": %.3g, \"at_rel\": %.4g, \"mean_err\": %.3g}\n",
+           m_abs, z_abs, m_rel, z_rel, sum_err / n);
+  }
   // relative error of lg2 for j = 1, 2, 4, ..., 2^22
   for (int j = 1; j <= (1 << 22); j <<= 2) {
     double u = 1.0 - (double)j * std::ldexp(1.0, -24);
