@@ -38,84 +38,137 @@ struct CdcScratch {
   double zd[kMaxM];
 };
 
-// ---- pass p: histogram of digit p (bits [24 - 8p, 32 - 8p)) of the elements matching a slot prefix
+// ---- pass p: histogram of digit p (bits [24 - 8p, 32 - 8p)) of the elements matching a slot prefix.
+// The states of one step are concentrated in a few digit bins, so the shared-memory increments are
+// warp-aggregated (__match_any_sync: one atomic per distinct bin per warp) instead of one per element.
+__device__ __forceinline__ void warp_hist_add(uint32_t* h, int bin) {   // bin < 0: nothing (all lanes call)
+  const unsigned peers = __match_any_sync(0xffffffffu, bin);
+  if (bin >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[bin], (uint32_t)__popc(peers));
+}
+
 __global__ void __launch_bounds__(256) cdc_hist_kernel(const float* __restrict__ y, uint64_t n, int pass,
                                                        const CdcScratch* s, unsigned long long* __restrict__ hist) {
-  __shared__ uint32_t h[kCdcMaxT][256];
+  __shared__ uint32_t h[kCdcMaxT * 256];
   __shared__ uint32_t sp[kCdcMaxT];
   const int nslot = s->nslot;
-  for (int i = threadIdx.x; i < nslot * 256; i += blockDim.x) h[i >> 8][i & 255] = 0u;
+  for (int i = threadIdx.x; i < nslot * 256; i += blockDim.x) h[i] = 0u;
   if (threadIdx.x < nslot) sp[threadIdx.x] = s->slot_prefix[threadIdx.x];
   __syncthreads();
   const int shift = 24 - 8 * pass;
   const uint32_t lo = sp[0], hi = sp[nslot - 1];
-  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (uint64_t)gridDim.x * blockDim.x) {
-    const float v = y[q];
-    if (!isfinite(v)) continue;
-    const uint32_t key = f2key(v);
-    const uint32_t digit = (key >> shift) & 255u;
-    int slot = 0;
-    if (pass > 0) {
-      const uint32_t pre = key >> (shift + 8);
-      if (pre < lo || pre > hi) continue;
-      int a = 0, b = nslot - 1;   // binary search in the ascending slot prefixes
-      while (a < b) {
-        const int mid = (a + b) >> 1;
-        if (sp[mid] < pre) a = mid + 1; else b = mid;
-      }
-      if (sp[a] != pre) continue;
-      slot = a;
+  const int lane = threadIdx.x & 31;
+  // each warp takes chunks of 128 consecutive elements: 4 coalesced loads in flight per thread, then the
+  // four (warp-aggregated) increments; the trip count is warp-uniform, so every lane joins each match
+  constexpr int U = 4;
+  const uint64_t wstride = (uint64_t)gridDim.x * blockDim.x * U;
+  for (uint64_t base = ((uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) * U; base < n; base += wstride) {
+    float v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t q = base + 32 * u + lane;
+      v[u] = (q < n) ? y[q] : __int_as_float(0x7F800000);   // +inf: skipped below
     }
-    atomicAdd(&h[slot][digit], 1u);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      int bin = -1;
+      if (isfinite(v[u])) {
+        const uint32_t key = f2key(v[u]);
+        const int digit = (int)((key >> shift) & 255u);
+        if (pass == 0) {
+          bin = digit;
+        } else {
+          const uint32_t pre = key >> (shift + 8);
+          if (pre >= lo && pre <= hi) {
+            int a = 0, b = nslot - 1;   // binary search in the ascending slot prefixes
+            while (a < b) {
+              const int mid = (a + b) >> 1;
+              if (sp[mid] < pre) a = mid + 1; else b = mid;
+            }
+            if (sp[a] == pre) bin = a * 256 + digit;
+          }
+        }
+      }
+      warp_hist_add(h, bin);
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < nslot * 256; i += blockDim.x) {
-    const uint32_t c = h[i >> 8][i & 255];
+    const uint32_t c = h[i];
     if (c) atomicAdd(&hist[i], (unsigned long long)c);
   }
 }
 
-// ---- after pass p: fix each target's digit; set up the next pass (one block of 256 threads)
+// ---- after pass p: fix each target's digit; set up the next pass.  One block of 1024 threads: warp t
+// finds target t's bin with a warp scan over the slot's 256 counts (lane l owns bins 8l..8l+7).
 // hist: [slot][256] counts of this pass over ALL paths of the run (summed over ranks for a sharded run);
 // clear: zero it afterwards (the single-call path reuses the scratch histogram).
-__global__ void __launch_bounds__(256) cdc_scan_kernel(int pass, int m, CdcScratch* s, const __grid_constant__ CdcLevels lv,
-                                                       unsigned long long* hist, int clear) {
-  const int T = 2 * m;
-  if (threadIdx.x == 0) {
-    if (pass == 0) {
-      // M finite states; target order statistics (0-based) of the plotting-position quantiles
+__global__ void __launch_bounds__(1024) cdc_scan_kernel(int pass, int m, CdcScratch* s, const __grid_constant__ CdcLevels lv,
+                                                        unsigned long long* hist, int clear) {
+  const int T = 2 * m, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (pass == 0) {
+    if (warp == 0) {
       unsigned long long M = 0;
-      for (int b = 0; b < 256; ++b) M += hist[b];
-      s->M = M;
-      for (int k = 0; k < m && M == 0; ++k) {   // no finite state: every target at rank 0 (z = NaN below)
-        s->frac[k] = 0.0;
-        s->rank[2 * k] = s->rank[2 * k + 1] = 0ull;
-        s->prefix[2 * k] = s->prefix[2 * k + 1] = 0u;
-      }
-      for (int k = 0; k < m && M > 0; ++k) {
-        double pos = lv.p[k] * (double)M + 0.5;                  // 1-based fractional rank
-        if (pos < 1.0) pos = 1.0;
-        if (pos > (double)M) pos = (double)M;
-        const double kk = floor(pos);
-        s->frac[k] = pos - kk;
-        const unsigned long long r0 = (unsigned long long)kk - 1ull;
-        const unsigned long long r1 = ((unsigned long long)kk < M) ? (unsigned long long)kk : M - 1ull;
-        s->rank[2 * k] = r0;
-        s->rank[2 * k + 1] = r1;
-        s->prefix[2 * k] = s->prefix[2 * k + 1] = 0u;
+      for (int b = lane; b < 256; b += 32) M += hist[b];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) M += __shfl_xor_sync(0xffffffffu, M, o);
+      if (lane == 0) s->M = M;
+      if (lane < m) {
+        // target order statistics (0-based) of the plotting-position quantile (as the oracle:
+        // pos = p M + 0.5 clamped to [1, M], k = floor(pos), f = pos - k, ranks k - 1 and min(k, M - 1))
+        double f = 0.0;
+        unsigned long long r0 = 0ull, r1 = 0ull;   // no finite state: every target at rank 0 (z = NaN below)
+        if (M > 0) {
+          double pos = __dadd_rn(__dmul_rn(lv.p[lane], (double)M), 0.5);
+          pos = fmin(fmax(pos, 1.0), (double)M);
+          const double kk = floor(pos);
+          f = pos - kk;
+          r0 = (unsigned long long)kk - 1ull;
+          r1 = ((unsigned long long)kk < M) ? (unsigned long long)kk : M - 1ull;
+        }
+        s->frac[lane] = f;
+        s->rank[2 * lane] = r0;
+        s->rank[2 * lane + 1] = r1;
+        s->prefix[2 * lane] = s->prefix[2 * lane + 1] = 0u;
       }
     }
-    // descend one digit per target
-    for (int t = 0; t < T; ++t) {
-      const int sl = (pass == 0) ? 0 : s->slot_of[t];
-      const unsigned long long r = s->rank[t];
-      int b = 0;
-      unsigned long long below = 0;   // elements of this prefix in bins < b
-      const unsigned long long* h = hist + 256 * sl;
-      while (b < 255 && below + h[b] <= r) below += h[b++];
+    __syncthreads();
+  }
+  if (warp < T && s->M > 0) {
+    const int t = warp, sl = (pass == 0) ? 0 : s->slot_of[t];
+    const unsigned long long r = s->rank[t];
+    const unsigned long long* hs = hist + 256 * sl;
+    unsigned long long c[8], sum = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      c[u] = hs[lane * 8 + u];
+      sum += c[u];
+    }
+    unsigned long long inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long nb = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += nb;
+    }
+    const unsigned long long exc = inc - sum;
+    if (r >= exc && r < inc) {
+      unsigned long long below = exc;
+      int b = lane * 8;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (below + c[u] > r) {
+          b = lane * 8 + u;
+          break;
+        }
+        below += c[u];
+      }
       s->rank[t] = r - below;
       s->prefix[t] = (s->prefix[t] << 8) | (uint32_t)b;
     }
+  } else if (warp < T && lane == 0) {
+    s->prefix[warp] <<= 8;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
     if (pass < 3) {
       // distinct prefixes (targets are ordered by rank, so prefixes are non-decreasing)
       int ns = 0;
@@ -130,7 +183,8 @@ __global__ void __launch_bounds__(256) cdc_scan_kernel(int pass, int m, CdcScrat
       for (int k = 0; k < m; ++k) {
         const double a = (double)key2f(s->prefix[2 * k]), b = (double)key2f(s->prefix[2 * k + 1]);
         const double f = s->frac[k];
-        s->zd[k] = (s->M > 0) ? a * (1.0 - f) + b * f : __longlong_as_double(0x7FF8000000000000ll);
+        s->zd[k] = (s->M > 0) ? __dadd_rn(__dmul_rn(a, 1.0 - f), __dmul_rn(b, f))
+                              : __longlong_as_double(0x7FF8000000000000ll);
         if (k > 0 && !(s->zd[k] > s->zd[k - 1])) degen = 1;   // repeated (or NaN) marginal points
       }
       s->degenerate = degen;
@@ -205,11 +259,14 @@ __global__ void __launch_bounds__(256) cdc_table_mlp_kernel(const __grid_constan
 template <int MR, bool RT_M>
 __global__ void __launch_bounds__(256) cdc_step_kernel(const __grid_constant__ RunParams p, const CdcScratch* s,
                                                        const float* yin, float* yout,   // may alias (in place)
-                                                       int step, int last) {
+                                                       int step, int last, unsigned long long* next_hist) {
   extern __shared__ uint32_t hist[];
   __shared__ double red[8];
   __shared__ float sz[kMaxM], sv[kMaxM], sC[kMaxM][kMaxM];
   __shared__ int sdeg;
+  __shared__ uint32_t nh[256];   // pass-0 digit histogram of the new states (next step's selection)
+  if (next_hist)
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) nh[i] = 0u;
   for (int i = threadIdx.x; i < kMaxM * kMaxM; i += blockDim.x) {
     const int k = i / kMaxM, j = i % kMaxM;
     sC[k][j] = (k < p.m && j < p.m) ? s->C[k][j] : 0.0f;
@@ -222,9 +279,23 @@ __global__ void __launch_bounds__(256) cdc_step_kernel(const __grid_constant__ R
   if (last) hist_init(p, hist);
   __syncthreads();
   const int m = p.m;
+  // the m x m table in registers when m is a compile-time constant (49 for m = 7): it is the same for every
+  // path, and reading it from shared memory cost one LDS per FFMA of the contraction below
+  float Cr[RT_M ? 1 : MR][RT_M ? 1 : MR];
+  if constexpr (!RT_M) {
+#pragma unroll
+    for (int k = 0; k < MR; ++k)
+#pragma unroll
+      for (int j = 0; j < MR; ++j) Cr[k][j] = sC[k][j];
+  }
   StatAcc acc;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < p.n_paths; q += stride) {
+  const int lane = threadIdx.x & 31;
+  // warp-uniform trip count (the fused histogram's __match_any_sync needs every lane)
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < p.n_paths; base += stride) {
+    const uint64_t q = base + lane;
+    int nbin = -1;
+    if (q < p.n_paths) {
     const float Y = yin[q];
     float y[MR];
     if (sdeg) {
@@ -256,21 +327,33 @@ __global__ void __launch_bounds__(256) cdc_step_kernel(const __grid_constant__ R
       for (int j = 0; j < MR; ++j) {
         float a = 0.0f;
 #pragma unroll
-        for (int k = 0; k < MR; ++k) a = fmaf(lk[k], sC[k][j], a);
+        for (int k = 0; k < MR; ++k) {
+          if constexpr (RT_M) a = fmaf(lk[k], sC[k][j], a);
+          else a = fmaf(lk[k], Cr[k][j], a);
+        }
         y[j] = a * rden;
       }
     }
-    // X_hat for (path, step) and g_m on the Gauss-Hermite grid
+    // X_hat for (path, step): the Philox block of the step, then only the Box-Muller pair that holds it
     const uint64_t gp = p.path_offset + q;
-    float z4[4];
-    normals4_rk<false>(p, gp, (uint32_t)(step >> 2), z4[0], z4[1], z4[2], z4[3]);
+    const uint4 rr = philox_path_block_rk(p.rk0, p.rk1, gp, (uint32_t)(step >> 2));
     const int r = step & 3;
-    const float Z = (r == 0) ? z4[0] : (r == 1) ? z4[1] : (r == 2) ? z4[2] : z4[3];
+    float za, zb;
+    box_muller((r < 2) ? rr.x : rr.z, (r < 2) ? rr.y : rr.w, za, zb);
+    const float Z = (r & 1) ? zb : za;
     const float Yn = gm_eval<MR, RT_M>(p, Z, y);
     yout[q] = Yn;
     if (last && p.has_stats) stat_add(acc, p, Yn, 0.0, hist);
+    nbin = isfinite(Yn) ? (int)(f2key(Yn) >> 24) : -1;
+    }
+    if (next_hist) warp_hist_add(nh, nbin);   // one call site, all lanes
   }
   if (last && p.has_stats) stat_flush(acc, p, hist, red);
+  if (next_hist) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256; i += blockDim.x)
+      if (nh[i]) atomicAdd(&next_hist[i], (unsigned long long)nh[i]);
+  }
 }
 
 __global__ void fill_kernel(float* y, uint64_t n, float v) {
@@ -315,13 +398,13 @@ int cdc_hist(const RunParams& p, void* scratch, const float* y, int pass, unsign
 
 int cdc_select(const RunParams& p, const CdcLevels& lv, void* scratch, int pass, unsigned long long* hist, bool clear,
                void* stream) {
-  cdc_scan_kernel<<<1, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(pass, p.m, reinterpret_cast<CdcScratch*>(scratch),
+  cdc_scan_kernel<<<1, 1024, 0, reinterpret_cast<cudaStream_t>(stream)>>>(pass, p.m, reinterpret_cast<CdcScratch*>(scratch),
                                                                           lv, hist, clear ? 1 : 0);
   return (int)cudaGetLastError();
 }
 
 int cdc_advance(const RunParams& p, void* scratch, const float* yin, float* yout, int step, bool stats, void* stream,
-                int num_sms) {
+                int num_sms, unsigned long long* next_hist) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   CdcScratch* s = reinterpret_cast<CdcScratch*>(scratch);
   if (p.colloc == kAnn) {
@@ -337,7 +420,7 @@ int cdc_advance(const RunParams& p, void* scratch, const float* yin, float* yout
     const cudaError_t e = cudaFuncSetAttribute(step_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hist);
     if (e != cudaSuccess) return (int)e;
   }
-  step_k<<<cdc_grid(p.n_paths, num_sms), 256, hist, st>>>(p, s, yin, yout, step, stats ? 1 : 0);
+  step_k<<<cdc_grid(p.n_paths, num_sms), 256, hist, st>>>(p, s, yin, yout, step, stats ? 1 : 0, next_hist);
   return (int)cudaGetLastError();
 }
 
@@ -352,12 +435,15 @@ int launch_cdc(const RunParams& p, const CdcLevels& lv, void* scratch, float* co
     const float* yin = rows[(nrows == 1) ? 0 : i];
     float* yout = rows[(nrows == 1) ? 0 : i + 1];
     for (int pass = 0; pass < 4; ++pass) {
-      e = cdc_hist(p, scratch, yin, pass, hist, false, stream, num_sms);
-      if (e) return e;
+      if (pass > 0 || i == 0) {   // pass 0 of steps >= 1: histogrammed by the previous step kernel
+        e = cdc_hist(p, scratch, yin, pass, hist, false, stream, num_sms);
+        if (e) return e;
+      }
       e = cdc_select(p, lv, scratch, pass, hist, true, stream);
       if (e) return e;
     }
-    e = cdc_advance(p, scratch, yin, yout, i, i == p.n_steps - 1 && p.has_stats, stream, num_sms);
+    const bool last = (i == p.n_steps - 1);
+    e = cdc_advance(p, scratch, yin, yout, i, last && p.has_stats, stream, num_sms, last ? nullptr : hist);
     if (e) return e;
   }
   return 0;

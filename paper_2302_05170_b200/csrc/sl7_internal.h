@@ -129,7 +129,7 @@ int cdc_hist(const RunParams& p, void* scratch, const float* y, int pass, unsign
 int cdc_select(const RunParams& p, const CdcLevels& lv, void* scratch, int pass, unsigned long long* hist, bool clear,
                void* stream);
 int cdc_advance(const RunParams& p, void* scratch, const float* yin, float* yout, int step, bool stats, void* stream,
-                int num_sms);
+                int num_sms, unsigned long long* next_hist = nullptr);
 
 // launchers (sl7_kernels.cu / sl7_tc.cu); return cudaError_t as int
 int launch_step_kernel(const RunParams& p, int prec, void* stream, int num_sms);

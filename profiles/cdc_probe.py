@@ -1,0 +1,25 @@
+"""One 7L-CDC run of cfg2 OU (ANN fp32 table, 1e8 paths x 16 steps, STATS) for ncu launch lists:
+
+  ncu --metrics gpu__time_duration.sum -k regex:cdc_ --csv python profiles/cdc_probe.py
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import paper_2302_05170_b200 as sl7  # noqa: E402
+from sl7_inputs import load_golden_blob, workloads  # noqa: E402
+
+torch.cuda.set_device(0)
+w = workloads()["cfg2_ou"]
+N = int(sys.argv[1]) if len(sys.argv) > 1 else 100_000_000
+ctx = sl7.Context(w.m, list(w.dims), w.act, device=0)
+ctx.load_weights(load_golden_blob(w.blob))
+st = torch.zeros(sl7.stats_elems(4096), dtype=torch.float64, device="cuda")
+opts = sl7.make_opts(prec=sl7.PREC_FP32, colloc=sl7.COLLOC_ANN, scheme=sl7.SCHEME_CDC, n_bins=4096, hist_lo=-3.0,
+                     hist_hi=3.0, shift=1.0)
+ctx.simulate(w.y0, w.dt, w.n_steps, w.theta, N, w.seed, sl7.OUT_STATS, opts, stats=st)
+torch.cuda.synchronize()
+print("ok", sl7.stats_summary(st.cpu().numpy(), opts)["mean"])
