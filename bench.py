@@ -131,7 +131,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="sl7", choices=["sl7", "reference"])
-    ap.add_argument("--prec", default="auto", choices=["auto", "fp32", "bf16", "split"])
+    ap.add_argument("--prec", default="auto", choices=["auto", "fp32", "bf16", "tf32", "split"])
     ap.add_argument("--paths", type=int, default=10_000_000, help="paths per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     a = ap.parse_args()
@@ -181,8 +181,9 @@ def main():
     blob = load_golden_blob(W.blob)
     ctx = sl7.Context(W.m, list(W.dims), W.act, device=local)
     ctx.load_weights(blob)
-    prec = {"auto": sl7.PREC_FP32, "fp32": sl7.PREC_FP32, "bf16": sl7.PREC_BF16, "split": sl7.PREC_SPLIT}[a.prec]
-    prec_name = {sl7.PREC_FP32: "fp32", sl7.PREC_BF16: "bf16", sl7.PREC_SPLIT: "split-bf16x3"}
+    prec = {"auto": sl7.PREC_FP32, "fp32": sl7.PREC_FP32, "bf16": sl7.PREC_BF16, "tf32": sl7.PREC_TF32,
+            "split": sl7.PREC_SPLIT}[a.prec]
+    prec_name = {sl7.PREC_FP32: "fp32", sl7.PREC_BF16: "bf16", sl7.PREC_TF32: "tf32", sl7.PREC_SPLIT: "split-bf16x3"}
     if a.prec == "auto" and getattr(sl7, "HAS_TC", False):
         prec = sl7.PREC_BF16
     from paper_2302_05170_b200.dist import allreduce_stats, max_over_ranks, weak_shard
@@ -306,6 +307,7 @@ def main():
         achieved = trans_ps * rate / 1e12
         peak = n_sms * 16 * sm_max * 1e6 / 1e12
         bf16 = peaks.get("bf16_tflops", 1642.7)
+        tpk = bf16 / 2 if prec == sl7.PREC_TF32 else bf16
         mma_flops_ps = flops_ps - 2 * W.dims[1]
         tens = mma_flops_ps * rate / 1e12
         roof = {"bound": "alu", "pipe": "XU (MUFU)", "achieved": achieved, "peak": peak, "unit": "Top/s",
@@ -317,13 +319,14 @@ def main():
                 "algorithmic": "%d transcendental activations per path-step (one per hidden unit); the kernel "
                                "spends one MUFU op per tanh (MUFU.TANH, measured max error 9.9e-6 relative) and "
                                "1.5 per softplus (ex2 + lg2, half of the log1p on the FMA pipe)" % trans_ps,
-                "tensor": {"achieved": tens, "peak": bf16, "unit": "TFLOP/s", "frac": tens / bf16,
-                           "basis": "%d MMA FLOP per path-step vs MEASURED_PEAKS.json bf16_tflops (burst)" % mma_flops_ps,
+                "tensor": {"achieved": tens, "peak": tpk, "unit": "TFLOP/s", "frac": tens / tpk,
+                           "basis": "%d MMA FLOP per path-step vs MEASURED_PEAKS.json bf16_tflops (burst)%s" % (
+                               mma_flops_ps, " x 1/2 (nominal tf32:bf16 dense ratio)" if prec == sl7.PREC_TF32 else ""),
                            "issued_per_algorithmic": 6 if prec == sl7.PREC_SPLIT else 1}}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": {sl7.PREC_FP32: "f32", sl7.PREC_BF16: "bf16", sl7.PREC_SPLIT: "bf16x3"}[prec],
+            "dtype": {sl7.PREC_FP32: "f32", sl7.PREC_BF16: "bf16", sl7.PREC_TF32: "tf32", sl7.PREC_SPLIT: "bf16x3"}[prec],
             "data": "synthetic (oracle-fitted weights)",
             "config": dict(config, prec=prec_name[prec], parallelism="dp%d" % world),
             "roofline": roof, "gpu_launches": a.steps * 2 * len(N_SWEEP),

@@ -187,6 +187,7 @@ def main():
             ctx.load_weights(load_golden_blob(w.blob))
             lo, hi = (-3.0, 3.0) if w.process == "ou" else (0.0, 0.6)
             modes = [("ann_bf16_tcgen05", ctx, sl7.COLLOC_ANN, sl7.PREC_BF16, 0, w.theta, N),
+                     ("ann_tf32_tcgen05", ctx, sl7.COLLOC_ANN, sl7.PREC_TF32, 0, w.theta, N),
                      ("ann_split_bf16x3_tcgen05", ctx, sl7.COLLOC_ANN, sl7.PREC_SPLIT, 0, w.theta, N),
                      ("ann_fp32", ctx, sl7.COLLOC_ANN, sl7.PREC_FP32, 0, w.theta, N // 10),
                      ("cdc_ann_fp32_table", ctx, sl7.COLLOC_ANN, sl7.PREC_FP32, -1, w.theta, N)]
@@ -216,7 +217,7 @@ def main():
                         "unit": UNIT, "ms_per_launch": ms, "paths": n_paths, "n_steps": w.n_steps, "m": w.m,
                         "terminal": {k: s[k] for k in ("mean", "var", "skew", "exkurt", "strong_err")},
                         "quantiles_1_50_99": s["quantiles"], "clocks": clk.summary()}
-                if colloc == sl7.COLLOC_ANN and prec == sl7.PREC_BF16:
+                if colloc == sl7.COLLOC_ANN and prec in (sl7.PREC_BF16, sl7.PREC_TF32):
                     trans = sum(w.dims[1:-1])
                     ach = trans * rate / 1e12
                     pk = n_sms * 16 * sm_max * 1e6 / 1e12

@@ -72,7 +72,8 @@ typedef enum { SL7_OUT_FULL = 0, SL7_OUT_TERMINAL = 1, SL7_OUT_STATS = 2 } sl7_o
  *  FP32:  CUDA-core fp32 FFMA, accurate activations ("exact mode").
  *  BF16:  tcgen05 tensor cores, operands rounded to bf16 (RNE), fp32 accumulate, fp32 bias and
  *         activations; reproduces the quantisation-aware oracle O6.
- *  TF32:  tcgen05 kind::tf32, operands rounded with cvt.rna (reserved; SL7_EUNSUPPORTED here).
+ *  TF32:  tcgen05 kind::tf32 (K = 8 per instruction), operands rounded with cvt.rna (ties away, 11
+ *         significant bits), fp32 accumulate; reproduces O6 with TF32 rounding.
  *  SPLIT: tcgen05 with every operand split into three bf16 parts (a = a0 + a1 + a2, same for W) and
  *         the six partial products of size >= 2^-16 accumulated in fp32: fp32-class results (checked
  *         against the plain float64 oracle at the fp32 tolerance) at tensor-core speed.
@@ -104,7 +105,8 @@ typedef enum { SL7_REF_NONE = 0, SL7_REF_GBM = 1, SL7_REF_OU = 2 } sl7_ref;
  * levels Phi(x_k) (plotting position (k - 0.5)/M, linear interpolation; exact order statistics by radix
  * select on the device), and each path's conditional points are the Lagrange interpolant of the table
  * rows on the z_k at its own state; repeated z_k (step 0) use the nearest row.  The marginal points
- * couple the paths, so a CDC call must hold the whole path set (no sharding; opts->ref must be NONE). */
+ * couple the paths, so one sl7_simulate CDC call holds the whole path set (opts->ref must be NONE); runs
+ * sharded over ranks use the sl7_cdc_* calls below. */
 typedef enum { SL7_SCHEME_7L = 0, SL7_SCHEME_CDC = 1 } sl7_scheme;
 
 typedef struct {

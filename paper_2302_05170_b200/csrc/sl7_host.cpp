@@ -46,6 +46,7 @@ struct sl7_ctx_s {
   float* d_wf32 = nullptr;
   void* d_wtc = nullptr;   // bf16 SWIZZLE_128B operand image for the tcgen05 kernel
   void* d_wtc_split = nullptr;   // the same with W split into three bf16 parts (SL7_PREC_SPLIT)
+  void* d_wtc_tf32 = nullptr;    // tf32 operand image (SL7_PREC_TF32)
   TcParams tcp;            // biases + image pointer for the tcgen05 kernel
   int num_sms = 148;
   // host-mode staging
@@ -305,8 +306,49 @@ sl7_status build_tc_image(sl7_ctx c) {
     e = cudaMemcpy(d, img.data(), img.size() * 2, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemcpy(tc weights)");
   }
+  // SL7_PREC_TF32 image: each tile = two SWIZZLE_128B K-blocks [N rows][128 B = 32 tf32] (K 0..31, 32..63),
+  // values rounded with cvt.rna semantics (ties away from zero), the width-50 bias as three tf32 terms
+  {
+    auto rna = [](float v) {
+      uint32_t u;
+      std::memcpy(&u, &v, 4);
+      u = (u + 0x1000u) & 0xFFFFE000u;
+      float f;
+      std::memcpy(&f, &u, 4);
+      return f;
+    };
+    const size_t tile_b = 2 * (size_t)kTcTileBytes, out_b = 2 * (size_t)kTcOutBytes;
+    std::vector<float> img((nL * tile_b + out_b) / 4, 0.0f);
+    auto put = [&](size_t off, int nrows, int n, int k, float v) {
+      const size_t byte = off + (size_t)(k >> 5) * nrows * 128 + (size_t)n * 128 +
+                          (size_t)(((((k & 31) * 4) >> 4) ^ (n & 7)) << 4) + (size_t)(((k & 31) * 4) & 15);
+      img[byte / 4] = v;
+    };
+    for (int l = 1; l <= L; ++l) {
+      const int fi = c->dims[l], fo = c->dims[l + 1];
+      const int nrows = (l < L) ? kTcN : kTcNOut;
+      const size_t base = (l < L) ? (size_t)(l - 1) * tile_b : (size_t)nL * tile_b;
+      for (int n = 0; n < fo; ++n)
+        for (int k = 0; k < fi; ++k) put(base, nrows, n, k, rna(c->W[l][(size_t)n * fi + k]));
+      if (c->width == 50)
+        for (int n = 0; n < fo; ++n) {
+          const float b = c->b[l][n];
+          const float hi = rna(b), mid = rna(b - hi), lo = rna(b - hi - mid);
+          put(base, nrows, n, 50, hi);
+          put(base, nrows, n, 51, mid);
+          put(base, nrows, n, 52, lo);
+        }
+    }
+    if (c->d_wtc_tf32) cudaFree(c->d_wtc_tf32);
+    c->d_wtc_tf32 = nullptr;
+    cudaError_t e = cudaMalloc(&c->d_wtc_tf32, img.size() * 4);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaMalloc(tf32 weights)");
+    e = cudaMemcpy(c->d_wtc_tf32, img.data(), img.size() * 4, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemcpy(tf32 weights)");
+  }
   c->tcp.wimg = c->d_wtc;
   c->tcp.wimg_split = c->d_wtc_split;
+  c->tcp.wimg_tf32 = c->d_wtc_tf32;
   return SL7_OK;
 }
 
@@ -457,8 +499,8 @@ sl7_status prepare(sl7_ctx c, double Y0, double dt, int32_t n_steps, const doubl
       if (!c->has_net) return fail(c, SL7_ESTATE, "ANN mode before sl7_load_weights");
       const int d_in = c->dims[0];
       if (n_theta != d_in - 2) return fail(c, SL7_EINVAL, "n_theta must equal layer_dims[0] - 2");
-      if (o->prec != SL7_PREC_FP32 && o->prec != SL7_PREC_BF16 && o->prec != SL7_PREC_SPLIT)
-        return fail(c, SL7_EUNSUPPORTED, "precision mode %d not available in this build", (int)o->prec);
+      if (o->prec != SL7_PREC_FP32 && o->prec != SL7_PREC_BF16 && o->prec != SL7_PREC_SPLIT && o->prec != SL7_PREC_TF32)
+        return fail(c, SL7_EINVAL, "prec");
       const int H1 = c->dims[1];
       // features f = (Y, dt, theta...); normalised f' = (f - in_shift) / in_scale
       std::vector<double> f(d_in), sh(d_in, 0.0), sc(d_in, 1.0);
@@ -592,14 +634,15 @@ sl7_status run(sl7_ctx c, RunParams& p, const sl7_run_opts* o, float* d_out, dou
     CdcLevels lv;
     for (int k = 0; k < kMaxM; ++k) lv.p[k] = (k < c->m) ? 0.5 * std::erfc(-c->x[k] / std::sqrt(2.0)) : 0.0;
     e = launch_cdc(p, lv, c->d_cdc, rows.data(), (int)rows.size(), o->stream, c->num_sms);
-  } else if (p.colloc == kAnn && (o->prec == SL7_PREC_BF16 || o->prec == SL7_PREC_SPLIT)) {
+  } else if (p.colloc == kAnn && (o->prec == SL7_PREC_BF16 || o->prec == SL7_PREC_SPLIT || o->prec == SL7_PREC_TF32)) {
     // per-run part of the TC parameters: layer 1 folded (as in RunParams) and pre-scaled in double
     TcParams t = c->tcp;
     const char* v = std::getenv("SL7_TC_VARIANT");
     t.variant = v ? std::atoi(v) : 0;
     t.split = (o->prec == SL7_PREC_SPLIT) ? 1 : 0;
+    t.tf32 = (o->prec == SL7_PREC_TF32) ? 1 : 0;
     // tanh on MUFU.TANH by default (variants 1..9 select the older ex2 + rcp epilogues for A/B timing)
-    t.tanh_mufu = (c->act == SL7_ACT_TANH && !t.split && (t.variant == 0 || t.variant >= 20)) ? 1 : 0;
+    t.tanh_mufu = (c->act == SL7_ACT_TANH && !t.split && (t.tf32 || t.variant == 0 || t.variant >= 20)) ? 1 : 0;
     const double sc = (c->act == SL7_ACT_TANH && !t.tanh_mufu) ? 2.0 / std::log(2.0) : 1.0;
     t.act_scale = (float)sc;
     for (int k = 0; k < kTcN; ++k) {
@@ -1059,6 +1102,7 @@ void sl7_destroy(sl7_ctx c) {
     if (c->d_wf32) cudaFree(c->d_wf32);
     if (c->d_wtc) cudaFree(c->d_wtc);
     if (c->d_wtc_split) cudaFree(c->d_wtc_split);
+    if (c->d_wtc_tf32) cudaFree(c->d_wtc_tf32);
     if (c->d_cdc) cudaFree(c->d_cdc);
     if (c->d_state) cudaFree(c->d_state);
     if (c->d_out_scratch) cudaFree(c->d_out_scratch);

@@ -106,10 +106,12 @@ struct TcParams {
   float bout[kTcNOut];
   const void* wimg;
   const void* wimg_split;   // SL7_PREC_SPLIT: per tile the three bf16 parts W = W0 + W1 + W2 in turn
+  const void* wimg_tf32;    // SL7_PREC_TF32: tf32 (cvt.rna) tiles, two SWIZZLE_128B K-blocks [N][128 B] each
   int n_mma_hidden;   // L - 1
   int variant;        // activation variant (experiment hook, SL7_TC_VARIANT)
   int split;          // 1: SL7_PREC_SPLIT
   int tanh_mufu;      // tanh on MUFU.TANH (argument unscaled: act_scale = 1)
+  int tf32;           // 1: SL7_PREC_TF32
 };
 
 // 7L-CDC: quantile levels Phi(x_k) of the marginal collocation points (host, double).

@@ -180,6 +180,44 @@ __device__ __forceinline__ void act_pack_32(const uint32_t (&v)[32], int col0, f
   }
 }
 
+// SL7_PREC_TF32: activations rounded to tf32 with cvt.rna (ties away, reading A-15), one 32-bit TMEM
+// column per unit (the A operand of kind::tf32 is K-major fp32-width).
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+template <int ACT, int H, unsigned NMASK, bool FOLD>
+__device__ __forceinline__ void act_tf32_32(const uint32_t (&v)[32], int col0, float scale, const float* bs,
+                                            uint32_t (&w)[32]) {
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const int c = col0 + k;
+    float h;
+    if (c < H) {
+      const float acc = __uint_as_float(v[k]);
+      const float u = FOLD ? ((ACT == kActTanhX || ACT == kActSoftplusX) ? acc : acc * scale) : fmaf(acc, scale, bs[c]);
+      h = tc_act_u<ACT>(u, use_newton<ACT, NMASK>(c));
+    } else {
+      h = (FOLD && c < H + 3) ? 1.0f : 0.0f;
+    }
+    w[k] = tf32_rna(h);
+  }
+}
+
+// kind::tf32 MMA issue for one layer: K = 64 as 8 instructions of K = 8 (32 bytes of each K-major row).
+// The weight tile is two SWIZZLE_128B K-blocks of [N rows][128 B] (K 0..31, then K 32..63), so K-step k
+// reads block k / 4 at byte offset 32 (k % 4); the A operand advances 8 TMEM columns per K-step.
+__device__ __forceinline__ void issue_layer_tf32(uint32_t acc_t, uint32_t a_t, uint32_t b_base, uint32_t n_rows,
+                                                 uint32_t idesc) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint64_t bdesc = tc::smem_desc_sw128(b_base + (uint32_t)(k >> 2) * n_rows * 128u) + 2u * (uint32_t)(k & 3);
+    tc::mma_tf32_ts(acc_t, a_t + 8u * k, bdesc, idesc, k > 0 ? 1u : 0u);
+  }
+}
+
 // MMA issue for one layer: sum over (A part, B part) pairs of [128 x 64] x [64 x N] with K = 4 x 16.
 // NP = 1: bf16 x bf16.  NP = 3: the six pairs whose products are >= 2^-16 of the leading one
 // (hh, hm, mh, hl, lh, mm): fp32-class products from bf16 tensor cores.
@@ -199,7 +237,7 @@ __device__ __forceinline__ void issue_layer(uint32_t acc_t, uint32_t a_t, uint32
   }
 }
 
-template <int NG, int H, int MR, bool RT_M, int ACT, unsigned NMASK, int NP = 1, bool SKIPMMA = false>
+template <int NG, int H, int MR, bool RT_M, int ACT, unsigned NMASK, int NP = 1, bool SKIPMMA = false, bool TF32 = false>
 __global__ void __launch_bounds__(NG * kGroupThreads, 1)
     ann_tc_step_kernel(const __grid_constant__ RunParams p, const __grid_constant__ TcParams t) {
   extern __shared__ uint8_t smem_raw[];
@@ -211,7 +249,10 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
   const int g = warp >> 2;                 // tile group
   const int wq = warp & 3;                 // warp within the group -> TMEM lanes [32 wq, 32 wq + 32)
   const int tid_g = threadIdx.x & (kGroupThreads - 1);
-  constexpr uint32_t kCols = kAccCol + 64u + 32u * NP;     // acc fp32 [0,64) + NP bf16 A parts
+  static_assert(!TF32 || NP == 1, "TF32 has one operand part");
+  constexpr uint32_t kCols = kAccCol + 64u + (TF32 ? 64u : 32u * NP);   // acc fp32 [0,64) + A (NP bf16 parts | tf32)
+  constexpr uint32_t kTileB = TF32 ? 2u * kTcTileBytes : (uint32_t)kTcTileBytes;   // bytes per weight tile part
+  constexpr uint32_t kOutB = TF32 ? 2u * kTcOutBytes : (uint32_t)kTcOutBytes;
   constexpr uint32_t kTmemCols = NG * kCols <= 256 ? 256u : 512u;
   static_assert(NG * kCols <= 512, "TMEM: 512 columns per SM");
   constexpr bool FOLD = (H <= kTcN - 3);   // biases ride in spare K columns (host image must match)
@@ -220,7 +261,7 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
   const uint32_t sbase = (tc::smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* wsm = smem_raw + (sbase - tc::smem_u32(smem_raw));
   const int nL = t.n_mma_hidden;
-  const int wbytes = NP * (nL * kTcTileBytes + kTcOutBytes);
+  const int wbytes = NP * (nL * (int)kTileB + (int)kOutB);
   uint32_t* hist = reinterpret_cast<uint32_t*>(wsm + wbytes);
   // per-thread running sums of the statistics live in shared memory ([8][threads], SoA), not in registers:
   // they change once per tile, and the 12 registers they would pin are worth more to the epilogue
@@ -230,7 +271,7 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
   if (p.has_stats)
     for (int k = 0; k < 8; ++k) sst[k * kThreads + threadIdx.x] = 0.0;
   {
-    const uint4* src = reinterpret_cast<const uint4*>(NP == 1 ? t.wimg : t.wimg_split);
+    const uint4* src = reinterpret_cast<const uint4*>(TF32 ? t.wimg_tf32 : (NP == 1 ? t.wimg : t.wimg_split));
     uint4* dst = reinterpret_cast<uint4*>(wsm);
     for (int i = threadIdx.x; i < wbytes / 16; i += blockDim.x) dst[i] = src[i];
   }
@@ -249,8 +290,8 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
   const uint32_t gcol = tbase + (uint32_t)g * kCols;
   const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
   const uint32_t acc_t = gcol + kAccCol, a_t = gcol + kACol;
-  constexpr uint32_t idesc_h = tc::idesc_bf16_f32(128, kTcN);
-  constexpr uint32_t idesc_o = tc::idesc_bf16_f32(128, kTcNOut);
+  constexpr uint32_t idesc_h = TF32 ? tc::idesc_tf32_f32(128, kTcN) : tc::idesc_bf16_f32(128, kTcN);
+  constexpr uint32_t idesc_o = TF32 ? tc::idesc_tf32_f32(128, kTcNOut) : tc::idesc_bf16_f32(128, kTcNOut);
   uint64_t* bar = &mbar[g];
   uint32_t phase = 0;
 
@@ -272,21 +313,32 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
       // ---- layer 1 (fp32, rank 1 in Y) -> A operand in TMEM, two 32-unit halves
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
-        uint32_t pk[NP][16];
+        if constexpr (TF32) {
+          uint32_t w[32];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          float h[2];
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int c = 32 * half + 2 * k + q;
-            h[q] = (c < H) ? tc_act_u<ACT>(fmaf(Y, t.l1w[c], t.l1b[c]), use_newton<ACT, NMASK>(c))
-                           : ((FOLD && c < H + 3) ? 1.0f : 0.0f);
+          for (int k = 0; k < 32; ++k) {
+            const int c = 32 * half + k;
+            w[k] = tf32_rna((c < H) ? tc_act_u<ACT>(fmaf(Y, t.l1w[c], t.l1b[c]), use_newton<ACT, NMASK>(c))
+                                    : ((FOLD && c < H + 3) ? 1.0f : 0.0f));
           }
-          split_pack<NP>(h[0], h[1], pk, k);
-        }
+          tc::tmem_st_32x32b_x32(a_t + lane_off + 32u * half, w);
+        } else {
+          uint32_t pk[NP][16];
 #pragma unroll
-        for (int part = 0; part < NP; ++part)
-          tc::tmem_st_32x32b_x16(a_t + 32u * part + lane_off + 16u * half, pk[part]);
+          for (int k = 0; k < 16; ++k) {
+            float h[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int c = 32 * half + 2 * k + q;
+              h[q] = (c < H) ? tc_act_u<ACT>(fmaf(Y, t.l1w[c], t.l1b[c]), use_newton<ACT, NMASK>(c))
+                             : ((FOLD && c < H + 3) ? 1.0f : 0.0f);
+            }
+            split_pack<NP>(h[0], h[1], pk, k);
+          }
+#pragma unroll
+          for (int part = 0; part < NP; ++part)
+            tc::tmem_st_32x32b_x16(a_t + 32u * part + lane_off + 16u * half, pk[part]);
+        }
       }
       tc::wait_st();
       // ---- layers 2..L+1 on the tensor cores; the Lagrange basis at Z (independent of the MLP)
@@ -303,6 +355,9 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
           // epilogue of columns 0..31 with the MMAs of 32..63, measured slower: 1.38e10 vs 1.41e10.)
           if (SKIPMMA) {
             // timing experiment only (SL7_TC_VARIANT=9): same synchronisation, no tensor work
+          } else if (TF32) {
+            if (last) issue_layer_tf32(acc_t, a_t, sbase + (uint32_t)(nL * kTileB), kTcNOut, idesc_o);
+            else issue_layer_tf32(acc_t, a_t, sbase + (uint32_t)(l * kTileB), kTcN, idesc_h);
           } else if (last) {
             issue_layer<NP>(acc_t, a_t, sbase + (uint32_t)(NP * nL * kTcTileBytes), kTcOutBytes, idesc_o);
           } else {
@@ -317,14 +372,20 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
         if (!last) {
 #pragma unroll
           for (int half = 0; half < 2; ++half) {
-            uint32_t pk[NP][16];
             uint32_t v[32];
             tc::tmem_ld_32x32b_x32(acc_t + lane_off + 32u * half, v);
             tc::wait_ld();
-            act_pack_32<ACT, H, NMASK, FOLD, NP>(v, 32 * half, t.act_scale, t.bias[l], pk);
+            if constexpr (TF32) {
+              uint32_t w[32];
+              act_tf32_32<ACT, H, NMASK, FOLD>(v, 32 * half, t.act_scale, t.bias[l], w);
+              tc::tmem_st_32x32b_x32(a_t + lane_off + 32u * half, w);
+            } else {
+              uint32_t pk[NP][16];
+              act_pack_32<ACT, H, NMASK, FOLD, NP>(v, 32 * half, t.act_scale, t.bias[l], pk);
 #pragma unroll
-            for (int part = 0; part < NP; ++part)
-              tc::tmem_st_32x32b_x16(a_t + 32u * part + lane_off + 16u * half, pk[part]);
+              for (int part = 0; part < NP; ++part)
+                tc::tmem_st_32x32b_x16(a_t + 32u * part + lane_off + 16u * half, pk[part]);
+            }
           }
           tc::wait_st();
         } else {
@@ -371,12 +432,13 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
 
 namespace {
 
-template <int NG, int H, int MR, bool RT, int ACT, unsigned NMASK = 0u, int NP = 1, bool SKIP = false>
+template <int NG, int H, int MR, bool RT, int ACT, unsigned NMASK = 0u, int NP = 1, bool SKIP = false, bool TF32 = false>
 cudaError_t launch_tc_t(const RunParams& p, const TcParams& t, cudaStream_t st, int num_sms) {
-  auto kernel = ann_tc_step_kernel<NG, H, MR, RT, ACT, NMASK, NP, SKIP>;
+  auto kernel = ann_tc_step_kernel<NG, H, MR, RT, ACT, NMASK, NP, SKIP, TF32>;
   const size_t hist = (p.has_stats && p.n_bins > 0) ? sizeof(uint32_t) * (size_t)((p.n_bins + 2 + 1) & ~1) : 0;
   const size_t sst = p.has_stats ? sizeof(double) * 8 * NG * kGroupThreads : 0;
-  const size_t smem = 1024 + (size_t)NP * ((size_t)t.n_mma_hidden * kTcTileBytes + kTcOutBytes) + hist + sst;
+  const size_t tile_b = TF32 ? 2 * kTcTileBytes : kTcTileBytes, out_b = TF32 ? 2 * kTcOutBytes : kTcOutBytes;
+  const size_t smem = 1024 + (size_t)NP * ((size_t)t.n_mma_hidden * tile_b + out_b) + hist + sst;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const uint64_t tiles = (p.n_paths + kGroupThreads - 1) / kGroupThreads;
@@ -443,8 +505,22 @@ cudaError_t launch_tc_act_x(const RunParams& p, const TcParams& t, cudaStream_t 
 
 }  // namespace
 
+// SL7_PREC_TF32: TMEM 64 + 64 columns per group -> 4 groups (512 columns)
+constexpr int kTcGroupsTf32 = 4;
+
+template <int ACT, unsigned NM>
+cudaError_t launch_tc_tf32(const RunParams& p, const TcParams& t, cudaStream_t st, int num_sms) {
+  constexpr int NG = kTcGroupsTf32;
+  if (p.width == 50 && p.m == 5) return launch_tc_t<NG, 50, 5, false, ACT, NM, 1, false, true>(p, t, st, num_sms);
+  if (p.width == 50 && p.m == 7) return launch_tc_t<NG, 50, 7, false, ACT, NM, 1, false, true>(p, t, st, num_sms);
+  return launch_tc_t<NG, 64, kMaxM, true, ACT, NM, 1, false, true>(p, t, st, num_sms);
+}
+
 int launch_tc_kernel(const RunParams& p, const TcParams& t, void* stream, int num_sms) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (t.tf32)
+    return (int)(p.act == SL7_ACT_TANH ? launch_tc_tf32<kActTanhX, 0x00u>(p, t, st, num_sms)
+                                       : launch_tc_tf32<SL7_ACT_SOFTPLUS, kSoftplusPolyMask>(p, t, st, num_sms));
   if (p.act == SL7_ACT_SOFTPLUS && !t.split && t.variant >= 30 && p.width == 50 && p.m == 7) {
     switch (t.variant) {   // A/B hooks: one-MUFU softplus, group count, FMA-pipe share
       case 30: return (int)launch_tc_t<5, 50, 7, false, kActSoftplusX, 0x00u>(p, t, st, num_sms);

@@ -42,13 +42,13 @@ def test_validation_errors(gpu_lib):
         ctx.simulate(1.0, 0.5, 2, (), 10, 1, sl7.OUT_TERMINAL, sl7.make_opts(colloc=sl7.COLLOC_ANN), out=out)
 
 
-@pytest.mark.parametrize("prec", ["fp32", "bf16", "split"])
+@pytest.mark.parametrize("prec", ["fp32", "bf16", "tf32", "split"])
 def test_chunked_accumulate_equals_single_run(gpu_lib, prec):
     """Checkpoint/resume semantics: the counter-based RNG makes any path range recomputable, and
     opts.accumulate sums chunk statistics into one vector."""
     sl7 = gpu_lib
     torch = _torch()
-    p = {"fp32": sl7.PREC_FP32, "bf16": sl7.PREC_BF16, "split": sl7.PREC_SPLIT}[prec]
+    p = {"fp32": sl7.PREC_FP32, "bf16": sl7.PREC_BF16, "tf32": sl7.PREC_TF32, "split": sl7.PREC_SPLIT}[prec]
     w = workloads()["cfg2_ou"]
     ctx = sl7.Context(w.m, list(w.dims), w.act)
     ctx.load_weights(load_golden_blob(w.blob))
@@ -83,7 +83,7 @@ def test_host_entry_stats_only(gpu_lib):
     assert s["strong_err"] < 1e-6      # exact OU collocation = Eq. 6.6 on the same normals
 
 
-@pytest.mark.parametrize("kind", ["exact", "fp32", "bf16", "split", "cdc"])
+@pytest.mark.parametrize("kind", ["exact", "fp32", "bf16", "tf32", "split", "cdc"])
 def test_single_path_and_single_step(gpu_lib, kind):
     sl7 = gpu_lib
     torch = _torch()
@@ -95,7 +95,8 @@ def test_single_path_and_single_step(gpu_lib, kind):
         ctx = sl7.Context(w.m, list(w.dims), w.act)
         ctx.load_weights(blob)
         colloc, theta = sl7.COLLOC_ANN, ()
-        prec = {"fp32": sl7.PREC_FP32, "bf16": sl7.PREC_BF16, "split": sl7.PREC_SPLIT, "cdc": sl7.PREC_FP32}[kind]
+        prec = {"fp32": sl7.PREC_FP32, "bf16": sl7.PREC_BF16, "tf32": sl7.PREC_TF32, "split": sl7.PREC_SPLIT,
+                "cdc": sl7.PREC_FP32}[kind]
     scheme = sl7.SCHEME_CDC if kind == "cdc" else sl7.SCHEME_7L
     for n_paths, n_steps in [(1, 1), (1, 5), (129, 1)]:
         o = sl7.make_opts(prec=prec, colloc=colloc, scheme=scheme)
@@ -103,9 +104,9 @@ def test_single_path_and_single_step(gpu_lib, kind):
         torch.cuda.synchronize()
         Yd = out.double().cpu().numpy().reshape(n_steps + 1, n_paths)
         spec = O.Spec(5, "gbm" if kind == "exact" else "ann", theta, 1.0, 0.5, n_steps, net=O.parse_blob(blob),
-                      quant="bf16" if kind == "bf16" else None)
+                      quant=kind if kind in ("bf16", "tf32") else None)
         Z = O.normals(5, np.arange(n_paths, dtype=np.uint64), n_steps)
-        tol = 5e-3 if kind == "bf16" else 1e-5
+        tol = 5e-3 if kind in ("bf16", "tf32") else 1e-5
         for i in range(n_steps):
             if kind == "cdc":
                 ref, kap = O.cdc_step(spec, Yd[i], Z[i]), O.cdc_step_error_scale(spec, Yd[i], Z[i])

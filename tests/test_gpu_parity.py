@@ -319,6 +319,44 @@ def test_ann_bf16_terminal_moments(gpu_lib, name):
 
 
 @pytest.mark.parametrize("name,gen", ANN_CASES, ids=[c[0] for c in ANN_CASES])
+def test_ann_tf32_tc_teacher_forced(gpu_lib, name, gen):
+    """T-3 for SL7_PREC_TF32 (tcgen05 kind::tf32): within 5e-3 * kappa of O6 with TF32 (cvt.rna) rounding."""
+    sl7 = gpu_lib
+    blob, m, dims, act, theta, y0, n_steps, dt = _ann_case(name, gen)
+    n_paths = 4 * 128 * 3 + 51
+    ctx = sl7.Context(m, dims, act)
+    ctx.load_weights(blob)
+    Yd, _ = _run(sl7, ctx, dict(y0=y0, dt=dt, n_steps=n_steps), n_paths, 57, sl7.OUT_FULL, sl7.COLLOC_ANN,
+                 prec=sl7.PREC_TF32, theta=theta)
+    Yd = Yd.reshape(n_steps + 1, n_paths)
+    spec = O.Spec(m, "ann", theta, y0, dt, n_steps, net=O.parse_blob(blob), quant="tf32")
+    Z = O.normals(57, np.arange(n_paths, dtype=np.uint64), n_steps)
+    worst = _teacher_forced(spec, Yd, Z, tol=5e-3)
+    print("tf32 teacher-forced worst |err|/kappa = %.3g" % worst)
+
+
+@pytest.mark.parametrize("name", ["cfg0", "cfg2_ou"])
+def test_ann_tf32_terminal_moments(gpu_lib, name):
+    """T-4 for SL7_PREC_TF32 against O6 (tf32) on the identical path set."""
+    sl7 = gpu_lib
+    blob, m, dims, act, theta, y0, n_steps, dt = _ann_case(name, None)
+    w = workloads()[name]
+    n_steps, dt = w.n_steps, w.dt
+    n_paths = 20_000
+    ctx = sl7.Context(m, dims, act)
+    ctx.load_weights(blob)
+    YT, _ = _run(sl7, ctx, dict(y0=y0, dt=dt, n_steps=n_steps), n_paths, w.seed, sl7.OUT_TERMINAL, sl7.COLLOC_ANN,
+                 prec=sl7.PREC_TF32, theta=theta)
+    spec = O.Spec(m, "ann", theta, y0, dt, n_steps, net=O.parse_blob(blob), quant="tf32")
+    Yo, _ = O.simulate(spec, w.seed, np.arange(n_paths, dtype=np.uint64))
+    mo, md = Yo[-1].mean(), YT.mean()
+    vo, vd = Yo[-1].var(), YT.var()
+    sd = np.sqrt(vo)
+    assert abs(md - mo) <= 1e-4 * max(abs(mo), sd if abs(mo) < 1e-3 * sd else abs(mo))
+    assert abs(vd - vo) <= 1e-4 * vo
+
+
+@pytest.mark.parametrize("name,gen", ANN_CASES, ids=[c[0] for c in ANN_CASES])
 def test_ann_split_tc_teacher_forced(gpu_lib, name, gen):
     """SL7_PREC_SPLIT: bf16 tensor cores with three-part operands reach the fp32 bar (T-2, 1e-5 kappa)
     against the plain float64 oracle O3."""
