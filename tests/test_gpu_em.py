@@ -209,3 +209,24 @@ def test_em_and_training_validation(gpu_lib):
         ctx.training_set(sl7.MODEL_OU, bad, 100, 0.1, 1, sl7.make_opts())
     with pytest.raises(sl7.Sl7Error, match="theta"):
         ctx.training_set(sl7.MODEL_GBM, np.array([[1.0, 0.5, 0.1, -0.2]]), 100, 0.1, 1, sl7.make_opts())
+
+
+def test_training_set_chunked_scratch_equals_caller_buffer(gpu_lib):
+    """Without d_terminal the library processes the rows in chunks of its 1 GiB scratch
+    (2^28 / M rows): with M = 2^20 that is 256 rows, so 300 rows take two chunks.  The labels must equal
+    those of the single-chunk run into a caller buffer, row for row."""
+    sl7 = gpu_lib
+    torch = _torch()
+    M, R = 1 << 20, 300
+    F = sample_features("ou", R, seed=12, dt_range=(0.01, 0.02))      # dtau = 0.05 -> K = 1
+    ctx = sl7.Context(5)
+    term = torch.empty((R, M), dtype=torch.float32, device="cuda")
+    _, a = ctx.training_set(sl7.MODEL_OU, F, M, 0.05, 3, sl7.make_opts(flags=sl7.FLAG_FAST_NORMALS), terminal=term)
+    _, b = ctx.training_set(sl7.MODEL_OU, F, M, 0.05, 3, sl7.make_opts(flags=sl7.FLAG_FAST_NORMALS))
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    for r in (0, 255, 256, 299):                                          # both sides of the chunk boundary
+        T = term[r].double().cpu().numpy()
+        lv = O.normal_cdf(O.gauss_hermite_nodes(5))
+        Q = O.quantiles(T, lv)
+        np.testing.assert_allclose(a[r].cpu().numpy(), Q, rtol=1e-12, atol=1e-12)
