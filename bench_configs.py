@@ -11,6 +11,9 @@ cfg2: OU (Ybar=0, lam=1, sigma=0.5, Y0=1) and CIR (kappa=1, Ybar=0.1, sigma=0.3,
 em:   Euler-Maruyama comparator on cfg2's OU and CIR, 16 large steps of 0.125 with
       K = 1, 8, 125 sub-steps (dtau = 1e-3 at K = 125), STATS + strong error vs the exact OU solution on
       the same fine normals; the 7L lines of cfg2 give the contrast.  Unit: fine path-steps/s.
+cfg4: CIR as cfg2, T=4, 32 steps, 4e9 paths in ONE call on one GPU (64-bit path ids past 2^32), STATS;
+      ANN-BF16 (tcgen05) and 7L-CDC.  (The scaling runs of BASELINE configs[4] shard these paths over ranks
+      with path_offset; only one GPU is available to this harness.)
 train: training-set generation (§8(f) row 2): 4096 OU feature rows over SPEC.md:180's ranges
       (dt in [0.05, 2]), M = 1e5 inner paths, dtau = 1e-3 (K_r = ceil(dt/dtau) <= 2000), labels at m = 7.
 cfg3: GBM, T=1, 64 steps, m=5, 2e8 paths, FULL step-major path tensor (65 x 2e8 fp32 = 52 GB in HBM).
@@ -52,11 +55,12 @@ def timed_launches(fn, steps, warmup, flush, stream):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--config", default="all", choices=["cfg2", "cfg3", "em", "train", "all"])
+    ap.add_argument("--config", default="all", choices=["cfg2", "cfg3", "cfg4", "em", "train", "all"])
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--cfg3-paths", type=int, default=200_000_000)
     ap.add_argument("--cfg2-paths", type=int, default=100_000_000)
+    ap.add_argument("--cfg4-paths", type=int, default=4_000_000_000)
     ap.add_argument("--train-rows", type=int, default=4096)
     ap.add_argument("--train-inner", type=int, default=100_000)
     a = ap.parse_args()
@@ -176,6 +180,36 @@ def main():
                 line["roofline"] = {"bound": "alu", "pipe": "issue", "achieved": ach / 1e12, "peak": issue_peak / 1e12,
                                     "unit": "T thread-instr/s", "frac": ach / issue_peak,
                                     "algorithmic": "%.0f instructions per fine path-step" % em_instr}
+            emit(line)
+
+    if a.config in ("cfg4", "all"):
+        w = Wl["cfg4"]
+        N = a.cfg4_paths
+        stats = torch.zeros(sl7.stats_elems(4096), dtype=torch.float64, device=dev)
+        ctx = sl7.Context(w.m, list(w.dims), w.act, device=0)
+        ctx.load_weights(load_golden_blob(w.blob))
+        for label, prec, scheme, n_paths in [("ann_bf16_tcgen05", sl7.PREC_BF16, sl7.SCHEME_7L, N),
+                                             ("cdc_ann_fp32_table", sl7.PREC_FP32, sl7.SCHEME_CDC, N // 10)]:
+            opts = sl7.make_opts(prec=prec, colloc=sl7.COLLOC_ANN, stream=stream, n_bins=4096, hist_lo=0.0, hist_hi=0.6,
+                                 shift=w.y0, scheme=scheme)
+            fn = (lambda opts=opts, n_paths=n_paths:
+                  ctx.simulate(w.y0, w.dt, w.n_steps, w.theta, n_paths, w.seed, sl7.OUT_STATS, opts, stats=stats))
+            clk = ClockSampler(0)
+            clk.start()
+            ms, ms_min = timed_launches(fn, max(1, a.steps - 1), 1, flush, stream)
+            clk.stop()
+            s = sl7.stats_summary(stats.cpu().numpy(), opts, q_levels=[0.01, 0.5, 0.99])
+            rate = n_paths * w.n_steps / (ms * 1e-3)
+            line = {"config": "cfg4", "mode": label, "metric": "7L path-steps/sec (device-timed)", "value": rate,
+                    "unit": UNIT, "ms_per_launch": ms, "paths": n_paths, "n_steps": w.n_steps, "m": w.m,
+                    "terminal": {k: s[k] for k in ("mean", "var", "skew", "exkurt")}, "n_counted": s["n"],
+                    "quantiles_1_50_99": s["quantiles"], "clocks": clk.summary()}
+            if prec == sl7.PREC_BF16:
+                trans = sum(w.dims[1:-1])
+                ach = trans * rate / 1e12
+                pk = n_sms * 16 * sm_max * 1e6 / 1e12
+                line["roofline"] = {"bound": "alu", "pipe": "XU (MUFU)", "achieved": ach, "peak": pk, "unit": "Top/s",
+                                    "frac": ach / pk, "algorithmic": "%d softplus activations per path-step" % trans}
             emit(line)
 
     if a.config in ("cfg2", "all"):
