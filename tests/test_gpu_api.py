@@ -113,3 +113,37 @@ def test_single_path_and_single_step(gpu_lib, kind):
             else:
                 ref, kap = O.step(spec, Yd[i], Z[i]), O.step_error_scale(spec, Yd[i], Z[i])
             assert np.all(np.abs(Yd[i + 1] - ref) <= tol * kap), (kind, n_paths, n_steps, i)
+
+
+@pytest.mark.parametrize("kind", ["exact", "fp32", "bf16", "tf32", "split", "cdc", "em"])
+def test_max_histogram_bins(gpu_lib, kind):
+    """The largest histogram (16384 bins, 64 KB of shared memory next to the weight tiles and, in the
+    tensor-core kernels, the per-thread statistics) on the deepest network (cfg2, 4 hidden layers): the
+    fused histogram equals numpy's histogram of the same run's terminal values, count for count."""
+    sl7 = gpu_lib
+    torch = _torch()
+    w = workloads()["cfg2_ou"]
+    nb, lo, hi, N = 16384, -3.0, 3.0, 50_000
+    st = torch.zeros(sl7.stats_elems(nb), dtype=torch.float64, device="cuda")
+    kw = dict(n_bins=nb, hist_lo=lo, hist_hi=hi, shift=1.0)
+    if kind in ("exact", "em"):
+        ctx = sl7.Context(w.m)
+    else:
+        ctx = sl7.Context(w.m, list(w.dims), w.act)
+        ctx.load_weights(load_golden_blob(w.blob))
+    if kind == "em":
+        out, _ = ctx.simulate_em(sl7.MODEL_OU, w.y0, w.dt, w.n_steps, 2, w.theta, N, w.seed, sl7.OUT_TERMINAL,
+                                 sl7.make_opts(**kw), stats=st)
+    else:
+        colloc = sl7.COLLOC_EXACT_OU if kind == "exact" else sl7.COLLOC_ANN
+        prec = {"exact": sl7.PREC_FP32, "fp32": sl7.PREC_FP32, "bf16": sl7.PREC_BF16, "tf32": sl7.PREC_TF32,
+                "split": sl7.PREC_SPLIT, "cdc": sl7.PREC_FP32}[kind]
+        scheme = sl7.SCHEME_CDC if kind == "cdc" else sl7.SCHEME_7L
+        out, _ = ctx.simulate(w.y0, w.dt, w.n_steps, w.theta, N, w.seed, sl7.OUT_TERMINAL,
+                              sl7.make_opts(prec=prec, colloc=colloc, scheme=scheme, **kw), stats=st)
+    torch.cuda.synchronize()
+    v = st.cpu().numpy()
+    ref = O.stats_vector(out.double().cpu().numpy(), 1.0, lo, hi, nb)
+    assert v[0] == ref[0] == N
+    np.testing.assert_array_equal(v[8:], ref[8:])
+    np.testing.assert_allclose(v[2:6], ref[2:6], rtol=1e-10)
