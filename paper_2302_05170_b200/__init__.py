@@ -212,9 +212,10 @@ class Context:
         self.layer_dims = dims
 
     def close(self):
-        if getattr(self, "_h", None):
-            _lib.sl7_destroy(self._h)
-            self._h = None
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:      # at interpreter exit the module global may already be gone
+            _lib.sl7_destroy(h)
+        self._h = None
 
     __del__ = close
 
