@@ -1,0 +1,119 @@
+"""Parity at BASELINE.json's full sizes, in the launch configurations bench.py / bench_configs.py time:
+sampled paths (strided over the whole range, plus the first and the ragged last ones) teacher-forced
+against the float64 oracle step by step, and properties that hold at any size (fused statistics equal the
+moments / histogram of the same launch's terminal values; TERMINAL equals the last FULL row; path counts).
+"""
+import numpy as np
+import pytest
+
+from oracle import sl7_oracle as O
+from sl7_inputs import load_golden_blob, workloads
+
+pytestmark = pytest.mark.gpu
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _sample_ids(N, k=1500):
+    ids = np.unique(np.concatenate([np.arange(8), np.linspace(0, N - 1, k).astype(np.int64), np.arange(N - 8, N)]))
+    return ids.astype(np.int64)
+
+
+def _teacher_forced_sample(spec, rows, ids, seed, tol, Z=None):
+    """rows: [n+1][len(ids)] device values of the sampled paths; one oracle step per row."""
+    if Z is None:
+        Z = O.normals(seed, ids.astype(np.uint64), spec.n_steps)
+    worst = 0.0
+    for i in range(spec.n_steps):
+        ref = O.step(spec, rows[i], Z[i])
+        kap = O.step_error_scale(spec, rows[i], Z[i])
+        r = np.abs(rows[i + 1] - ref) / kap
+        worst = max(worst, float(r.max()))
+        assert r.max() <= tol, (i, float(r.max()), int(ids[np.argmax(r)]))
+    return worst
+
+
+@pytest.mark.parametrize("prec", ["bf16", "tf32"])
+def test_cfg1_full_size_sampled(gpu_lib, prec):
+    """cfg1 at 1e7 paths and n = 64 (the longest launch of bench.py's sweep), tcgen05 path."""
+    sl7 = gpu_lib
+    torch = _torch()
+    w = workloads()["cfg1"]
+    N, n = w.n_paths, 64
+    ctx = sl7.Context(w.m, list(w.dims), w.act)
+    blob = load_golden_blob(w.blob)
+    ctx.load_weights(blob)
+    p = {"bf16": sl7.PREC_BF16, "tf32": sl7.PREC_TF32}[prec]
+    full, _ = ctx.simulate(w.y0, 1.0 / n, n, (), N, w.seed, sl7.OUT_FULL, sl7.make_opts(prec=p, colloc=sl7.COLLOC_ANN))
+    nb = 4096
+    st = torch.zeros(sl7.stats_elems(nb), dtype=torch.float64, device="cuda")
+    opts = sl7.make_opts(prec=p, colloc=sl7.COLLOC_ANN, n_bins=nb, hist_lo=0.0, hist_hi=4.0, shift=1.0,
+                         ref=sl7.REF_GBM, ref_theta=w.theta)
+    term, _ = ctx.simulate(w.y0, 1.0 / n, n, (), N, w.seed, sl7.OUT_TERMINAL, opts, stats=st)
+    torch.cuda.synchronize()
+    F = full.view(n + 1, N)
+    assert torch.equal(F[n], term)                                   # TERMINAL = last FULL row, bit for bit
+    ids = _sample_ids(N)
+    rows = F[:, torch.as_tensor(ids, device="cuda")].double().cpu().numpy()
+    spec = O.Spec(w.m, "ann", (), w.y0, 1.0 / n, n, net=O.parse_blob(blob), quant=prec)
+    worst = _teacher_forced_sample(spec, rows, ids, w.seed, 5e-3)
+    print("cfg1 %s full-size sampled worst |err|/kappa = %.3g" % (prec, worst))
+    v = st.cpu().numpy()
+    T = term.double().cpu().numpy()
+    ref = O.stats_vector(T, 1.0, 0.0, 4.0, nb)
+    assert v[0] == N and v[1] == 0
+    np.testing.assert_array_equal(v[8:], ref[8:])
+    np.testing.assert_allclose(v[2:6], ref[2:6], rtol=1e-9)
+
+
+def test_cfg2_full_size_sampled(gpu_lib):
+    """cfg2 OU at 1e8 paths, 16 steps, softplus 4x50 on tcgen05 (bench_configs' bf16 line)."""
+    sl7 = gpu_lib
+    torch = _torch()
+    w = workloads()["cfg2_ou"]
+    N = w.n_paths
+    ctx = sl7.Context(w.m, list(w.dims), w.act)
+    blob = load_golden_blob(w.blob)
+    ctx.load_weights(blob)
+    opts = sl7.make_opts(prec=sl7.PREC_BF16, colloc=sl7.COLLOC_ANN)
+    full, _ = ctx.simulate(w.y0, w.dt, w.n_steps, w.theta, N, w.seed, sl7.OUT_FULL, opts)
+    torch.cuda.synchronize()
+    F = full.view(w.n_steps + 1, N)
+    ids = _sample_ids(N, 1000)
+    rows = F[:, torch.as_tensor(ids, device="cuda")].double().cpu().numpy()
+    del full, F
+    torch.cuda.empty_cache()
+    spec = O.Spec(w.m, "ann", w.theta, w.y0, w.dt, w.n_steps, net=O.parse_blob(blob), quant="bf16")
+    worst = _teacher_forced_sample(spec, rows, ids, w.seed, 5e-3)
+    print("cfg2 bf16 full-size sampled worst |err|/kappa = %.3g" % worst)
+
+
+def test_cfg3_full_size_sampled(gpu_lib):
+    """cfg3 at 2e8 paths x 65 rows (the 52 GB FULL tensor), exact GBM with fast normals + closed-form g_m,
+    as bench_configs times it; the sampled paths are driven by the device's own fast normals."""
+    sl7 = gpu_lib
+    torch = _torch()
+    w = workloads()["cfg3"]
+    N, n = w.n_paths, w.n_steps
+    ctx = sl7.Context(w.m)
+    flags = sl7.FLAG_FAST_NORMALS | sl7.FLAG_SPECIALIZED
+    full, _ = ctx.simulate(w.y0, w.dt, n, w.theta, N, w.seed, sl7.OUT_FULL,
+                           sl7.make_opts(colloc=sl7.COLLOC_EXACT_GBM, flags=flags))
+    torch.cuda.synchronize()
+    F = full.view(n + 1, N)
+    # contiguous sample blocks (sl7_normals takes a path range): start, middle, end
+    blocks = [(0, 700), (N // 2 - 350, 700), (N - 700, 700)]
+    for lo, k in blocks:
+        rows = F[:, lo:lo + k].double().cpu().numpy()
+        z = torch.empty(n * k, dtype=torch.float32, device="cuda")
+        sl7.normals(w.seed, lo, k, n, z, flags=sl7.FLAG_FAST_NORMALS)
+        torch.cuda.synchronize()
+        Z = z.double().cpu().numpy().reshape(n, k)
+        spec = O.Spec(w.m, "gbm", w.theta, w.y0, w.dt, n)
+        _teacher_forced_sample(spec, rows, np.arange(lo, lo + k), w.seed, 1e-5, Z=Z)
+    assert torch.isfinite(F[n]).all()
+    del full, F
+    torch.cuda.empty_cache()
