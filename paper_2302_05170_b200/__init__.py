@@ -130,6 +130,19 @@ def _dptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
+def _dbuf(t, dtype, n, name):
+    """Device pointer of a caller tensor after checking what the C ABI cannot: a contiguous CUDA tensor of
+    the expected dtype holding at least n elements (the library writes n of them)."""
+    if t is None:
+        return None
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == dtype and t.is_contiguous()):
+        raise Sl7Error(EINVAL, "%s must be a contiguous CUDA %s tensor" % (name, dtype))
+    if n is not None and t.numel() < n:
+        raise Sl7Error(EINVAL, "%s holds %d elements, %d needed" % (name, t.numel(), n))
+    return ctypes.c_void_p(t.data_ptr())
+
+
 def _stream_ptr(stream):
     import torch
     s = torch.cuda.current_stream() if stream is None else stream
@@ -185,13 +198,17 @@ def stats_summary(h_stats, opts, q_levels=()):
 
 def philox_u32(seed, path_offset, n_paths, block, out, stream=None):
     L = load_library()
-    _check(L.sl7_philox_u32(int(seed), int(path_offset), int(n_paths), int(block), _dptr(out), _stream_ptr(stream)))
+    import torch
+    o = _dbuf(out, out.dtype if out is not None and out.dtype in (torch.int32, torch.uint32) else torch.int32, 4 * int(n_paths), "out")
+    _check(L.sl7_philox_u32(int(seed), int(path_offset), int(n_paths), int(block), o, _stream_ptr(stream)))
     return out
 
 
 def normals(seed, path_offset, n_paths, n_steps, out, stream=None, flags=0):
     L = load_library()
-    _check(L.sl7_normals(int(seed), int(path_offset), int(n_paths), int(n_steps), int(flags), _dptr(out),
+    import torch
+    o = _dbuf(out, torch.float32, int(n_paths) * int(n_steps), "out")
+    _check(L.sl7_normals(int(seed), int(path_offset), int(n_paths), int(n_steps), int(flags), o,
                          _stream_ptr(stream)))
     return out
 
@@ -229,8 +246,10 @@ class Context:
         if out is None and out_mode != OUT_STATS:
             out = torch.empty(out_elems(n_steps, n_paths, out_mode), dtype=torch.float32, device=dev)
         th = (ctypes.c_double * max(1, len(theta)))(*theta)
+        po = _dbuf(out, torch.float32, out_elems(n_steps, n_paths, out_mode), "out") if out_mode != OUT_STATS else None
+        ps = _dbuf(stats, torch.float64, _stats_need(opts), "stats")
         _check(_lib.sl7_simulate(self._h, float(y0), float(dt), int(n_steps), th, len(theta), int(n_paths),
-                                 int(seed), out_mode, ctypes.byref(opts), _dptr(out), _dptr(stats)), self._h)
+                                 int(seed), out_mode, ctypes.byref(opts), po, ps), self._h)
         return out, stats
 
     def simulate_host(self, y0, dt, n_steps, theta, n_paths, seed, out_mode, opts, h_out=None, h_stats=None):
@@ -238,8 +257,14 @@ class Context:
         import numpy as np
         th = (ctypes.c_double * max(1, len(theta)))(*theta)
         up, down = ctypes.c_uint64(), ctypes.c_uint64()
-        po = None if h_out is None else h_out.ctypes.data_as(ctypes.c_void_p)
-        ps = None if h_stats is None else h_stats.ctypes.data_as(ctypes.c_void_p)
+        def hbuf(a, dtype, n, name):
+            if a is None:
+                return None
+            if not (isinstance(a, np.ndarray) and a.dtype == dtype and a.flags["C_CONTIGUOUS"] and a.size >= n):
+                raise Sl7Error(EINVAL, "%s must be a C-contiguous numpy %s array of >= %d elements" % (name, dtype, n))
+            return a.ctypes.data_as(ctypes.c_void_p)
+        po = hbuf(h_out, np.float32, out_elems(n_steps, n_paths, out_mode), "h_out") if out_mode != OUT_STATS else None
+        ps = hbuf(h_stats, np.float64, _stats_need(opts) or 0, "h_stats")
         _check(_lib.sl7_simulate_host(self._h, float(y0), float(dt), int(n_steps), th, len(theta), int(n_paths),
                                       int(seed), out_mode, ctypes.byref(opts), po, ps, ctypes.byref(up),
                                       ctypes.byref(down)), self._h)
@@ -253,9 +278,10 @@ class Context:
         if out is None and out_mode != OUT_STATS:
             out = torch.empty(out_elems(n_steps, n_paths, out_mode), dtype=torch.float32, device=dev)
         th = (ctypes.c_double * max(1, len(theta)))(*theta)
+        po = _dbuf(out, torch.float32, out_elems(n_steps, n_paths, out_mode), "out") if out_mode != OUT_STATS else None
+        ps = _dbuf(stats, torch.float64, _stats_need(opts), "stats")
         _check(_lib.sl7_simulate_em(self._h, int(model), float(y0), float(dt), int(n_steps), int(substeps), th,
-                                    len(theta), int(n_paths), int(seed), out_mode, ctypes.byref(opts), _dptr(out),
-                                    _dptr(stats)), self._h)
+                                    len(theta), int(n_paths), int(seed), out_mode, ctypes.byref(opts), po, ps), self._h)
         return out, stats
 
     def training_set(self, model, features, n_inner, dtau, seed, opts, terminal=None, labels=None):
@@ -267,25 +293,44 @@ class Context:
         n_rows = F.shape[0]
         if labels is None:
             labels = torch.empty((n_rows, self.m), dtype=torch.float64, device=torch.device("cuda", self.device))
+        pt = _dbuf(terminal, torch.float32, n_rows * int(n_inner), "terminal")
+        pl = _dbuf(labels, torch.float64, n_rows * self.m, "labels")
         _check(_lib.sl7_training_set(self._h, int(model), F.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                                      int(n_rows), int(n_inner), float(dtau), int(seed), ctypes.byref(opts),
-                                     _dptr(terminal), _dptr(labels)), self._h)
+                                     pt, pl), self._h)
         return terminal, labels
 
     # ---- sharded 7L-CDC (include/sl7.h, "Sharded 7L-CDC"): the caller drives the loop -------------
     def cdc_init(self, y0, dt, n_steps, theta, n_paths, seed, opts, state):
+        import torch
         th = (ctypes.c_double * max(1, len(theta)))(*theta)
+        ps = _dbuf(state, torch.float32, int(n_paths), "state")
         _check(_lib.sl7_cdc_init(self._h, float(y0), float(dt), int(n_steps), th, len(theta), int(n_paths), int(seed),
-                                 ctypes.byref(opts), _dptr(state)), self._h)
+                                 ctypes.byref(opts), ps), self._h)
+        self._cdc_n, self._cdc_bins = int(n_paths), int(opts.n_bins)
 
     def cdc_hist(self, state, pass_, hist):
-        _check(_lib.sl7_cdc_hist(self._h, _dptr(state), int(pass_), _dptr(hist)), self._h)
+        import torch
+        n = getattr(self, "_cdc_n", 0)
+        _check(_lib.sl7_cdc_hist(self._h, _dbuf(state, torch.float32, n, "state"), int(pass_),
+                                 _dbuf(hist, torch.int64, cdc_hist_elems(), "hist")), self._h)
 
     def cdc_select(self, pass_, hist):
-        _check(_lib.sl7_cdc_select(self._h, int(pass_), _dptr(hist)), self._h)
+        import torch
+        _check(_lib.sl7_cdc_select(self._h, int(pass_), _dbuf(hist, torch.int64, cdc_hist_elems(), "hist")), self._h)
 
     def cdc_step(self, step, state_in, state_out, stats=None):
-        _check(_lib.sl7_cdc_step(self._h, int(step), _dptr(state_in), _dptr(state_out), _dptr(stats)), self._h)
+        import torch
+        n = getattr(self, "_cdc_n", 0)
+        _check(_lib.sl7_cdc_step(self._h, int(step), _dbuf(state_in, torch.float32, n, "state_in"),
+                                 _dbuf(state_out, torch.float32, n, "state_out"),
+                                 _dbuf(stats, torch.float64, stats_elems(getattr(self, "_cdc_bins", 0)), "stats")),
+               self._h)
+
+
+def _stats_need(opts):
+    """Elements of the stats vector opts describes (None when n_bins is invalid: the library rejects it)."""
+    return stats_elems(opts.n_bins) if 0 <= opts.n_bins <= 16384 else None
 
 
 def cdc_hist_elems():

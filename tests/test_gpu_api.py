@@ -147,3 +147,24 @@ def test_max_histogram_bins(gpu_lib, kind):
     assert v[0] == ref[0] == N
     np.testing.assert_array_equal(v[8:], ref[8:])
     np.testing.assert_allclose(v[2:6], ref[2:6], rtol=1e-10)
+
+
+def test_binding_rejects_undersized_or_mistyped_buffers(gpu_lib):
+    """The C ABI takes plain device pointers; the binding checks dtype, device, contiguity and size first."""
+    sl7 = gpu_lib
+    torch = _torch()
+    ctx = sl7.Context(5)
+    o = sl7.make_opts(colloc=sl7.COLLOC_EXACT_GBM)
+    th = (0.05, 0.2)
+    for out, msg in [(torch.empty(29, dtype=torch.float32, device="cuda"), "needed"),
+                     (torch.empty(30, dtype=torch.float64, device="cuda"), "float32"),
+                     (torch.empty(30, dtype=torch.float32), "CUDA"),
+                     (torch.empty(60, dtype=torch.float32, device="cuda")[::2], "contiguous")]:
+        with pytest.raises(sl7.Sl7Error, match=msg):
+            ctx.simulate(1.0, 0.5, 2, th, 10, 1, sl7.OUT_FULL, o, out=out)
+    with pytest.raises(sl7.Sl7Error, match="stats"):
+        ctx.simulate(1.0, 0.5, 2, th, 10, 1, sl7.OUT_STATS, sl7.make_opts(colloc=sl7.COLLOC_EXACT_GBM, n_bins=64,
+                                                                          hist_lo=0, hist_hi=2),
+                     stats=torch.zeros(sl7.stats_elems(64) - 1, dtype=torch.float64, device="cuda"))
+    with pytest.raises(sl7.Sl7Error, match="h_out"):
+        ctx.simulate_host(1.0, 0.5, 2, th, 10, 1, sl7.OUT_TERMINAL, o, np.empty(9, dtype=np.float32))

@@ -189,7 +189,7 @@ def test_em_and_training_validation(gpu_lib):
     sl7 = gpu_lib
     torch = _torch()
     ctx = sl7.Context(5)
-    out = torch.empty(10, dtype=torch.float32, device="cuda")
+    out = torch.empty(15, dtype=torch.float32, device="cuda")
     for kw, msg in [(dict(model=0), "model"), (dict(model=4), "model"), (dict(theta=(0.1,)), "theta"),
                     (dict(substeps=0), "substeps"), (dict(flags=sl7.FLAG_SPECIALIZED), "flags"),
                     (dict(theta=(0.0, -1.0, 0.5)), "rate"), (dict(dt=-1.0), "dt")]:
