@@ -21,8 +21,9 @@ paper's order (Algorithm I):
 Pins (tests/test_oracle_*.py, marked "not gpu") tie each part to something
 other than itself: closed-form Hermite roots, Random123 known-answer vectors,
 mpmath Box-Muller, torch float64 MLP, polynomial reproduction, the GBM and OU
-closed forms (Eq. 6.6), numpy statistics.  Parity unpinned: none of O1-O6 --
-only *multi-step ANN paths* are pinned by composition alone.
+closed forms (Eq. 6.6), numpy statistics; multi-step ANN composition through an exactly-affine
+softplus network against the Eq. 6.6 recursion.  Parity unpinned: multi-step paths of a generic
+trained network beyond that composition test.
 """
 from __future__ import annotations
 

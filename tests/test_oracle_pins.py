@@ -526,3 +526,50 @@ def test_cir_exact_collocation_paths_match_cir_moments():
     var = y0f * s * s / k * (e - e * e) + ybar * s * s / (2 * k) * (1 - e) ** 2
     assert abs(YT.mean() - mean) < 4 * math.sqrt(var / P)
     assert abs(YT.var() - var) < 4 * var * math.sqrt(2.0 / P) * 1.5
+
+
+# --------------------------------------------------- multi-step ANN paths against a closed form
+
+def _affine_softplus_mlp(dims, slope, intercepts):
+    """A softplus MLP whose output is exactly y_j = slope * Y + intercepts[j]: softplus(z) - softplus(-z) = z,
+    so hidden units 0 and 1 carry softplus(+Y) and softplus(-Y) through every layer (weights +-1) and all
+    other units are dead (zero outgoing weights)."""
+    W, bs = [], []
+    for l in range(len(dims) - 1):
+        fi, fo = dims[l], dims[l + 1]
+        w, bb = np.zeros((fo, fi)), np.zeros(fo)
+        if l == 0:
+            w[0, 0], w[1, 0] = 1.0, -1.0
+        elif l < len(dims) - 2:
+            w[0, 0], w[0, 1], w[1, 0], w[1, 1] = 1.0, -1.0, -1.0, 1.0
+        else:
+            w[:, 0], w[:, 1] = slope, -slope
+            bb = np.asarray(intercepts, dtype=np.float64)
+        W.append(w)
+        bs.append(bb)
+    return MlpParams(tuple(dims), ACT_SOFTPLUS, W, bs)
+
+
+def test_multistep_ann_paths_equal_affine_recursion():
+    """Multi-step ANN composition pinned to a closed form: with the OU collocation points of Eq. 6.6
+    (y_j = a Y + b + s x_j) built into an exactly-affine softplus network, n 7L steps must equal the
+    recursion Y <- a32 Y + L(Z) on the same normals, L the Lagrange interpolant of the (fp32-stored)
+    intercepts -- to float64 rounding, over 12 steps -- and, the intercepts being affine in x_j up to their
+    fp32 rounding, stay within 1e-6 of the exact Eq. 6.6 path."""
+    theta, dt, n, m = (0.3, 1.2, 0.4), 0.25, 12, 7
+    ybar, lam, sig = theta
+    x = O.gauss_hermite_nodes(m)
+    a = math.exp(-lam * dt)
+    b = ybar * (1 - a)
+    s = sig * math.sqrt((1 - math.exp(-2 * lam * dt)) / (2 * lam))
+    net = O.parse_blob(pack_blob(_affine_softplus_mlp((5, 50, 50, 50, 50, m), a, b + s * x)))
+    a32 = float(np.float32(a))
+    c32 = (b + s * x).astype(np.float32).astype(np.float64)
+    paths = np.arange(2000, dtype=np.uint64)
+    Ya, Z = O.simulate(O.Spec(m, "ann", theta, 0.7, dt, n, net=net), 5, paths)
+    Y = np.full(len(paths), 0.7)
+    for i in range(n):
+        Y = a32 * Y + O.lagrange_eval(Z[i], x, np.broadcast_to(c32, (len(paths), m)))
+        np.testing.assert_allclose(Ya[i + 1], Y, rtol=0, atol=1e-12)
+    R = O.exact_reference("ou", theta, 0.7, dt, Z)
+    np.testing.assert_allclose(Ya[-1], R, rtol=0, atol=1e-6)
