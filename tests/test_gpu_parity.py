@@ -457,3 +457,35 @@ def test_specialized_rejects_large_m(gpu_lib):
     opts = sl7.make_opts(colloc=sl7.COLLOC_EXACT_GBM, flags=sl7.FLAG_SPECIALIZED)
     with pytest.raises(sl7.Sl7Error, match="EUNSUPPORTED"):
         ctx.simulate(1.0, 0.5, 2, (0.05, 0.2), 100, 1, sl7.OUT_TERMINAL, opts)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "split"])
+def test_multistep_ann_affine_network_free_running(gpu_lib, prec):
+    """16 free-running ANN steps of the exactly-affine softplus network (tests/test_oracle_pins.py) against
+    the closed-form recursion Y <- a32 Y + L(Z) on the device's own normals: fp32-class kernels stay within
+    the accumulated activation error (4 layers x 2 units x ~2.5e-7 per step, ~16 steps)."""
+    from _helpers import affine_softplus_mlp
+    sl7 = gpu_lib
+    torch = _torch()
+    theta, dt, n, m, N = (0.3, 1.2, 0.4), 0.125, 16, 7, 20_000
+    ybar, lam, sig = theta
+    x = O.gauss_hermite_nodes(m)
+    a = np.exp(-lam * dt)
+    b = ybar * (1 - a)
+    s = sig * np.sqrt((1 - np.exp(-2 * lam * dt)) / (2 * lam))
+    blob = pack_blob(affine_softplus_mlp((5, 50, 50, 50, 50, m), a, b + s * x))
+    ctx = sl7.Context(m, [5, 50, 50, 50, 50, m], ACT_SOFTPLUS)
+    ctx.load_weights(blob)
+    p = {"fp32": sl7.PREC_FP32, "split": sl7.PREC_SPLIT}[prec]
+    out, _ = ctx.simulate(0.7, dt, n, theta, N, 21, sl7.OUT_FULL, sl7.make_opts(prec=p, colloc=sl7.COLLOC_ANN))
+    z = torch.empty(n * N, dtype=torch.float32, device="cuda")
+    sl7.normals(21, 0, N, n, z)
+    torch.cuda.synchronize()
+    Yd = out.double().cpu().numpy().reshape(n + 1, N)
+    Z = z.double().cpu().numpy().reshape(n, N)
+    a32 = float(np.float32(a))
+    c32 = (b + s * x).astype(np.float32).astype(np.float64)
+    Y = np.full(N, float(np.float32(0.7)))
+    for i in range(n):
+        Y = a32 * Y + O.lagrange_eval(Z[i], x, np.broadcast_to(c32, (N, m)))
+        assert np.abs(Yd[i + 1] - Y).max() <= 5e-6 * (i + 1), (i, np.abs(Yd[i + 1] - Y).max())

@@ -14,6 +14,7 @@ import scipy.integrate
 import scipy.stats
 import torch
 
+from _helpers import affine_softplus_mlp
 from oracle import sl7_oracle as O
 from sl7_inputs import ACT_SOFTPLUS, ACT_TANH, MlpParams, glorot_mlp, pack_blob
 
@@ -530,26 +531,6 @@ def test_cir_exact_collocation_paths_match_cir_moments():
 
 # --------------------------------------------------- multi-step ANN paths against a closed form
 
-def _affine_softplus_mlp(dims, slope, intercepts):
-    """A softplus MLP whose output is exactly y_j = slope * Y + intercepts[j]: softplus(z) - softplus(-z) = z,
-    so hidden units 0 and 1 carry softplus(+Y) and softplus(-Y) through every layer (weights +-1) and all
-    other units are dead (zero outgoing weights)."""
-    W, bs = [], []
-    for l in range(len(dims) - 1):
-        fi, fo = dims[l], dims[l + 1]
-        w, bb = np.zeros((fo, fi)), np.zeros(fo)
-        if l == 0:
-            w[0, 0], w[1, 0] = 1.0, -1.0
-        elif l < len(dims) - 2:
-            w[0, 0], w[0, 1], w[1, 0], w[1, 1] = 1.0, -1.0, -1.0, 1.0
-        else:
-            w[:, 0], w[:, 1] = slope, -slope
-            bb = np.asarray(intercepts, dtype=np.float64)
-        W.append(w)
-        bs.append(bb)
-    return MlpParams(tuple(dims), ACT_SOFTPLUS, W, bs)
-
-
 def test_multistep_ann_paths_equal_affine_recursion():
     """Multi-step ANN composition pinned to a closed form: with the OU collocation points of Eq. 6.6
     (y_j = a Y + b + s x_j) built into an exactly-affine softplus network, n 7L steps must equal the
@@ -562,7 +543,7 @@ def test_multistep_ann_paths_equal_affine_recursion():
     a = math.exp(-lam * dt)
     b = ybar * (1 - a)
     s = sig * math.sqrt((1 - math.exp(-2 * lam * dt)) / (2 * lam))
-    net = O.parse_blob(pack_blob(_affine_softplus_mlp((5, 50, 50, 50, 50, m), a, b + s * x)))
+    net = O.parse_blob(pack_blob(affine_softplus_mlp((5, 50, 50, 50, 50, m), a, b + s * x)))
     a32 = float(np.float32(a))
     c32 = (b + s * x).astype(np.float32).astype(np.float64)
     paths = np.arange(2000, dtype=np.uint64)
