@@ -224,7 +224,8 @@ def main():
                      ("ann_tf32_tcgen05", ctx, sl7.COLLOC_ANN, sl7.PREC_TF32, 0, w.theta, N),
                      ("ann_split_bf16x3_tcgen05", ctx, sl7.COLLOC_ANN, sl7.PREC_SPLIT, 0, w.theta, N),
                      ("ann_fp32", ctx, sl7.COLLOC_ANN, sl7.PREC_FP32, 0, w.theta, N // 10),
-                     ("cdc_ann_fp32_table", ctx, sl7.COLLOC_ANN, sl7.PREC_FP32, -1, w.theta, N)]
+                     ("cdc_ann_fp32_table", ctx, sl7.COLLOC_ANN, sl7.PREC_FP32, -1, w.theta, N),
+                     ("cdc_ann_fp32_table_fast_normals", ctx, sl7.COLLOC_ANN, sl7.PREC_FP32, -2, w.theta, N)]
             if w.process == "cir":
                 ex = sl7.Context(w.m, device=0)
                 modes += [("exact_cir_ncx2_fp64", ex, sl7.COLLOC_EXACT_CIR, sl7.PREC_FP32, 0, w.theta, N // 100)]
@@ -234,9 +235,10 @@ def main():
                           ("exact_ou_fast_specialized", ex, sl7.COLLOC_EXACT_OU, sl7.PREC_FP32,
                            sl7.FLAG_FAST_NORMALS | sl7.FLAG_SPECIALIZED, w.theta, N)]
             for label, c, colloc, prec, flags, theta, n_paths in modes:
-                cdc = flags == -1            # marker: 7L-CDC scheme
+                cdc = flags < 0              # markers: 7L-CDC scheme (-2: with SL7_FLAG_FAST_NORMALS)
                 ref = sl7.REF_OU if (w.process == "ou" and not cdc) else sl7.REF_NONE
-                opts = sl7.make_opts(prec=prec, colloc=colloc, stream=stream, flags=0 if cdc else flags, n_bins=4096,
+                fl = (sl7.FLAG_FAST_NORMALS if flags == -2 else 0) if cdc else flags
+                opts = sl7.make_opts(prec=prec, colloc=colloc, stream=stream, flags=fl, n_bins=4096,
                                      hist_lo=lo, hist_hi=hi, shift=w.y0, ref=ref, ref_theta=w.theta,
                                      scheme=sl7.SCHEME_CDC if cdc else sl7.SCHEME_7L)
                 fn = (lambda c=c, theta=theta, opts=opts, n_paths=n_paths:

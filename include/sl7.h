@@ -124,7 +124,7 @@ typedef struct {
   sl7_scheme scheme;        /* SL7_SCHEME_7L (Algorithm I) or SL7_SCHEME_CDC */
 } sl7_run_opts;
 
-/* opts->flags (exact-collocation modes only; ignored otherwise):
+/* opts->flags (exact-collocation modes and 7L-CDC (FAST_NORMALS only); ignored by the 7L ANN kernels):
  *  SL7_FLAG_FAST_NORMALS : Box-Muller with MUFU lg2 (exact series for u -> 1) and a polynomial sincos
  *                          reduced exactly in revolutions: ~3x fewer instructions, |X_hat - X| <= ~1e-6.
  *  SL7_FLAG_SPECIALIZED  : evaluate g_m in closed form for the linear structure of the exact points:

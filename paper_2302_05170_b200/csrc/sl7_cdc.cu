@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(256) cdc_table_mlp_kernel(const __grid_constan
 }
 
 // ---- per-path CDC step: conditional points by interpolation in the state, then g_m(X_hat)
-template <int MR, bool RT_M>
+template <int MR, bool RT_M, bool FAST = false>
 __global__ void __launch_bounds__(256) cdc_step_kernel(const __grid_constant__ RunParams p, const CdcScratch* s,
                                                        const float* yin, float* yout,   // may alias (in place)
                                                        int step, int last, unsigned long long* next_hist) {
@@ -339,7 +339,8 @@ __global__ void __launch_bounds__(256) cdc_step_kernel(const __grid_constant__ R
     const uint4 rr = philox_path_block_rk(p.rk0, p.rk1, gp, (uint32_t)(step >> 2));
     const int r = step & 3;
     float za, zb;
-    box_muller((r < 2) ? rr.x : rr.z, (r < 2) ? rr.y : rr.w, za, zb);
+    if constexpr (FAST) box_muller_fast((r < 2) ? rr.x : rr.z, (r < 2) ? rr.y : rr.w, za, zb);
+    else box_muller((r < 2) ? rr.x : rr.z, (r < 2) ? rr.y : rr.w, za, zb);
     const float Z = (r & 1) ? zb : za;
     const float Yn = gm_eval<MR, RT_M>(p, Z, y);
     yout[q] = Yn;
@@ -414,8 +415,10 @@ int cdc_advance(const RunParams& p, void* scratch, const float* yin, float* yout
     cdc_table_exact_kernel<<<1, kMaxM * kMaxM, 0, st>>>(p, s);
   }
   const size_t hist = (stats && p.has_stats && p.n_bins > 0) ? sizeof(uint32_t) * (size_t)(p.n_bins + 2) : 0;
-  auto step_k = (p.m == 5) ? cdc_step_kernel<5, false> : (p.m == 7) ? cdc_step_kernel<7, false>
-                                                                    : cdc_step_kernel<kMaxM, true>;
+  const bool fast = p.flags & SL7_FLAG_FAST_NORMALS;
+  auto step_k = (p.m == 5) ? (fast ? cdc_step_kernel<5, false, true> : cdc_step_kernel<5, false>)
+              : (p.m == 7) ? (fast ? cdc_step_kernel<7, false, true> : cdc_step_kernel<7, false>)
+                           : (fast ? cdc_step_kernel<kMaxM, true, true> : cdc_step_kernel<kMaxM, true>);
   if (hist > 48 * 1024) {
     const cudaError_t e = cudaFuncSetAttribute(step_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hist);
     if (e != cudaSuccess) return (int)e;

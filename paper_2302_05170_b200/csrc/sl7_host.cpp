@@ -537,11 +537,12 @@ sl7_status prepare(sl7_ctx c, double Y0, double dt, int32_t n_steps, const doubl
   if (o->scheme != SL7_SCHEME_7L && o->scheme != SL7_SCHEME_CDC) return fail(c, SL7_EINVAL, "scheme");
   if (o->scheme == SL7_SCHEME_CDC) {
     if (o->ref != SL7_REF_NONE) return fail(c, SL7_EUNSUPPORTED, "scheme CDC: ref must be SL7_REF_NONE");
-    if (o->flags) return fail(c, SL7_EUNSUPPORTED, "scheme CDC: flags must be 0");
+    if (o->flags & ~SL7_FLAG_FAST_NORMALS)
+      return fail(c, SL7_EUNSUPPORTED, "scheme CDC: flags may only hold SL7_FLAG_FAST_NORMALS");
     if (p.colloc == kAnn && o->prec != SL7_PREC_FP32)
       return fail(c, SL7_EUNSUPPORTED, "scheme CDC: the m-row table runs in fp32 (prec must be SL7_PREC_FP32)");
   }
-  p.flags = (p.colloc == kAnn) ? 0u : o->flags;
+  p.flags = (p.colloc == kAnn && o->scheme != SL7_SCHEME_CDC) ? 0u : o->flags;
   return SL7_OK;
 }
 

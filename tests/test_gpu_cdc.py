@@ -34,19 +34,27 @@ def _setup(sl7, name, m, colloc, theta, y0, dt, n_steps):
     return ctx, code, theta, O.Spec(m, colloc, theta, y0, dt, n_steps)
 
 
+@pytest.mark.parametrize("fast", [False, True])
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
-def test_cdc_teacher_forced(gpu_lib, case):
+def test_cdc_teacher_forced(gpu_lib, case, fast):
     import torch
     sl7 = gpu_lib
     name, m, colloc, theta, y0, dt, n_steps = case
     ctx, code, th, spec = _setup(sl7, name, m, colloc, theta, y0, dt, n_steps)
     n_paths = 20_011
-    opts = sl7.make_opts(prec=sl7.PREC_FP32, colloc=code, scheme=sl7.SCHEME_CDC)
+    flags = sl7.FLAG_FAST_NORMALS if fast else 0
+    opts = sl7.make_opts(prec=sl7.PREC_FP32, colloc=code, scheme=sl7.SCHEME_CDC, flags=flags)
     out, _ = ctx.simulate(spec.y0, spec.dt, n_steps, th, n_paths, 9, sl7.OUT_FULL, opts)
     torch.cuda.synchronize()
     Yd = out.double().cpu().numpy().reshape(n_steps + 1, n_paths)
     assert np.all(Yd[0] == np.float32(spec.y0))
-    Z = O.normals(9, np.arange(n_paths, dtype=np.uint64), n_steps)
+    if fast:   # the fast Box-Muller is its own approximation: drive the oracle with the device's normals
+        z = torch.empty(n_steps * n_paths, dtype=torch.float32, device="cuda")
+        sl7.normals(9, 0, n_paths, n_steps, z, flags=sl7.FLAG_FAST_NORMALS)
+        torch.cuda.synchronize()
+        Z = z.double().cpu().numpy().reshape(n_steps, n_paths)
+    else:
+        Z = O.normals(9, np.arange(n_paths, dtype=np.uint64), n_steps)
     worst = 0.0
     for i in range(n_steps):
         ref = O.cdc_step(spec, Yd[i], Z[i])
