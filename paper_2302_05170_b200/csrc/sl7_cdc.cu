@@ -42,24 +42,54 @@ struct CdcScratch {
 // The states of one step are concentrated in a few digit bins, so the shared-memory increments are
 // warp-aggregated (__match_any_sync: one atomic per distinct bin per warp) instead of one per element.
 __device__ __forceinline__ void warp_hist_add(uint32_t* h, int bin) {   // bin < 0: nothing (all lanes call)
+  if (!__any_sync(0xffffffffu, bin >= 0)) return;   // later passes: most warps hold no candidate at all
   const unsigned peers = __match_any_sync(0xffffffffu, bin);
   if (bin >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[bin], (uint32_t)__popc(peers));
 }
 
+// Slot lookup: the elements of a pass that count are those whose key prefix (the 8 p bits fixed so far)
+// equals one of the <= 2m slot prefixes.  Instead of a per-element binary search (the targets span the
+// 0.01%..99.99% quantiles, so nearly every element is inside the prefix range and searched), the block
+// builds a table in shared memory: pass 1 indexes the 8-bit prefix directly; pass 2 the 16-bit prefix
+// (64 KB of one-byte slot ids); pass 3 maps the top 16 bits to a group of slots and then the next 8 bits
+// within that group.  Entries hold slot + 1 (0: no slot).
+constexpr int kCdcLutBytes = 65536 + kCdcMaxT * 256;
+
+template <int U>
 __global__ void __launch_bounds__(256) cdc_hist_kernel(const float* __restrict__ y, uint64_t n, int pass,
                                                        const CdcScratch* s, unsigned long long* __restrict__ hist) {
+  extern __shared__ uint4 lut4[];
+  uint8_t* lut16 = reinterpret_cast<uint8_t*>(lut4);        // [65536] (pass 1 uses the first 256)
+  uint8_t* lut3 = lut16 + 65536;                             // [groups][256] (pass 3)
   __shared__ uint32_t h[kCdcMaxT * 256];
-  __shared__ uint32_t sp[kCdcMaxT];
   const int nslot = s->nslot;
   for (int i = threadIdx.x; i < nslot * 256; i += blockDim.x) h[i] = 0u;
-  if (threadIdx.x < nslot) sp[threadIdx.x] = s->slot_prefix[threadIdx.x];
+  if (pass > 0) {
+    const int words = (pass == 1) ? 256 / 16 : kCdcLutBytes / 16;
+    for (int i = threadIdx.x; i < words; i += blockDim.x) lut4[i] = make_uint4(0u, 0u, 0u, 0u);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (pass < 3) {
+        for (int k = 0; k < nslot; ++k) lut16[s->slot_prefix[k]] = (uint8_t)(k + 1);   // 8- or 16-bit prefixes
+      } else {
+        int ng = 0;   // slot prefixes are ascending, so equal top-16 parts are adjacent
+        uint32_t last = 0xFFFFFFFFu;
+        for (int k = 0; k < nslot; ++k) {
+          const uint32_t sp = s->slot_prefix[k];
+          if ((sp >> 8) != last) {
+            last = sp >> 8;
+            lut16[last] = (uint8_t)(++ng);
+          }
+          lut3[(ng - 1) * 256 + (sp & 255u)] = (uint8_t)(k + 1);
+        }
+      }
+    }
+  }
   __syncthreads();
   const int shift = 24 - 8 * pass;
-  const uint32_t lo = sp[0], hi = sp[nslot - 1];
   const int lane = threadIdx.x & 31;
-  // each warp takes chunks of 128 consecutive elements: 4 coalesced loads in flight per thread, then the
-  // four (warp-aggregated) increments; the trip count is warp-uniform, so every lane joins each match
-  constexpr int U = 4;
+  // each warp takes chunks of 32 U consecutive elements: U coalesced loads in flight per thread (the LUT
+  // passes run at 2 blocks per SM, so they need the deeper chunks to keep HBM busy)
   const uint64_t wstride = (uint64_t)gridDim.x * blockDim.x * U;
   for (uint64_t base = ((uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) * U; base < n; base += wstride) {
     float v[U];
@@ -77,18 +107,18 @@ __global__ void __launch_bounds__(256) cdc_hist_kernel(const float* __restrict__
         if (pass == 0) {
           bin = digit;
         } else {
-          const uint32_t pre = key >> (shift + 8);
-          if (pre >= lo && pre <= hi) {
-            int a = 0, b = nslot - 1;   // binary search in the ascending slot prefixes
-            while (a < b) {
-              const int mid = (a + b) >> 1;
-              if (sp[mid] < pre) a = mid + 1; else b = mid;
-            }
-            if (sp[a] == pre) bin = a * 256 + digit;
+          int slot;
+          if (pass < 3) {
+            slot = (int)lut16[key >> (shift + 8)] - 1;
+          } else {
+            const int g = (int)lut16[key >> 16];
+            slot = g ? (int)lut3[(g - 1) * 256 + ((key >> 8) & 255u)] - 1 : -1;
           }
+          if (slot >= 0) bin = slot * 256 + digit;
         }
       }
-      warp_hist_add(h, bin);
+      if (pass == 0) warp_hist_add(h, bin);              // few distinct bins: aggregate per warp
+      else if (bin >= 0) atomicAdd(&h[bin], 1u);
     }
   }
   __syncthreads();
@@ -392,8 +422,15 @@ int cdc_hist(const RunParams& p, void* scratch, const float* y, int pass, unsign
     const cudaError_t e = cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * kCdcMaxT * 256, st);
     if (e != cudaSuccess) return (int)e;
   }
-  cdc_hist_kernel<<<cdc_grid(p.n_paths, num_sms), 256, 0, st>>>(y, p.n_paths, pass,
-                                                                 reinterpret_cast<const CdcScratch*>(scratch), hist);
+  const CdcScratch* sc = reinterpret_cast<const CdcScratch*>(scratch);
+  if (pass < 2) {
+    cdc_hist_kernel<4><<<cdc_grid(p.n_paths, num_sms), 256, pass ? 256 : 0, st>>>(y, p.n_paths, pass, sc, hist);
+  } else {
+    const cudaError_t e = cudaFuncSetAttribute(cdc_hist_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               kCdcLutBytes);
+    if (e != cudaSuccess) return (int)e;
+    cdc_hist_kernel<16><<<cdc_grid(p.n_paths, num_sms), 256, kCdcLutBytes, st>>>(y, p.n_paths, pass, sc, hist);
+  }
   return (int)cudaGetLastError();
 }
 
