@@ -322,11 +322,16 @@ __global__ void __launch_bounds__(256) cdc_step_kernel(const __grid_constant__ R
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const int lane = threadIdx.x & 31;
   // warp-uniform trip count (the fused histogram's __match_any_sync needs every lane)
-  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < p.n_paths; base += stride) {
+  // the state of the next path is loaded one iteration ahead: at ~25% occupancy the load latency of Y was
+  // the top stall (the first use of Y), not the arithmetic
+  const uint64_t first = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
+  float Ynext = (first + lane < p.n_paths) ? yin[first + lane] : 0.0f;
+  for (uint64_t base = first; base < p.n_paths; base += stride) {
     const uint64_t q = base + lane;
+    const float Y = Ynext;
+    if (q + stride < p.n_paths) Ynext = yin[q + stride];   // yin may alias yout: a different path's slot
     int nbin = -1;
     if (q < p.n_paths) {
-    const float Y = yin[q];
     float y[MR];
     if (sdeg) {
       int kb = 0;
