@@ -195,6 +195,21 @@ sl7_status sl7_simulate_host(sl7_ctx ctx, double Y0, double dt, int32_t n_steps,
                              const sl7_run_opts* opts, float* h_out, double* h_stats,
                              uint64_t* h2d_bytes, uint64_t* d2h_bytes);
 
+/* Pipelined form of sl7_simulate_host: enqueues the kernels on opts->stream and the result copies into
+ * h_out / h_stats on a context-owned copy stream, and returns without waiting, so the next call's kernels
+ * overlap this call's device->host copies.  The host buffers should be page-locked (cudaHostAlloc /
+ * torch pin_memory) -- pageable buffers work but serialise -- and must not be read (or, with
+ * opts->accumulate, h_stats modified) before sl7_sync(ctx) returns.  The context alternates between two
+ * device staging slots; a call waits on the device for the copies of the call two before it.  Byte
+ * counts as sl7_simulate_host.  Errors: as sl7_simulate_host (launch errors surface at the latest in
+ * sl7_sync). */
+sl7_status sl7_simulate_host_async(sl7_ctx ctx, double Y0, double dt, int32_t n_steps, const double* theta,
+                                   int32_t n_theta, uint64_t n_paths, uint64_t seed, sl7_out out_mode,
+                                   const sl7_run_opts* opts, float* h_out, double* h_stats,
+                                   uint64_t* h2d_bytes, uint64_t* d2h_bytes);
+/* Wait until every sl7_simulate_host_async result of this context is in host memory. */
+sl7_status sl7_sync(sl7_ctx ctx);
+
 /* Moments, strong error and quantiles from a HOST copy of a stats vector (which the caller may
  * have all-reduced across ranks first).  opts supplies shift, hist_lo, hist_hi, n_bins.
  * Returns SL7_ENONFINITE (after filling *out) if n_nonfinite > 0; SL7_EINVAL if n == 0. */

@@ -62,7 +62,8 @@ class Sl7Error(RuntimeError):
 STATUS_NAMES = {0: "SL7_OK", 1: "SL7_EINVAL", 2: "SL7_ESTATE", 3: "SL7_EFORMAT", 4: "SL7_ENOMEM",
                 5: "SL7_ECUDA", 6: "SL7_ENONFINITE", 7: "SL7_EUNSUPPORTED"}
 
-EXPORTS = ["sl7_create", "sl7_load_weights", "sl7_simulate", "sl7_simulate_host", "sl7_simulate_em",
+EXPORTS = ["sl7_create", "sl7_load_weights", "sl7_simulate", "sl7_simulate_host", "sl7_simulate_host_async",
+           "sl7_sync", "sl7_simulate_em",
            "sl7_training_set", "sl7_cdc_hist_elems", "sl7_cdc_init", "sl7_cdc_hist", "sl7_cdc_select",
            "sl7_cdc_step", "sl7_stats",
            "sl7_philox_u32", "sl7_normals", "sl7_gh_grid", "sl7_out_elems", "sl7_stats_elems",
@@ -87,6 +88,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                c.POINTER(sl7_run_opts), fp, fp]
     L.sl7_simulate_host.argtypes = [vp, c.c_double, c.c_double, i32, dp, i32, u64, u64, c.c_int,
                                     c.POINTER(sl7_run_opts), fp, fp, c.POINTER(u64), c.POINTER(u64)]
+    L.sl7_simulate_host_async.argtypes = L.sl7_simulate_host.argtypes
+    L.sl7_sync.argtypes = [vp]
     L.sl7_simulate_em.argtypes = [vp, c.c_int, c.c_double, c.c_double, i32, i32, dp, i32, u64, u64, c.c_int,
                                   c.POINTER(sl7_run_opts), fp, fp]
     L.sl7_training_set.argtypes = [vp, c.c_int, dp, u64, c.c_uint32, c.c_double, u64, c.POINTER(sl7_run_opts),
@@ -112,7 +115,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L.sl7_abi_version.restype = i32
     L.sl7_destroy.argtypes = [vp]
     L.sl7_destroy.restype = None
-    for name in ("sl7_create", "sl7_load_weights", "sl7_simulate", "sl7_simulate_host", "sl7_simulate_em",
+    for name in ("sl7_create", "sl7_load_weights", "sl7_simulate", "sl7_simulate_host", "sl7_simulate_host_async",
+                 "sl7_sync", "sl7_simulate_em",
                  "sl7_training_set", "sl7_cdc_init", "sl7_cdc_hist", "sl7_cdc_select", "sl7_cdc_step", "sl7_stats",
                  "sl7_philox_u32", "sl7_normals", "sl7_gh_grid"):
         getattr(L, name).restype = c.c_int
@@ -269,6 +273,29 @@ class Context:
                                       int(seed), out_mode, ctypes.byref(opts), po, ps, ctypes.byref(up),
                                       ctypes.byref(down)), self._h)
         return h_out, h_stats, up.value, down.value
+
+    def simulate_host_async(self, y0, dt, n_steps, theta, n_paths, seed, out_mode, opts, h_out=None, h_stats=None):
+        """sl7_simulate_host_async: enqueue a host-buffer run and return (h_out, h_stats, h2d, d2h) at once;
+        the buffers (ideally pinned) hold the results after sync()."""
+        import numpy as np
+        th = (ctypes.c_double * max(1, len(theta)))(*theta)
+        up, down = ctypes.c_uint64(), ctypes.c_uint64()
+
+        def hbuf(a, dtype, n, name):
+            if a is None:
+                return None
+            if not (isinstance(a, np.ndarray) and a.dtype == dtype and a.flags["C_CONTIGUOUS"] and a.size >= n):
+                raise Sl7Error(EINVAL, "%s must be a C-contiguous numpy %s array of >= %d elements" % (name, dtype, n))
+            return a.ctypes.data_as(ctypes.c_void_p)
+        po = hbuf(h_out, np.float32, out_elems(n_steps, n_paths, out_mode), "h_out") if out_mode != OUT_STATS else None
+        ps = hbuf(h_stats, np.float64, _stats_need(opts) or 0, "h_stats")
+        _check(_lib.sl7_simulate_host_async(self._h, float(y0), float(dt), int(n_steps), th, len(theta), int(n_paths),
+                                            int(seed), out_mode, ctypes.byref(opts), po, ps, ctypes.byref(up),
+                                            ctypes.byref(down)), self._h)
+        return h_out, h_stats, up.value, down.value
+
+    def sync(self):
+        _check(_lib.sl7_sync(self._h), self._h)
 
     def simulate_em(self, model, y0, dt, n_steps, substeps, theta, n_paths, seed, out_mode, opts, out=None,
                     stats=None):

@@ -54,6 +54,18 @@ struct sl7_ctx_s {
   size_t out_cap = 0;
   double* d_stats_scratch = nullptr;
   size_t stats_cap = 0;
+  // sl7_simulate_host_async: two device staging slots used alternately, D2H on a context-owned stream
+  struct Staging {
+    float* d_out = nullptr;
+    size_t out_cap = 0;
+    double* d_stats = nullptr;
+    size_t stats_cap = 0;
+    cudaEvent_t copied = nullptr;   // D2H of this slot's last call finished
+    bool used = false;
+  } stage[2];
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t computed = nullptr;
+  int next_stage = 0;
   // training-set generator: feature rows and terminal-value scratch
   EmRow* d_rows = nullptr;
   size_t rows_cap = 0;
@@ -1035,6 +1047,100 @@ sl7_status sl7_simulate_host(sl7_ctx c, double Y0, double dt, int32_t n_steps, c
   return SL7_OK;
 }
 
+sl7_status sl7_simulate_host_async(sl7_ctx c, double Y0, double dt, int32_t n_steps, const double* theta,
+                                   int32_t n_theta, uint64_t n_paths, uint64_t seed, sl7_out out_mode,
+                                   const sl7_run_opts* opts, float* h_out, double* h_stats, uint64_t* h2d_bytes,
+                                   uint64_t* d2h_bytes) {
+  RunParams p;
+  sl7_status s = prepare(c, Y0, dt, n_steps, theta, n_theta, n_paths, seed, out_mode, opts, p, h_out != nullptr,
+                         h_stats != nullptr);
+  if (s != SL7_OK) return s;
+  DeviceGuard g(c->device);
+  if (!g.ok) return fail(c, SL7_ECUDA, "cudaSetDevice(%d)", c->device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(opts->stream);
+  cudaError_t e;
+  if (!c->copy_stream) {
+    e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_fail(c, e, "copy stream");
+    e = cudaEventCreateWithFlags(&c->computed, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(c, e, "event");
+    for (auto& sg : c->stage) {
+      e = cudaEventCreateWithFlags(&sg.copied, cudaEventDisableTiming);
+      if (e != cudaSuccess) return cuda_fail(c, e, "event");
+    }
+  }
+  auto& sg = c->stage[c->next_stage];
+  const size_t n_out = sl7_out_elems(n_steps, n_paths, out_mode);
+  const size_t n_st = h_stats ? sl7_stats_elems(opts->n_bins) : 0;
+  // this slot's previous D2H must be done before its buffers are rewritten (and before reallocation)
+  if (sg.used) {
+    e = cudaStreamWaitEvent(st, sg.copied, 0);
+    if (e != cudaSuccess) return cuda_fail(c, e, "wait for staging slot");
+  }
+  if (n_out > sg.out_cap || n_st > sg.stats_cap) {
+    if (sg.used) {
+      e = cudaEventSynchronize(sg.copied);
+      if (e != cudaSuccess) return cuda_fail(c, e, "staging slot");
+    }
+    if (n_out > sg.out_cap) {
+      if (sg.d_out) cudaFree(sg.d_out);
+      sg.d_out = nullptr;
+      sg.out_cap = 0;
+      e = cudaMalloc(&sg.d_out, n_out * sizeof(float));
+      if (e != cudaSuccess) return cuda_fail(c, e, "cudaMalloc(staging out)");
+      sg.out_cap = n_out;
+    }
+    if (n_st > sg.stats_cap) {
+      if (sg.d_stats) cudaFree(sg.d_stats);
+      sg.d_stats = nullptr;
+      sg.stats_cap = 0;
+      e = cudaMalloc(&sg.d_stats, n_st * sizeof(double));
+      if (e != cudaSuccess) return cuda_fail(c, e, "cudaMalloc(staging stats)");
+      sg.stats_cap = n_st;
+    }
+  }
+  uint64_t up = 0, down = 0;
+  sl7_run_opts o = *opts;
+  if (h_stats && opts->accumulate) {
+    e = cudaMemcpyAsync(sg.d_stats, h_stats, n_st * sizeof(double), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(c, e, "H2D stats");
+    up += n_st * sizeof(double);
+  }
+  s = run(c, p, &o, n_out ? sg.d_out : nullptr, h_stats ? sg.d_stats : nullptr);
+  if (s != SL7_OK) return s;
+  // results leave on the copy stream, so the next call's kernels (on opts->stream) overlap this D2H
+  e = cudaEventRecord(c->computed, st);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(c->copy_stream, c->computed, 0);
+  if (e != cudaSuccess) return cuda_fail(c, e, "copy ordering");
+  if (n_out) {
+    e = cudaMemcpyAsync(h_out, sg.d_out, n_out * sizeof(float), cudaMemcpyDeviceToHost, c->copy_stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, "D2H out");
+    down += n_out * sizeof(float);
+  }
+  if (n_st) {
+    e = cudaMemcpyAsync(h_stats, sg.d_stats, n_st * sizeof(double), cudaMemcpyDeviceToHost, c->copy_stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, "D2H stats");
+    down += n_st * sizeof(double);
+  }
+  e = cudaEventRecord(sg.copied, c->copy_stream);
+  if (e != cudaSuccess) return cuda_fail(c, e, "event record");
+  sg.used = true;
+  c->next_stage ^= 1;
+  up += sizeof(RunParams);
+  if (h2d_bytes) *h2d_bytes = up;
+  if (d2h_bytes) *d2h_bytes = down;
+  return SL7_OK;
+}
+
+sl7_status sl7_sync(sl7_ctx c) {
+  if (!c) return fail(c, SL7_EINVAL, "ctx is NULL");
+  if (!c->copy_stream) return SL7_OK;
+  DeviceGuard g(c->device);
+  if (!g.ok) return fail(c, SL7_ECUDA, "cudaSetDevice(%d)", c->device);
+  const cudaError_t e = cudaStreamSynchronize(c->copy_stream);
+  return e == cudaSuccess ? SL7_OK : cuda_fail(c, e, "sl7_sync");
+}
+
 sl7_status sl7_stats(const double* v, const sl7_run_opts* o, sl7_summary* out) {
   if (!v || !o || !out) return fail(nullptr, SL7_EINVAL, "NULL argument");
   if (o->n_bins < 0 || o->n_bins > 16384) return fail(nullptr, SL7_EINVAL, "n_bins");
@@ -1110,6 +1216,14 @@ void sl7_destroy(sl7_ctx c) {
     if (c->d_stats_scratch) cudaFree(c->d_stats_scratch);
     if (c->d_rows) cudaFree(c->d_rows);
     if (c->d_term_scratch) cudaFree(c->d_term_scratch);
+    if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+    for (auto& sg : c->stage) {
+      if (sg.d_out) cudaFree(sg.d_out);
+      if (sg.d_stats) cudaFree(sg.d_stats);
+      if (sg.copied) cudaEventDestroy(sg.copied);
+    }
+    if (c->computed) cudaEventDestroy(c->computed);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   }
   delete c;
 }

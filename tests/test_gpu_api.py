@@ -168,3 +168,27 @@ def test_binding_rejects_undersized_or_mistyped_buffers(gpu_lib):
                      stats=torch.zeros(sl7.stats_elems(64) - 1, dtype=torch.float64, device="cuda"))
     with pytest.raises(sl7.Sl7Error, match="h_out"):
         ctx.simulate_host(1.0, 0.5, 2, th, 10, 1, sl7.OUT_TERMINAL, o, np.empty(9, dtype=np.float32))
+
+
+def test_host_async_pipeline_equals_sync_calls(gpu_lib):
+    """Several sl7_simulate_host_async calls in flight (two staging slots, copies overlapping the next
+    call's kernels) give exactly the results of the blocking calls."""
+    sl7 = gpu_lib
+    torch = _torch()
+    w = workloads()["cfg1"]
+    ctx = sl7.Context(w.m, list(w.dims), w.act)
+    ctx.load_weights(load_golden_blob(w.blob))
+    opts = sl7.make_opts(prec=sl7.PREC_BF16, colloc=sl7.COLLOC_ANN, n_bins=64, hist_lo=0, hist_hi=4, shift=1.0)
+    N, sweep = 300_001, (1, 2, 4, 8, 16)
+    outs = [torch.empty(N, dtype=torch.float32, pin_memory=True).numpy() for _ in sweep]
+    sts = [torch.empty(sl7.stats_elems(64), dtype=torch.float64, pin_memory=True).numpy() for _ in sweep]
+    for ns, o, s_ in zip(sweep, outs, sts):
+        ctx.simulate_host_async(w.y0, 1.0 / ns, ns, (), N, w.seed, sl7.OUT_TERMINAL, opts, o, s_)
+    ctx.sync()
+    for ns, o, s_ in zip(sweep, outs, sts):
+        ro = np.empty(N, dtype=np.float32)
+        rs = np.empty(sl7.stats_elems(64), dtype=np.float64)
+        ctx.simulate_host(w.y0, 1.0 / ns, ns, (), N, w.seed, sl7.OUT_TERMINAL, opts, ro, rs)
+        np.testing.assert_array_equal(o, ro)
+        assert s_[0] == rs[0] == N and np.array_equal(s_[8:], rs[8:])
+        np.testing.assert_allclose(s_[2:6], rs[2:6], rtol=1e-12)
