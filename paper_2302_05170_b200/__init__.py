@@ -217,6 +217,14 @@ def normals(seed, path_offset, n_paths, n_steps, out, stream=None, flags=0):
     return out
 
 
+_LIVE = None   # weak set of open contexts, closed at interpreter exit (before the CUDA runtime is torn down)
+
+
+def _close_all():
+    for c in list(_LIVE or ()):
+        c.close()
+
+
 class Context:
     """Owns one sl7_ctx (one device)."""
 
@@ -231,6 +239,13 @@ class Context:
         _check(L.sl7_create(m, arr if dims else None, len(dims), act, self.device, ctypes.byref(h)))
         self._h = h
         self.layer_dims = dims
+        global _LIVE
+        if _LIVE is None:
+            import atexit
+            import weakref
+            _LIVE = weakref.WeakSet()
+            atexit.register(_close_all)
+        _LIVE.add(self)
 
     def close(self):
         h = getattr(self, "_h", None)

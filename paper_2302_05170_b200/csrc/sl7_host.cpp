@@ -1204,6 +1204,11 @@ sl7_status sl7_normals(uint64_t seed, uint64_t off, uint64_t n, int32_t n_steps,
 
 void sl7_destroy(sl7_ctx c) {
   if (!c) return;
+  int dev = -1;
+  if (cudaGetDevice(&dev) == cudaErrorCudartUnloading) {   // process exit: the runtime is gone, so is the memory
+    delete c;
+    return;
+  }
   {
     DeviceGuard g(c->device);
     if (c->d_wf32) cudaFree(c->d_wf32);
