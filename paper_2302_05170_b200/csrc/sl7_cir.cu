@@ -63,17 +63,19 @@ __device__ double gamma_p(double a, double y, double lg_a1) {
   return 1.0 - exp(lpre + log(a)) * h;
 }
 
-// F(x) and dF/dx of the noncentral chi-square
-__device__ void ncx2_cdf_pdf(const Ncx2& n, double x, double& F, double& f) {
+// F(x), dF/dx and d2F/dx2 of the noncentral chi-square (the density of term k is w_k G(a_k) a_k / (2y) with
+// a_k = d/2 + k; its derivative multiplies it by (a_k - 1)/x - 1/2)
+__device__ void ncx2_cdf_pdf(const Ncx2& n, double x, double& F, double& f, double& df) {
   const double y = 0.5 * x;
   if (!(y > 0.0)) {
     F = 0.0;
     f = 0.0;
+    df = 0.0;
     return;
   }
   const double P = gamma_p(n.a_m, y, n.lg_m);
   const double G = exp(n.a_m * log(y) - y - n.lg_m);
-  double Fs = n.w_m * P, fs = n.w_m * G * n.a_m;   // density term: w y^{a-1} e^{-y} / Gamma(a) = w G a / y
+  double Fs = n.w_m * P, fs = n.w_m * G * n.a_m, fs2 = fs * (n.a_m - 1.0);
   {
     double Pk = P, Gk = G, wk = n.w_m, ak = n.a_m;
     for (int k = n.k_m + 1; k < n.k_m + 100000; ++k) {
@@ -82,8 +84,10 @@ __device__ void ncx2_cdf_pdf(const Ncx2& n, double x, double& F, double& f) {
       ak += 1.0;
       wk *= n.mu / (double)k;
       Fs += wk * Pk;
-      fs += wk * Gk * ak;
-      if (wk < 1e-18) break;
+      const double t = wk * Gk * ak;
+      fs += t;
+      fs2 = fma(t, ak - 1.0, fs2);
+      if (wk < 1e-17) break;
     }
   }
   {
@@ -94,31 +98,39 @@ __device__ void ncx2_cdf_pdf(const Ncx2& n, double x, double& F, double& f) {
       Pk += Gk;
       wk *= (double)(k + 1) / n.mu;
       Fs += wk * Pk;
-      fs += wk * Gk * ak;
-      if (wk < 1e-18) break;
+      const double t = wk * Gk * ak;
+      fs += t;
+      fs2 = fma(t, ak - 1.0, fs2);
+      if (wk < 1e-17) break;
     }
   }
   F = Fs;
   f = 0.5 * fs / y;
+  df = (0.5 / y) * (fs2 / x - 0.5 * fs);
 }
 
-// F^{-1}(p) with z = Phi^{-1}(p) for the starting point; lo: a known lower bracket (F(lo) <= p)
+// F^{-1}(p) with z = Phi^{-1}(p) for the starting point (Sankaran's normal approximation of a power of the
+// noncentral chi-square, a few 1e-3 relative), then bracketed Halley steps (cubic convergence: two or
+// three evaluations); lo: a known lower bracket (F(lo) <= p)
 __device__ double ncx2_quantile(const Ncx2& n, double p, double z, double d, double lam, double lo) {
-  const double h = d + lam, r = d + 2.0 * lam;
-  const double nu = h * h / r, rho = r / h, t = 2.0 / (9.0 * nu);
-  double w = 1.0 - t + z * sqrt(t);
-  w = fmax(w, 0.05);
-  double x = fmax(rho * nu * w * w * w, lo);
+  const double s1 = d + lam, s2 = d + 2.0 * lam, s3 = d + 3.0 * lam;
+  const double h = 1.0 - (2.0 / 3.0) * s1 * s3 / (s2 * s2);
+  const double pp = s2 / (s1 * s1), mm = (h - 1.0) * (1.0 - 3.0 * h);
+  const double mu = 1.0 + h * pp * (h - 1.0 - 0.5 * (2.0 - h) * mm * pp);
+  const double sd = h * sqrt(2.0 * pp * (1.0 + 0.5 * mm * pp));
+  const double base = fmax(mu + sd * z, 1e-3);
+  double x = fmax(s1 * pow(base, 1.0 / h), lo);
   double hi = CUDART_INF;
   for (int it = 0; it < 100; ++it) {
-    double F, f;
-    ncx2_cdf_pdf(n, x, F, f);
+    double F, f, df;
+    ncx2_cdf_pdf(n, x, F, f, df);
     const double g = F - p;
     if (g < 0.0) lo = x; else hi = x;
     if (g == 0.0) break;
-    double xn = x - g / f;
+    const double den = 2.0 * f * f - g * df;
+    double xn = (den > 0.0) ? x - 2.0 * g * f / den : x - g / f;   // Halley, Newton if the curvature term misbehaves
     if (!(f > 0.0) || !(xn > lo && xn < hi)) xn = (hi < CUDART_INF) ? 0.5 * (lo + hi) : 2.0 * x + 1.0;
-    const bool done = fabs(xn - x) <= 1e-14 * xn;
+    const bool done = fabs(xn - x) <= 1e-13 * xn;
     x = xn;
     if (done) break;
   }
