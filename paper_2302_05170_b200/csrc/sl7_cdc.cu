@@ -33,7 +33,8 @@ struct CdcScratch {
   unsigned long long M;                     // number of finite states
   double frac[kMaxM];                       // interpolation weight of the upper order statistic
   // the table the step kernel consumes
-  float z[kMaxM], v[kMaxM], C[kMaxM][kMaxM];
+  float z[kMaxM], zlo[kMaxM], v[kMaxM], C[kMaxM][kMaxM];   // z + zlo = the double marginal point
+  float sinv;   // 1 / half-range of the z_k: the interpolation works on (Y - z_k) * sinv (no fp32 under/overflow)
   int degenerate;
   double zd[kMaxM];
 };
@@ -200,11 +201,23 @@ __global__ void __launch_bounds__(1024) cdc_scan_kernel(int pass, int m, CdcScra
   __syncthreads();
   if (threadIdx.x == 0) {
     if (pass < 3) {
-      // distinct prefixes (targets are ordered by rank, so prefixes are non-decreasing)
+      // distinct prefixes, ascending.  The targets are NOT always in rank order: levels clamped to the
+      // extreme order statistics repeat the pair (0, 1) (or (M-2, M-1)), e.g. 0, 1, 0, 1, ...
       int ns = 0;
       for (int t = 0; t < T; ++t) {
-        if (ns == 0 || s->slot_prefix[ns - 1] != s->prefix[t]) s->slot_prefix[ns++] = s->prefix[t];
-        s->slot_of[t] = ns - 1;
+        const uint32_t v = s->prefix[t];
+        int a = 0;
+        while (a < ns && s->slot_prefix[a] < v) ++a;
+        if (a == ns || s->slot_prefix[a] != v) {
+          for (int b = ns; b > a; --b) s->slot_prefix[b] = s->slot_prefix[b - 1];
+          s->slot_prefix[a] = v;
+          ++ns;
+        }
+      }
+      for (int t = 0; t < T; ++t) {
+        int a = 0;
+        while (s->slot_prefix[a] != s->prefix[t]) ++a;
+        s->slot_of[t] = a;
       }
       s->nslot = ns;
     } else {
@@ -220,11 +233,16 @@ __global__ void __launch_bounds__(1024) cdc_scan_kernel(int pass, int m, CdcScra
       s->degenerate = degen;
       for (int k = 0; k < m; ++k) {
         s->z[k] = (float)s->zd[k];
+        s->zlo[k] = (float)(s->zd[k] - (double)s->z[k]);
+        // barycentric weights of the nodes scaled to O(1) spacing: the normalised formula is invariant to a
+        // common scale of all (Y - z_k), and for m up to 16 nodes the unscaled products under/overflow fp32
+        const double sc = (!degen && m > 1) ? 0.5 * (s->zd[m - 1] - s->zd[0]) : 1.0;
         double w = 1.0;
         if (!degen)
           for (int l = 0; l < m; ++l)
-            if (l != k) w *= (s->zd[k] - s->zd[l]);
+            if (l != k) w *= (s->zd[k] - s->zd[l]) / sc;
         s->v[k] = degen ? 0.0f : (float)(1.0 / w);
+        if (k == 0) s->sinv = (float)(1.0 / sc);
       }
     }
   }
@@ -292,7 +310,7 @@ __global__ void __launch_bounds__(256) cdc_step_kernel(const __grid_constant__ R
                                                        int step, int last, unsigned long long* next_hist) {
   extern __shared__ uint32_t hist[];
   __shared__ double red[8];
-  __shared__ float sz[kMaxM], sv[kMaxM], sC[kMaxM][kMaxM];
+  __shared__ float sz[kMaxM], szlo[kMaxM], sv[kMaxM], sC[kMaxM][kMaxM], ssinv;
   __shared__ int sdeg;
   __shared__ uint32_t nh[256];   // pass-0 digit histogram of the new states (next step's selection)
   if (next_hist)
@@ -304,6 +322,8 @@ __global__ void __launch_bounds__(256) cdc_step_kernel(const __grid_constant__ R
   if (threadIdx.x < kMaxM) {
     sz[threadIdx.x] = (threadIdx.x < p.m) ? s->z[threadIdx.x] : 0.0f;
     sv[threadIdx.x] = (threadIdx.x < p.m) ? s->v[threadIdx.x] : 0.0f;
+    szlo[threadIdx.x] = (threadIdx.x < p.m) ? s->zlo[threadIdx.x] : 0.0f;
+    if (threadIdx.x == 0) ssinv = s->sinv;
   }
   if (threadIdx.x == 0) sdeg = s->degenerate;
   if (last) hist_init(p, hist);
@@ -346,7 +366,8 @@ __global__ void __launch_bounds__(256) cdc_step_kernel(const __grid_constant__ R
       // Lagrange basis in the state on the marginal nodes (normalised barycentric product form)
       float d[MR], pre[MR];
 #pragma unroll
-      for (int k = 0; k < MR; ++k) d[k] = (RT_M && k >= m) ? 1.0f : (Y - sz[k]);
+      // Y - z_k with the marginal point carried as z + zlo (double-accurate nodes, as the GH grid's hi/lo)
+      for (int k = 0; k < MR; ++k) d[k] = (RT_M && k >= m) ? 1.0f : ((Y - sz[k]) - szlo[k]) * ssinv;
       pre[0] = 1.0f;
 #pragma unroll
       for (int k = 1; k < MR; ++k) pre[k] = pre[k - 1] * d[k - 1];

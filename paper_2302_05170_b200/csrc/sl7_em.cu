@@ -225,11 +225,23 @@ __global__ void __launch_bounds__(1024) row_quantiles_kernel(const float* __rest
     }
     __syncthreads();
     if (tid == 0 && pass < 3) {
-      // targets are ordered by rank, so their prefixes are non-decreasing
+      // distinct prefixes, ascending (levels clamped to the extreme order statistics repeat rank pairs out
+      // of order, e.g. 0, 1, 0, 1, ...)
       int n = 0;
       for (int t = 0; t < T; ++t) {
-        if (n == 0 || sp[n - 1] != pre[t]) sp[n++] = pre[t];
-        slot_of[t] = n - 1;
+        const uint32_t v = pre[t];
+        int a = 0;
+        while (a < n && sp[a] < v) ++a;
+        if (a == n || sp[a] != v) {
+          for (int b = n; b > a; --b) sp[b] = sp[b - 1];
+          sp[a] = v;
+          ++n;
+        }
+      }
+      for (int t = 0; t < T; ++t) {
+        int a = 0;
+        while (sp[a] != pre[t]) ++a;
+        slot_of[t] = a;
       }
       nslot = n;
     }

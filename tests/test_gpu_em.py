@@ -230,3 +230,21 @@ def test_training_set_chunked_scratch_equals_caller_buffer(gpu_lib):
         lv = O.normal_cdf(O.gauss_hermite_nodes(5))
         Q = O.quantiles(T, lv)
         np.testing.assert_allclose(a[r].cpu().numpy(), Q, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("m,M", [(16, 16), (16, 40), (11, 25), (7, 7)])
+def test_training_set_clamped_levels(gpu_lib, m, M):
+    """Few inner paths for many levels: several levels clamp to the extreme order statistics, so the
+    selection targets repeat rank pairs out of order (0, 1, 0, 1, ...); labels still equal the quantiles of
+    the device's terminal values."""
+    sl7 = gpu_lib
+    torch = _torch()
+    F = sample_features("ou", 5, seed=9, dt_range=(0.05, 0.2))
+    ctx = sl7.Context(m)
+    term = torch.empty((5, M), dtype=torch.float32, device="cuda")
+    _, lab = ctx.training_set(sl7.MODEL_OU, F, M, 0.05, 3, sl7.make_opts(), terminal=term)
+    torch.cuda.synchronize()
+    T, L = term.double().cpu().numpy(), lab.cpu().numpy()
+    lv = O.normal_cdf(O.gauss_hermite_nodes(m))
+    for r in range(5):
+        np.testing.assert_allclose(L[r], O.quantiles(T[r], lv), rtol=1e-12, atol=1e-12)

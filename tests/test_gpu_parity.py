@@ -489,3 +489,46 @@ def test_multistep_ann_affine_network_free_running(gpu_lib, prec):
     for i in range(n):
         Y = a32 * Y + O.lagrange_eval(Z[i], x, np.broadcast_to(c32, (N, m)))
         assert np.abs(Yd[i + 1] - Y).max() <= 5e-6 * (i + 1), (i, np.abs(Yd[i + 1] - Y).max())
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 16])
+@pytest.mark.parametrize("kind", ["exact", "fp32", "bf16", "tf32", "split", "cdc"])
+def test_edge_node_counts(gpu_lib, m, kind):
+    """m = 1 (g_m is the constant y_0: the conditional median, no randomness), m = 2, 3, and the largest
+    grid m = 16 (a 64-wide network, runtime-m kernels) for every kernel family, teacher-forced."""
+    sl7 = gpu_lib
+    n_paths, n_steps, dt = 3 * 128 + 5, 3, 0.25
+    if kind == "exact":
+        ctx = sl7.Context(m)
+        colloc, prec, theta, quant, oc = sl7.COLLOC_EXACT_GBM, sl7.PREC_FP32, (0.05, 0.2), None, "gbm"
+        spec = O.Spec(m, "gbm", theta, 1.0, dt, n_steps)
+    else:
+        dims = [4, 64, 64, m]
+        p = glorot_mlp(dims, ACT_TANH, seed=5, with_norm=True)
+        blob = pack_blob(p)
+        ctx = sl7.Context(m, dims, ACT_TANH)
+        ctx.load_weights(blob)
+        theta = (0.3, 0.5)
+        prec = {"fp32": sl7.PREC_FP32, "bf16": sl7.PREC_BF16, "tf32": sl7.PREC_TF32, "split": sl7.PREC_SPLIT,
+                "cdc": sl7.PREC_FP32}[kind]
+        quant = kind if kind in ("bf16", "tf32") else None
+        colloc = sl7.COLLOC_ANN
+        spec = O.Spec(m, "ann", theta, 1.0, dt, n_steps, net=O.parse_blob(blob), quant=quant)
+    scheme = sl7.SCHEME_CDC if kind == "cdc" else sl7.SCHEME_7L
+    torch = _torch()
+    opts = sl7.make_opts(prec=prec, colloc=colloc, scheme=scheme)
+    out, _ = ctx.simulate(1.0, dt, n_steps, theta, n_paths, 13, sl7.OUT_FULL, opts)
+    torch.cuda.synchronize()
+    Yd = out.double().cpu().numpy().reshape(n_steps + 1, n_paths)
+    Z = O.normals(13, np.arange(n_paths, dtype=np.uint64), n_steps)
+    tol = 5e-3 if quant else 1e-5
+    for i in range(n_steps):
+        if kind == "cdc":
+            ref, kap = O.cdc_step(spec, Yd[i], Z[i]), O.cdc_step_error_scale(spec, Yd[i], Z[i])
+        else:
+            ref, kap = O.step(spec, Yd[i], Z[i]), O.step_error_scale(spec, Yd[i], Z[i])
+        r = np.abs(Yd[i + 1] - ref) / kap
+        assert r.max() <= tol, (kind, m, i, float(r.max()))
+    if m == 1 and kind == "exact":   # no randomness: Y0 c_0^i with c_0 = exp((mu - s^2/2) dt)
+        c0 = np.float32(np.exp((0.05 - 0.02) * dt))
+        assert np.all(np.abs(Yd[-1] - float(c0) ** n_steps) <= 1e-6)
