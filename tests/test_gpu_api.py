@@ -192,3 +192,25 @@ def test_host_async_pipeline_equals_sync_calls(gpu_lib):
         np.testing.assert_array_equal(o, ro)
         assert s_[0] == rs[0] == N and np.array_equal(s_[8:], rs[8:])
         np.testing.assert_allclose(s_[2:6], rs[2:6], rtol=1e-12)
+
+
+def test_nonfinite_paths_are_counted_not_summed(gpu_lib):
+    """Paths that overflow (GBM with an absurd volatility) are counted in n_nonfinite and left out of the
+    sums and the histogram; the host summary then reports SL7_ENONFINITE."""
+    sl7 = gpu_lib
+    torch = _torch()
+    ctx = sl7.Context(5)
+    N = 4096
+    st = torch.zeros(sl7.stats_elems(16), dtype=torch.float64, device="cuda")
+    opts = sl7.make_opts(colloc=sl7.COLLOC_EXACT_GBM, n_bins=16, hist_lo=0.0, hist_hi=10.0)
+    out, _ = ctx.simulate(1.0, 1.0, 47, (2.0, 0.5), N, 2, sl7.OUT_TERMINAL, opts, stats=st)   # log Y_T ~ N(88, 3.4^2)
+    torch.cuda.synchronize()
+    Y = out.double().cpu().numpy()
+    v = st.cpu().numpy()
+    fin = np.isfinite(Y)
+    assert 0 < (~fin).sum() < N
+    assert v[0] == fin.sum() and v[1] == (~fin).sum()
+    ref = O.stats_vector(Y, 0.0, 0.0, 10.0, 16)
+    np.testing.assert_array_equal(v[8:], ref[8:])
+    s = sl7.stats_summary(v, opts)
+    assert s["status"] == sl7.ENONFINITE and s["n_nonfinite"] == (~fin).sum()
