@@ -115,10 +115,11 @@ def main():
 
     # issue roofline of the RNG-bound kernels: thread-instructions/s = SMs x 4 schedulers x 32 lanes x clock;
     # instructions per fine path-step with the fast normals, counted in the SASS of em_rows_kernel's
-    # unrolled OU loop body: 156 per Philox block of 4 fine steps (Philox4x32-10 ~56, two fast
-    # Box-Muller pairs ~80, four Euler updates 12, loop 8) = 39.  frac is then the issue-slot utilisation.
+    # unrolled OU loop body: 108 per Philox block of 4 fine steps (Philox4x32-10 ~50, two fast
+    # Box-Muller pairs with MUFU lg2/sqrt/sin/cos ~40, four Euler updates 12, loop ~6) = 27.  frac is then
+    # the issue-slot utilisation.
     issue_peak = n_sms * 4 * 32 * sm_max * 1e6
-    em_instr = 39.0
+    em_instr = 27.0
 
     if a.config in ("em", "all"):
         from sl7_inputs import CIR_THETA, OU_THETA

@@ -125,8 +125,9 @@ typedef struct {
 } sl7_run_opts;
 
 /* opts->flags (exact-collocation modes and 7L-CDC (FAST_NORMALS only); ignored by the 7L ANN kernels):
- *  SL7_FLAG_FAST_NORMALS : Box-Muller with MUFU lg2 (exact series for u -> 1) and a polynomial sincos
- *                          reduced exactly in revolutions: ~3x fewer instructions, |X_hat - X| <= ~1e-6.
+ *  SL7_FLAG_FAST_NORMALS : Box-Muller with MUFU lg2 (exact series for u -> 1) and MUFU sin/cos on the
+ *                          angle reduced exactly to (-pi, pi): ~4x fewer instructions,
+ *                          |X_hat - X| <= 2e-6 (1 + |X|) (measured 1.1e-6).
  *  SL7_FLAG_SPECIALIZED  : evaluate g_m in closed form for the linear structure of the exact points:
  *                          GBM y_j = Y c_j  =>  g_m(Z) = Y Q(Z), Q the degree-(m-1) interpolant of c_j
  *                          in monomial form (Horner; m <= 8); OU y_j = mean + std x_j  =>  g_m(Z) =

@@ -70,31 +70,12 @@ __device__ __forceinline__ float lg2_fast(float x) {
   return r;
 }
 
-// Fast Box-Muller on the MUFU pipe (exact-collocation kernels, where the RNG dominates the cost).
-// -2 ln u: MUFU lg2 has ~2^-22 ABSOLUTE error (measured on B200: relative error 0.86 at u = 1 - 2^-24),
-// so for v = 1 - u < 2^-4 (v exact) the log is the series 2 (v + v^2/2 + v^3/3 + v^4/4 + v^5/5)
-// (truncation <= 1.6e-7 relative); elsewhere lg2 is relatively accurate to <= 3e-7.  The angle is
-// reduced exactly in revolutions: t = u - 1/2 (exact), quadrant q = rint(4t), f = t - q/4 in
-// [-1/8, 1/8] (exact), then minimax polynomials for sin(2 pi f) / cos(2 pi f) (abs. error <= 1e-7) and
-// a quadrant rotation; 2 pi u = 2 pi t + pi flips both signs.  |Z_fast - Z| <= ~3e-7 (1 + |Z|).
-__device__ __forceinline__ void sincos_2pi_rev(float t, float& s, float& c) {
-  const float magic = 12582912.0f;  // 1.5 * 2^23: adding it rounds to an integer in the low mantissa bits
-  const float qm = fmaf(t, 4.0f, magic);
-  const float qf = qm - magic;
-  const float f = fmaf(qf, -0.25f, t);
-  const float f2 = f * f;
-  const float sp = f * fmaf(fmaf(fmaf(-7.524006653e+01f, f2, 8.158812714e+01f), f2, -4.134162903e+01f), f2,
-                            6.283185005e+00f);
-  const float cp = fmaf(fmaf(fmaf(fmaf(5.922040939e+01f, f2, -8.544285583e+01f), f2, 6.493931580e+01f), f2,
-                             -1.973920822e+01f), f2, 1.0f);
-  const int j = __float_as_int(qm) & 3;
-  float S = (j & 1) ? cp : sp, C = (j & 1) ? sp : cp;
-  S = __int_as_float(__float_as_int(S) ^ (((j >> 1) & 1) << 31));
-  C = __int_as_float(__float_as_int(C) ^ ((((j + 1) >> 1) & 1) << 31));
-  s = S;
-  c = C;
-}
-
+// Fast Box-Muller on the MUFU pipe (exact-collocation, EM and CDC kernels under SL7_FLAG_FAST_NORMALS,
+// where the RNG dominates the cost).  -2 ln u: MUFU lg2 has ~2^-22 ABSOLUTE error (measured on B200:
+// relative error 0.86 at u = 1 - 2^-24), so for v = 1 - u < 2^-4 (v exact) the log is the series
+// 2 (v + v^2/2 + v^3/3 + v^4/4 + v^5/5) (truncation <= 1.6e-7 relative); elsewhere lg2 is relatively
+// accurate to <= 3e-7.  The angle: 2 pi u = 2 pi (u - 1/2) + pi with u - 1/2 exact, so MUFU sin/cos see
+// (-pi, pi) (4e-7 absolute there) and the + pi flips both signs.  |Z_fast - Z| <= 2e-6 (1 + |Z|).
 __device__ __forceinline__ void box_muller_fast(uint32_t ra, uint32_t rb, float& za, float& zb) {
   const float ua = u32_to_unit(ra), ub = u32_to_unit(rb);
   const float v = 1.0f - ua;
@@ -103,8 +84,12 @@ __device__ __forceinline__ void box_muller_fast(uint32_t ra, uint32_t rb, float&
   const float t = (v < 0.0625f) ? ser : lg;
   float rad;
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(rad) : "f"(t));
+  // angle 2 pi u = 2 pi (u - 1/2) + pi: the reduced argument lies in (-pi, pi), where MUFU sin/cos are
+  // accurate to 4e-7 absolute (measured, profiles/r01_pipes.md); the + pi flips both signs
+  const float a = (ub - 0.5f) * 6.2831853071795865f;
   float s, c;
-  sincos_2pi_rev(ub - 0.5f, s, c);
+  asm("sin.approx.f32 %0, %1;" : "=f"(s) : "f"(a));
+  asm("cos.approx.f32 %0, %1;" : "=f"(c) : "f"(a));
   za = -rad * c;
   zb = -rad * s;
 }
