@@ -156,6 +156,7 @@ ANN_CASES = [
     ("cfg2_cir", None),
     ("glorot_generic", ((4, 17, 9, 33, 6), ACT_TANH)),
     ("glorot_generic_sp", ((3, 64, 64, 3), ACT_SOFTPLUS)),
+    ("glorot_max_shape", ((2, 64, 64, 64, 64, 64, 64, 16), ACT_TANH)),   # 6 hidden layers, width 64, m = 16
 ]
 
 
