@@ -71,7 +71,8 @@ typedef enum { SL7_OUT_FULL = 0, SL7_OUT_TERMINAL = 1, SL7_OUT_STATS = 2 } sl7_o
 /* Arithmetic of the ANN contractions (hidden layers 2..L and the output layer).
  *  FP32:  CUDA-core fp32 FFMA, accurate activations ("exact mode").
  *  BF16:  tcgen05 tensor cores, operands rounded to bf16 (RNE), fp32 accumulate, fp32 bias and
- *         activations; reproduces the quantisation-aware oracle O6.
+ *         activations (tanh on MUFU.TANH, <= 1e-5 relative); reproduces the quantisation-aware oracle O6
+ *         (DESIGN.md).  BF16 and TF32 draw X_hat with the fast Box-Muller of SL7_FLAG_FAST_NORMALS.
  *  TF32:  tcgen05 kind::tf32 (K = 8 per instruction), operands rounded with cvt.rna (ties away, 11
  *         significant bits), fp32 accumulate; reproduces O6 with TF32 rounding.
  *  SPLIT: tcgen05 with every operand split into three bf16 parts (a = a0 + a1 + a2, same for W) and

@@ -306,7 +306,9 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
     ref_init(rs, p);
     float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
     for (int i = 0; i < p.n_steps; ++i) {
-      if ((i & 3) == 0) normals4(p.key0, p.key1, gp, (uint32_t)(i >> 2), z0, z1, z2, z3);
+      // BF16 / TF32 draw X_hat with the fast Box-Muller (|dX| <= 2e-6 (1 + |X|), far below the operand
+      // rounding of these modes); SPLIT (fp32-class) keeps the libm one
+      if ((i & 3) == 0) normals4_rk<(NP == 1)>(p, gp, (uint32_t)(i >> 2), z0, z1, z2, z3);
       const float Z = z0;
       z0 = z1; z1 = z2; z2 = z3;
 
