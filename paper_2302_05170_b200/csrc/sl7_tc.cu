@@ -41,33 +41,15 @@ __device__ __forceinline__ float rcp12_newton(float s) {
   return r;
 }
 
-// Internal activation code of the TC kernel: tanh on the MUFU.TANH unit (tanh.approx.f32, max. relative
-// error ~2^-11, below the bf16 rounding of the activation that follows), argument unscaled (act_scale 1).
+// Internal activation code of the TC kernel: tanh on the MUFU.TANH unit (tanh.approx.f32; measured on
+// B200 at <= 9.9e-6 relative, 7.9e-6 absolute, far below the bf16 / tf32 rounding of the activation that
+// follows), argument unscaled (act_scale 1).  The default tanh epilogue of the BF16 / TF32 modes.
 constexpr int kActTanhX = 2;
-// softplus with one MUFU op per unit: e^{-|z|} on MUFU.EX2, log1p(e) by a minimax polynomial on the FMA pipe
-// (degree 8, abs. error 1.4e-7 on [0, 1]; degree 6 (1.3e-6) for the NMASK units).  A degree-5 polynomial
-// (8.8e-6) biased the terminal mean of cfg2 by 2e-3 relative (all 200 units err with the same sign).
-constexpr int kActSoftplusX = 3;
-
 __device__ __forceinline__ float tanh_mufu(float z) {
   float r;
   asm("tanh.approx.f32 %0, %1;" : "=f"(r) : "f"(z));
   return r;
 }
-
-// 2^v for v <= 0 on the FMA/ALU pipes: v = n + f (n = rint(v) by the 1.5 * 2^23 trick, f in [-1/2, 1/2]),
-// 2^f by its degree-4 Taylor polynomial (relative error <= 4.2e-5), 2^n added into the exponent field.
-__device__ __forceinline__ float exp2_fma(float v) {
-  v = fmaxf(v, -126.0f);
-  const float t = v + 12582912.0f;
-  const float f = v - (t - 12582912.0f);
-  const float p = fmaf(fmaf(fmaf(fmaf(9.6181291e-3f, f, 5.5504109e-2f), f, 2.4022651e-1f), f, 6.9314718e-1f), f, 1.0f);
-  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
-}
-
-// tanh with no MUFU op: tanh|z| = (1 - e) / (1 + e), e = 2^(-2 log2(e) |z|) from exp2_fma, the reciprocal of
-// 1 + e in [1, 2] by rcp12_newton.  Absolute error <= ~1e-4 (2^-13).
-__device__ __forceinline__ float tanh_fma(float z);
 
 // Activation of the TC epilogue.  The argument is u = z * scale with scale = 2 log2(e) (tanh) or 1
 // (softplus), folded on the host into layer 1 and into the biases.
@@ -76,39 +58,10 @@ __device__ __forceinline__ float tanh_fma(float z);
 //                      so its reciprocal is rcp12_newton on the FMA pipe; sign restored by copysign
 //   softplus, 2 MUFU:  max(z, 0) + ln2 log2(1 + 2^(-|z| log2 e))
 // Absolute error <= ~2e-7 in every variant.
-__device__ __forceinline__ float tanh_fma(float z) {
-  const float e = exp2_fma(fabsf(z) * -2.8853900817779268f);
-  const float r = rcp12_newton(1.0f + e);
-  return copysignf(fmaf(-e, r, r), z);
-}
-
 template <int ACT>
 __device__ __forceinline__ float tc_act_u(float u, bool newton) {
   if constexpr (ACT == kActTanhX) {
-    return newton ? tanh_fma(u) : tanh_mufu(u);
-  } else if constexpr (ACT == kActSoftplusX) {
-    const float e = ex2_approx(fabsf(u) * -1.4426950408889634f);
-    float lp;
-    if (newton) {   // degree 6: abs. error 1.3e-6
-      lp = -1.7807194e-02f;
-      lp = fmaf(lp, e, 8.3869926e-02f);
-      lp = fmaf(lp, e, -1.9167948e-01f);
-      lp = fmaf(lp, e, 3.1643384e-01f);
-      lp = fmaf(lp, e, -4.9753391e-01f);
-      lp = fmaf(lp, e, 9.9986143e-01f);
-      lp = fmaf(lp, e, 1.2839006e-06f);
-    } else {        // degree 8: abs. error 1.4e-7
-      lp = -6.301349960e-03f;
-      lp = fmaf(lp, e, 3.544928879e-02f);
-      lp = fmaf(lp, e, -9.422647208e-02f);
-      lp = fmaf(lp, e, 1.666473895e-01f);
-      lp = fmaf(lp, e, -2.402127683e-01f);
-      lp = fmaf(lp, e, 3.316470385e-01f);
-      lp = fmaf(lp, e, -4.998508692e-01f);
-      lp = fmaf(lp, e, 9.999948740e-01f);
-      lp = fmaf(lp, e, 2.928694798e-08f);
-    }
-    return fmaxf(u, 0.0f) + lp;
+    return tanh_mufu(u);
   } else if constexpr (ACT == SL7_ACT_TANH) {
     if (newton) {   // compile-time after unrolling
       const float e = ex2_approx(-fabsf(u));
@@ -170,7 +123,7 @@ __device__ __forceinline__ void act_pack_32(const uint32_t (&v)[32], int col0, f
       const int c = col0 + 2 * k + q;
       if (c < H) {
         const float acc = __uint_as_float(v[2 * k + q]);
-        const float u = FOLD ? ((ACT == kActTanhX || ACT == kActSoftplusX) ? acc : acc * scale) : fmaf(acc, scale, bs[c]);
+        const float u = FOLD ? (ACT == kActTanhX ? acc : acc * scale) : fmaf(acc, scale, bs[c]);
         h[q] = tc_act_u<ACT>(u, use_newton<ACT, NMASK>(c));
       } else {
         h[q] = (FOLD && c < H + 3) ? 1.0f : 0.0f;
@@ -197,7 +150,7 @@ __device__ __forceinline__ void act_tf32_32(const uint32_t (&v)[32], int col0, f
     float h;
     if (c < H) {
       const float acc = __uint_as_float(v[k]);
-      const float u = FOLD ? ((ACT == kActTanhX || ACT == kActSoftplusX) ? acc : acc * scale) : fmaf(acc, scale, bs[c]);
+      const float u = FOLD ? (ACT == kActTanhX ? acc : acc * scale) : fmaf(acc, scale, bs[c]);
       h = tc_act_u<ACT>(u, use_newton<ACT, NMASK>(c));
     } else {
       h = (FOLD && c < H + 3) ? 1.0f : 0.0f;
@@ -523,26 +476,7 @@ int launch_tc_kernel(const RunParams& p, const TcParams& t, void* stream, int nu
   if (t.tf32)
     return (int)(p.act == SL7_ACT_TANH ? launch_tc_tf32<kActTanhX, 0x00u>(p, t, st, num_sms)
                                        : launch_tc_tf32<SL7_ACT_SOFTPLUS, kSoftplusPolyMask>(p, t, st, num_sms));
-  if (p.act == SL7_ACT_SOFTPLUS && !t.split && t.variant >= 30 && p.width == 50 && p.m == 7) {
-    switch (t.variant) {   // A/B hooks: one-MUFU softplus, group count, FMA-pipe share
-      case 30: return (int)launch_tc_t<5, 50, 7, false, kActSoftplusX, 0x00u>(p, t, st, num_sms);
-      case 32: return (int)launch_tc_t<5, 50, 7, false, kActSoftplusX, 0xFFu>(p, t, st, num_sms);
-      case 34: return (int)launch_tc_t<5, 50, 7, false, SL7_ACT_SOFTPLUS, 0x77u>(p, t, st, num_sms);
-      case 35: return (int)launch_tc_t<4, 50, 7, false, SL7_ACT_SOFTPLUS, 0x55u>(p, t, st, num_sms);
-      default: break;
-    }
-  }
   if (p.act == SL7_ACT_TANH && t.tanh_mufu) {
-    if (p.width == 50 && p.m == 7 && !t.split) {
-      switch (t.variant) {   // A/B hook: units on the FMA-pipe tanh (mask over unit % 8)
-        case 21: return (int)launch_tc_t<kTcGroups, 50, 7, false, kActTanhX, 0x01u>(p, t, st, num_sms);
-        case 22: return (int)launch_tc_t<kTcGroups, 50, 7, false, kActTanhX, 0x11u>(p, t, st, num_sms);
-        case 23: return (int)launch_tc_t<kTcGroups, 50, 7, false, kActTanhX, 0x25u>(p, t, st, num_sms);
-        case 24: return (int)launch_tc_t<kTcGroups, 50, 7, false, kActTanhX, 0x55u>(p, t, st, num_sms);
-        case 25: return (int)launch_tc_t<4, 50, 7, false, kActTanhX, 0x00u>(p, t, st, num_sms);
-        default: break;
-      }
-    }
     return (int)launch_tc_act_x(p, t, st, num_sms);
   }
   return (int)(p.act == SL7_ACT_TANH ? launch_tc_act<SL7_ACT_TANH>(p, t, st, num_sms)
