@@ -131,3 +131,21 @@ def test_stats_quantile_outside_range_is_nan(lib):
     s = sl7.stats_summary(v, _opts(10, -0.5, 0.5, 0.0), q_levels=[0.1, 0.5, 0.9])
     assert math.isnan(s["quantiles"][0]) and math.isnan(s["quantiles"][2])
     assert abs(s["quantiles"][1]) <= 0.1
+
+
+def test_product_package_never_imports_the_oracle():
+    """The product path (paper_2302_05170_b200 and its C library) has no route to oracle/: importing the
+    package and its modules in a fresh interpreter loads no oracle module, and no product source names it."""
+    import subprocess
+    import sys
+    code = ("import sys, paper_2302_05170_b200, paper_2302_05170_b200.dist, paper_2302_05170_b200.build; "
+            "print(any(m == 'oracle' or m.startswith('oracle.') for m in sys.modules))")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT, timeout=120)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.strip() == "False"
+    pkg = os.path.join(ROOT, "paper_2302_05170_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
+                src = open(os.path.join(dirpath, f), encoding="utf-8", errors="replace").read()
+                assert "import oracle" not in src and "from oracle" not in src and "sl7_oracle" not in src, f
