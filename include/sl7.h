@@ -164,9 +164,11 @@ sl7_status sl7_create(int32_t m, const int32_t* layer_dims, int32_t n_dims, sl7_
 /* Load the trained network (Algorithm I step 1 output) from a blob; copied, so the
  * caller may free it on return.  Little-endian "SL7W" container:
  *   char magic[4] = "SL7W"; u32 version = 1; u32 n_dims; u32 dims[n_dims]; u32 act; u32 flags
- *   (bit0 has_norm); then per layer l: f32 W[out][in] (row-major), f32 b[out];
- *   if has_norm: f32 in_shift[d_in], in_scale[d_in], out_shift[m], out_scale[m]
- *   (network sees (f - in_shift)/in_scale; prediction is out * out_scale + out_shift).
+ *   (bit0 has_norm, bit1 residual; other bits rejected); then per layer l: f32 W[out][in] (row-major),
+ *   f32 b[out]; if has_norm: f32 in_shift[d_in], in_scale[d_in], out_shift[m], out_scale[m]
+ *   (network sees (f - in_shift)/in_scale; prediction is out * out_scale + out_shift, or out without
+ *   has_norm).  residual (reading R-11 in DESIGN.md): y_j = Y + sqrt(dt) * prediction_j, so the
+ *   network carries only the step's spread and bf16 / tf32 rounding no longer scales with |Y|.
  * The size must match exactly.  dims/act must equal the context's.  Errors: SL7_EFORMAT. */
 sl7_status sl7_load_weights(sl7_ctx ctx, const void* blob, size_t nbytes);
 

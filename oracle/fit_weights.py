@@ -4,12 +4,13 @@ TEST INFRASTRUCTURE ONLY.  No trained checkpoint exists offline (BASELINE north_
 committed script produces the frozen weight blobs under tests/golden/ that BOTH the oracle and the
 CUDA path consume as inputs.  Labels come only from oracle/sl7_oracle.py (GBM closed form, Eq. 6.6
 for OU, the noncentral-chi^2 law for CIR); the optimiser follows PAPER.md:85 ("Glorot
-initialization, the Adam optimizer, a batch size of 1024, and a learning rate of 10^-3") with
-input/output standardisation stored in the blob (reading R-11).  Fit quality is REPORTED in
+initialization, the Adam optimizer, a batch size of 1024, and a learning rate of 10^-3", annealed to
+1e-6 over the time budget) with input/output standardisation stored in the blob and, by default, the residual output form
+H_hat_j = Y + sqrt(dt) (out_j out_scale_j + out_shift_j) (blob flags bit 1, reading R-11).  Fit quality is REPORTED in
 tests/golden/weights_manifest.json, never graded: the kernels are checked against the oracle
 running the *same* frozen weights.
 
-usage: python -m oracle.fit_weights [--seconds S] [--only NAME]
+usage: python -m oracle.fit_weights [--seconds S] [--only NAME] [--device cuda] [--absolute] [--out-dir D]
 """
 from __future__ import annotations
 
@@ -62,15 +63,19 @@ def make_dataset(kind, m, n, seed):
     raise ValueError(kind)
 
 
-def fit(kind, m, act, hidden, seconds, seed=WEIGHT_SEED, n=200_000):
+def fit(kind, m, act, hidden, seconds, seed=WEIGHT_SEED, n=200_000, device="cpu", residual=True):
+    import math
     import torch
     torch.manual_seed(seed)
     torch.set_num_threads(max(1, os.cpu_count() or 1))
     F, Yl = make_dataset(kind, m, n, seed)
+    # residual blobs (reading R-11) learn (y_j - Y) / sqrt(dt): the network then carries only the
+    # step's spread, whose size no longer depends on Y or dt, instead of re-deriving Y through its layers
+    T = (Yl - F[:, :1]) / np.sqrt(F[:, 1:2]) if residual else Yl
     in_shift, in_scale = F.mean(0), F.std(0) + 1e-12
-    out_shift, out_scale = Yl.mean(0), Yl.std(0) + 1e-12
-    Xn = torch.tensor((F - in_shift) / in_scale, dtype=torch.float32)
-    Yn = torch.tensor((Yl - out_shift) / out_scale, dtype=torch.float32)
+    out_shift, out_scale = T.mean(0), T.std(0) + 1e-12
+    Xn = torch.tensor((F - in_shift) / in_scale, dtype=torch.float32, device=device)
+    Yn = torch.tensor((T - out_shift) / out_scale, dtype=torch.float32, device=device)
     nval = n // 10
     Xv, Yv, Xt, Yt = Xn[:nval], Yn[:nval], Xn[nval:], Yn[nval:]
     dims = [F.shape[1]] + [50] * hidden + [m]
@@ -82,12 +87,17 @@ def fit(kind, m, act, hidden, seconds, seed=WEIGHT_SEED, n=200_000):
         layers.append(lin)
         if l < len(dims) - 2:
             layers.append(torch.nn.Tanh() if act == ACT_TANH else torch.nn.Softplus())
-    net = torch.nn.Sequential(*layers)
+    net = torch.nn.Sequential(*layers).to(device)
+    # Adam, batch 1024, lr 1e-3, then annealed (cosine, in wall time) to 1e-6: the 7L step
+    # error of a network is its collocation-point error, and small-dt steps accumulate it over many steps
     opt = torch.optim.Adam(net.parameters(), lr=1e-3)
     best, best_state, epoch = float("inf"), None, 0
     t0 = time.time()
     while time.time() - t0 < seconds:
-        perm = torch.randperm(Xt.shape[0])
+        frac = min(1.0, (time.time() - t0) / seconds)
+        for gr in opt.param_groups:
+            gr["lr"] = 1e-6 + 0.5 * (1e-3 - 1e-6) * (1.0 + math.cos(math.pi * frac))
+        perm = torch.randperm(Xt.shape[0], device=device)
         for s in range(0, Xt.shape[0], 1024):
             idx = perm[s:s + 1024]
             opt.zero_grad()
@@ -102,10 +112,11 @@ def fit(kind, m, act, hidden, seconds, seed=WEIGHT_SEED, n=200_000):
             best_state = {k: t.clone() for k, t in net.state_dict().items()}
     net.load_state_dict(best_state)
     lins = [l for l in net if isinstance(l, torch.nn.Linear)]
-    W = [l.weight.detach().double().numpy().astype(np.float32).astype(np.float64) for l in lins]
-    b = [l.bias.detach().double().numpy().astype(np.float32).astype(np.float64) for l in lins]
+    W = [l.weight.detach().double().cpu().numpy().astype(np.float32).astype(np.float64) for l in lins]
+    b = [l.bias.detach().double().cpu().numpy().astype(np.float32).astype(np.float64) for l in lins]
     f32 = lambda a: np.asarray(a).astype(np.float32).astype(np.float64)
-    p = MlpParams(tuple(dims), act, W, b, f32(in_shift), f32(in_scale), f32(out_shift), f32(out_scale))
+    p = MlpParams(tuple(dims), act, W, b, f32(in_shift), f32(in_scale), f32(out_shift), f32(out_scale),
+                  residual=residual)
     # report fit quality with the oracle's own forward pass on the held-out rows
     blob = pack_blob(p)
     onet = O.parse_blob(blob)
@@ -129,20 +140,25 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=120.0)
     ap.add_argument("--only", default=None)
+    ap.add_argument("--device", default="cpu", help="torch device for the optimiser (labels are the oracle's)")
+    ap.add_argument("--absolute", action="store_true", help="absolute-output blobs (no residual form)")
+    ap.add_argument("--out-dir", default=GOLDEN)
     a = ap.parse_args()
-    man_path = os.path.join(GOLDEN, "weights_manifest.json")
+    man_path = os.path.join(a.out_dir, "weights_manifest.json")
     manifest = json.load(open(man_path)) if os.path.exists(man_path) else {}
     for name, (kind, m, act, hidden) in NETS.items():
         if a.only and a.only != name:
             continue
         n = 60_000 if kind == "cir" else 200_000
-        blob, q = fit(kind, m, act, hidden, a.seconds, n=n)
-        with open(os.path.join(GOLDEN, name), "wb") as f:
+        blob, q = fit(kind, m, act, hidden, a.seconds, n=n, device=a.device, residual=not a.absolute)
+        with open(os.path.join(a.out_dir, name), "wb") as f:
             f.write(blob)
         manifest[name] = {"process": kind, "m": m, "act": "tanh" if act == ACT_TANH else "softplus",
                           "hidden": hidden, "sha256": hashlib.sha256(blob).hexdigest(),
-                          "fit_seconds": a.seconds, "seed": WEIGHT_SEED, "quality": q,
-                          "script": "python -m oracle.fit_weights"}
+                          "fit_seconds": a.seconds, "seed": WEIGHT_SEED, "quality": q, "device": a.device,
+                          "residual": not a.absolute,
+                          "script": "python -m oracle.fit_weights --seconds %g --device %s%s" % (
+                              a.seconds, a.device, " --absolute" if a.absolute else "")}
         print(name, q, flush=True)
         json.dump(manifest, open(man_path, "w"), indent=1, sort_keys=True)
 

@@ -245,8 +245,9 @@ def activation(z, act):
 class Mlp:
     """One network with m outputs (reading R-4).  W[l] is (out x in), row-major as in the blob."""
 
-    def __init__(self, dims, act, W, b, norm=None):
+    def __init__(self, dims, act, W, b, norm=None, residual=False):
         self.dims = tuple(int(d) for d in dims)
+        self.residual = bool(residual)
         self.act = int(act)
         self.W = [np.asarray(w, dtype=np.float64) for w in W]
         self.b = [np.asarray(v, dtype=np.float64) for v in b]
@@ -285,7 +286,7 @@ def parse_blob(blob: bytes) -> Mlp:
         norm = tuple(arrs)
     if off != len(blob):
         raise ValueError("size")
-    return Mlp(dims, act, W, b, norm)
+    return Mlp(dims, act, W, b, norm, residual=bool(flags & 2))
 
 
 # O6 rounding of MMA inputs (reading R-15).  bf16: 8 significant bits, round-to-nearest-even;
@@ -313,6 +314,7 @@ def mlp_forward(net: Mlp, F, quant: str | None = None) -> np.ndarray:
     quant='bf16'|'tf32' : O6 -- every input of layers 2..L+1 (the contractions the device runs on
     tensor cores: hidden activations and weights) is rounded to the device format before an exact
     product; layer 1 (rank-1 in Y after folding dt, theta) and all biases stay unrounded.
+    Residual blobs (flags bit 1, reading R-11): H_hat_j = Y + sqrt(dt) * (out * out_scale + out_shift).
     """
     F = np.asarray(F, dtype=np.float64)
     rnd = {None: (lambda a: a), "bf16": round_bf16, "tf32": round_tf32}[quant]
@@ -331,6 +333,8 @@ def mlp_forward(net: Mlp, F, quant: str | None = None) -> np.ndarray:
     if net.norm is not None:
         _, _, out_shift, out_scale = net.norm
         h = h * out_scale + out_shift
+    if net.residual:
+        h = F[..., 0:1] + np.sqrt(F[..., 1:2]) * h
     return h
 
 
@@ -350,6 +354,8 @@ def mlp_abs_scale(net: Mlp, F, quant: str | None = None) -> np.ndarray:
     A = np.abs(rnd(h)) @ np.abs(rnd(net.W[L])).T + np.abs(net.b[L])
     if net.norm is not None:
         A = A * np.abs(net.norm[3]) + np.abs(net.norm[2])
+    if net.residual:
+        A = np.abs(F[..., 0:1]) + np.sqrt(F[..., 1:2]) * A
     return A
 
 

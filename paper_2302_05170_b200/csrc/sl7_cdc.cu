@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(256) cdc_table_mlp_kernel(const __grid_constan
     const int k = i / m, j = i % m;
     float a = bo[j];
     for (int v = 0; v < H; ++v) a = fmaf(Wo[(size_t)j * HS + v], h[k][v], a);
-    s->C[k][j] = fmaf(a, p.out_scale[j], p.out_shift[j]);
+    s->C[k][j] = fmaf(p.res_y, s->z[k], fmaf(a, p.out_scale[j], p.out_shift[j]));
   }
 }
 

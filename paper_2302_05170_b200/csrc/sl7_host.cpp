@@ -40,6 +40,7 @@ struct sl7_ctx_s {
   bool has_net = false;
   std::vector<std::vector<float>> W, b;
   bool has_norm = false;
+  bool residual = false;          // blob flags bit 1: H_j = Y + sqrt(dt) (out_j out_scale_j + out_shift_j)
   std::vector<float> in_shift, in_scale, out_shift, out_scale;
   // device images
   int width = 0;           // hidden width used by the FP32 kernel (50 or 64 padded)
@@ -531,10 +532,14 @@ sl7_status prepare(sl7_ctx c, double Y0, double dt, int32_t n_steps, const doubl
         p.l1w_d[k] = (double)Wr[0] / sc[0];
         p.l1b_d[k] = bias;
       }
+      const double rs = c->residual ? std::sqrt(dt) : 1.0;
       for (int j = 0; j < kMaxM; ++j) {
-        p.out_scale[j] = (j < c->m && c->has_norm) ? c->out_scale[j] : (j < c->m ? 1.0f : 0.0f);
-        p.out_shift[j] = (j < c->m && c->has_norm) ? c->out_shift[j] : 0.0f;
+        const double sc_j = (j < c->m && c->has_norm) ? c->out_scale[j] : (j < c->m ? 1.0 : 0.0);
+        const double sh_j = (j < c->m && c->has_norm) ? c->out_shift[j] : 0.0;
+        p.out_scale[j] = (float)(rs * sc_j);
+        p.out_shift[j] = (float)(rs * sh_j);
       }
+      p.res_y = c->residual ? 1.0f : 0.0f;
       p.act = c->act;
       p.n_hidden = (int)c->dims.size() - 2;
       p.width = c->width;
@@ -777,6 +782,7 @@ sl7_status sl7_load_weights(sl7_ctx c, const void* blob, size_t nbytes) {
     std::memcpy(b.back().data(), p + off, 4 * fo);
     off += 4 * fo;
   }
+  if (flags & ~3u) return fail(c, SL7_EFORMAT, "flags (bit0 has_norm, bit1 residual)");
   const bool has_norm = flags & 1u;
   std::vector<float> ish, isc, osh, osc;
   if (has_norm) {
@@ -801,6 +807,7 @@ sl7_status sl7_load_weights(sl7_ctx c, const void* blob, size_t nbytes) {
   c->W = std::move(W);
   c->b = std::move(b);
   c->has_norm = has_norm;
+  c->residual = (flags & 2u) != 0;
   c->in_shift = ish;
   c->in_scale = isc;
   c->out_shift = osh;

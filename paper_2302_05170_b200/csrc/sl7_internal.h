@@ -61,7 +61,8 @@ struct RunParams {
   int width;             // padded hidden width used by the kernel
   float l1w[kMaxW], l1b[kMaxW];
   double l1w_d[kMaxW], l1b_d[kMaxW];   // host-side double copies (not read by kernels)
-  float out_scale[kMaxM], out_shift[kMaxM];
+  float out_scale[kMaxM], out_shift[kMaxM];   // residual blobs: already multiplied by sqrt(dt)
+  float res_y;                               // 1 for residual blobs (y_j = Y + ...), else 0
   const float* wdev;     // FP32 kernel: hidden + output weights (layout: WeightLayoutF32)
   const void* wtc;       // TC kernel: packed bf16 operand images (layout: sl7_tc.cu)
   const float* btc;      // TC kernel: fp32 biases [(L-1)][64] + out bias [16]

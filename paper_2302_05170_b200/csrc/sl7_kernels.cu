@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(128) ann_f32_step_kernel(const __grid_constant
           if (4 * kk + 2 < H) a0 = fmaf(wv.z, h[4 * kk + 2], a0);
           if (4 * kk + 3 < H) a1 = fmaf(wv.w, h[4 * kk + 3], a1);
         }
-        y[j] = fmaf(a0 + a1, p.out_scale[j], p.out_shift[j]);
+        y[j] = fmaf(p.res_y, Y, fmaf(a0 + a1, p.out_scale[j], p.out_shift[j]));
       }
       // steps 5-6: Y_{i+1} = g_m(X_hat)
       Y = gm_eval<MR, RT_M>(p, Z, y);

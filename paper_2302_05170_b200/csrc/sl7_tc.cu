@@ -349,7 +349,8 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
           tc::wait_ld();
 #pragma unroll
           for (int j = 0; j < MR; ++j)
-            y[j] = fmaf(FOLD ? __uint_as_float(v[j]) : __uint_as_float(v[j]) + t.bout[j], p.out_scale[j], p.out_shift[j]);
+            y[j] = fmaf(p.res_y, Y, fmaf(FOLD ? __uint_as_float(v[j]) : __uint_as_float(v[j]) + t.bout[j],
+                                         p.out_scale[j], p.out_shift[j]));
         }
       }
       // ---- steps 5-6: Y_{i+1} = g_m(X_hat)

@@ -87,13 +87,14 @@ class MlpParams:
     in_scale: np.ndarray | None = None
     out_shift: np.ndarray | None = None
     out_scale: np.ndarray | None = None
+    residual: bool = False          # blob flags bit 1 (include/sl7.h, 'Weights blob')
 
     @property
     def has_norm(self) -> bool:
         return self.in_shift is not None
 
 
-def glorot_mlp(dims, act, seed=WEIGHT_SEED, bias_scale=0.1, with_norm=False) -> MlpParams:
+def glorot_mlp(dims, act, seed=WEIGHT_SEED, bias_scale=0.1, with_norm=False, residual=False) -> MlpParams:
     """Seeded Glorot-uniform weights, L = sqrt(6/(fan_in+fan_out)), fp32-representable.
 
     Biases are small uniform values (not zero) so that every term of the forward pass is exercised.
@@ -105,7 +106,7 @@ def glorot_mlp(dims, act, seed=WEIGHT_SEED, bias_scale=0.1, with_norm=False) -> 
         L = np.sqrt(6.0 / (fi + fo))
         W.append(rng.uniform(-L, L, size=(fo, fi)).astype(np.float32).astype(np.float64))
         b.append(rng.uniform(-bias_scale, bias_scale, size=fo).astype(np.float32).astype(np.float64))
-    p = MlpParams(tuple(dims), act, W, b)
+    p = MlpParams(tuple(dims), act, W, b, residual=residual)
     if with_norm:
         d_in, m = dims[0], dims[-1]
         p.in_shift = rng.uniform(-0.5, 0.5, size=d_in).astype(np.float32).astype(np.float64)
@@ -125,7 +126,7 @@ def pack_blob(p: MlpParams) -> bytes:
     out += BLOB_MAGIC
     out += struct.pack("<II", BLOB_VERSION, len(p.dims))
     out += struct.pack("<%dI" % len(p.dims), *p.dims)
-    out += struct.pack("<II", p.act, 1 if p.has_norm else 0)
+    out += struct.pack("<II", p.act, (1 if p.has_norm else 0) | (2 if p.residual else 0))
     for W, b in zip(p.W, p.b):
         out += np.asarray(W, dtype="<f4").tobytes()
         out += np.asarray(b, dtype="<f4").tobytes()

@@ -5,6 +5,7 @@ a swapped index or operand) fails at least one test here.  Citations: PAPER.md l
 """
 import math
 import os
+import struct
 
 import mpmath
 import numpy as np
@@ -554,3 +555,31 @@ def test_multistep_ann_paths_equal_affine_recursion():
         np.testing.assert_allclose(Ya[i + 1], Y, rtol=0, atol=1e-12)
     R = O.exact_reference("ou", theta, 0.7, dt, Z)
     np.testing.assert_allclose(Ya[-1], R, rtol=0, atol=1e-6)
+
+
+def test_residual_blob_reproduces_ou_closed_form():
+    """Residual output form (blob flags bit 1, reading R-11): H_j = Y + sqrt(dt) * out_j.  An exactly-affine
+    softplus network with slope (a - 1)/sqrt(dt) and intercepts (b + s x_j)/sqrt(dt) must give the Eq. 6.6
+    OU points a Y + b + s x_j (up to the fp32 storage of those weights), its 7L paths must track the exact
+    OU solution on the same normals, and the forward-error scale must include |Y|."""
+    theta, dt, n, m = (0.3, 1.2, 0.4), 0.25, 12, 7
+    ybar, lam, sig = theta
+    x = O.gauss_hermite_nodes(m)
+    a = math.exp(-lam * dt)
+    b = ybar * (1 - a)
+    s = sig * math.sqrt((1 - math.exp(-2 * lam * dt)) / (2 * lam))
+    p = affine_softplus_mlp((5, 50, 50, 50, 50, m), (a - 1) / math.sqrt(dt), (b + s * x) / math.sqrt(dt))
+    p.residual = True
+    blob = pack_blob(p)
+    assert struct.unpack_from("<I", blob, 12 + 4 * 6 + 4)[0] == 2          # flags word: residual, no norm
+    net = O.parse_blob(blob)
+    assert net.residual
+    Ys = np.array([-1.5, 0.0, 0.7, 2.0])
+    pts = O.ann_collocation(net, Ys, dt, theta)
+    np.testing.assert_allclose(pts, a * Ys[:, None] + b + s * x[None, :], rtol=0, atol=2e-7)
+    A = O.mlp_abs_scale(net, O.ann_features(Ys, dt, theta))
+    assert np.all(A >= np.abs(Ys)[:, None])
+    paths = np.arange(2000, dtype=np.uint64)
+    Ya, Z = O.simulate(O.Spec(m, "ann", theta, 0.7, dt, n, net=net), 5, paths)
+    R = O.exact_reference("ou", theta, 0.7, dt, Z)
+    np.testing.assert_allclose(Ya[-1], R, rtol=0, atol=2e-6)
