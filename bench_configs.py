@@ -53,6 +53,16 @@ def timed_launches(fn, steps, warmup, flush, stream):
     return statistics.mean(ms), min(ms)
 
 
+def _summary(sl7, stats, opts, q_levels=()):
+    """stats_summary, or a marker when no terminal value is finite (7L-CDC's polynomial extrapolation into
+    the far tails can diverge: DESIGN.md reading R-19) -- the line is still emitted, flagged."""
+    try:
+        return sl7.stats_summary(stats.cpu().numpy(), opts, q_levels=q_levels)
+    except sl7.Sl7Error:
+        keys = ("mean", "var", "skew", "exkurt", "strong_err", "rms_err")
+        return dict({k: None for k in keys}, n=0, n_nonfinite=int(stats[1].item()), quantiles=None, diverged=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="all", choices=["cfg2", "cfg3", "cfg4", "em", "train", "all"])
@@ -140,7 +150,7 @@ def main():
                     clk.start()
                     ms, ms_min = timed_launches(fn, a.steps, a.warmup, flush, stream)
                     clk.stop()
-                    s = sl7.stats_summary(stats.cpu().numpy(), opts)
+                    s = _summary(sl7, stats, opts)
                     rate = N * 16 * K / (ms * 1e-3)
                     line = {"config": "em_" + proc, "mode": "euler_maruyama_K%d%s" % (K, "_fast" if fast else ""),
                             "metric": "Euler-Maruyama fine path-steps/sec (device-timed)", "value": rate,
@@ -199,7 +209,7 @@ def main():
             clk.start()
             ms, ms_min = timed_launches(fn, max(1, a.steps - 1), 1, flush, stream)
             clk.stop()
-            s = sl7.stats_summary(stats.cpu().numpy(), opts, q_levels=[0.01, 0.5, 0.99])
+            s = _summary(sl7, stats, opts, [0.01, 0.5, 0.99])
             rate = n_paths * w.n_steps / (ms * 1e-3)
             line = {"config": "cfg4", "mode": label, "metric": "7L path-steps/sec (device-timed)", "value": rate,
                     "unit": UNIT, "ms_per_launch": ms, "paths": n_paths, "n_steps": w.n_steps, "m": w.m,
@@ -248,7 +258,7 @@ def main():
                 clk.start()
                 ms, ms_min = timed_launches(fn, a.steps, a.warmup, flush, stream)
                 clk.stop()
-                s = sl7.stats_summary(stats.cpu().numpy(), opts, q_levels=[0.01, 0.5, 0.99])
+                s = _summary(sl7, stats, opts, [0.01, 0.5, 0.99])
                 rate = n_paths * w.n_steps / (ms * 1e-3)
                 line = {"config": key, "mode": label, "metric": "7L path-steps/sec (device-timed)", "value": rate,
                         "unit": UNIT, "ms_per_launch": ms, "paths": n_paths, "n_steps": w.n_steps, "m": w.m,
@@ -276,7 +286,7 @@ def main():
             clk.start()
             ms, ms_min = timed_launches(sharded, a.steps, a.warmup, flush, stream)
             clk.stop()
-            s = sl7.stats_summary(stats.cpu().numpy(), opts, q_levels=[0.01, 0.5, 0.99])
+            s = _summary(sl7, stats, opts, [0.01, 0.5, 0.99])
             emit({"config": key, "mode": "cdc_sharded_driver_1rank", "metric": "7L path-steps/sec (device-timed)",
                   "value": N * w.n_steps / (ms * 1e-3), "unit": UNIT, "ms_per_launch": ms, "paths": N,
                   "n_steps": w.n_steps, "m": w.m, "exchange": "4 x %d-byte histogram all-reduces per step" % (
