@@ -214,3 +214,44 @@ def test_nonfinite_paths_are_counted_not_summed(gpu_lib):
     np.testing.assert_array_equal(v[8:], ref[8:])
     s = sl7.stats_summary(v, opts)
     assert s["status"] == sl7.ENONFINITE and s["n_nonfinite"] == (~fin).sum()
+
+
+@pytest.mark.parametrize("mode", ["ann_bf16", "ann_fp32", "cdc", "em"])
+def test_side_stream_equals_default_stream(gpu_lib, mode):
+    """opts.stream is honoured: every kernel family enqueued on a side stream (with the output buffers
+    allocated on it) gives bitwise the default-stream result once that stream is synchronised."""
+    sl7 = gpu_lib
+    torch = _torch()
+    w = workloads()["cfg2_ou"]
+    n, steps = 40_003, 6
+
+    def run(stream):
+        ctx = sl7.Context(w.m, list(w.dims), w.act)
+        ctx.load_weights(load_golden_blob(w.blob))
+        kw = dict(stream=stream, n_bins=256, hist_lo=-3.0, hist_hi=3.0)
+        if mode == "em":
+            opts = sl7.make_opts(**kw)
+            out, st = ctx.simulate_em(sl7.MODEL_OU, w.y0, w.dt, steps, 4, w.theta, n, w.seed, sl7.OUT_TERMINAL, opts,
+                                      stats=torch.zeros(sl7.stats_elems(256), dtype=torch.float64, device="cuda"))
+        else:
+            prec = sl7.PREC_BF16 if mode == "ann_bf16" else sl7.PREC_FP32
+            scheme = sl7.SCHEME_CDC if mode == "cdc" else sl7.SCHEME_7L
+            opts = sl7.make_opts(prec=prec, colloc=sl7.COLLOC_ANN, scheme=scheme, **kw)
+            out, st = ctx.simulate(w.y0, w.dt, steps, w.theta, n, w.seed, sl7.OUT_TERMINAL, opts,
+                                   stats=torch.zeros(sl7.stats_elems(256), dtype=torch.float64, device="cuda"))
+        return ctx, out, st
+
+    _, ref_out, ref_st = run(None)
+    torch.cuda.synchronize()
+    ref_out, ref_st = ref_out.clone(), ref_st.clone()
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        ctx, out, st = run(side)
+        ev = torch.cuda.Event()
+        ev.record(side)
+    side.synchronize()
+    assert ev.query()
+    assert torch.equal(out, ref_out)
+    torch.testing.assert_close(st[:2], ref_st[:2], rtol=0, atol=0)          # counts
+    torch.testing.assert_close(st[8:], ref_st[8:], rtol=0, atol=0)          # histogram
+    torch.testing.assert_close(st, ref_st, rtol=1e-12, atol=0)              # fp64 sums (atomic order)
