@@ -43,6 +43,10 @@ def ann_flops_per_path_step(dims):
     return f
 
 
+# NVML throttle reasons that void a timed region (sw_power_cap is kept and only noted)
+THROTTLE_REJECT = {"HwSlowdown", "HwThermalSlowdown", "SwThermalSlowdown", "HwPowerBrakeSlowdown"}
+
+
 class ClockSampler(threading.Thread):
     """Samples SM clock and throttle reasons via NVML every 100 ms during the timed region."""
 
@@ -230,20 +234,31 @@ def main():
         sweep(ann_opts, sl7.COLLOC_ANN)
     barrier()
 
-    # ---------------- timed region: K ANN sweeps (device-timed with CUDA events on the launch stream)
-    clk = ClockSampler(local)
-    clk.start()
-    per_step_ms, kernel_ms = [], []
-    barrier()
-    for _ in range(a.steps):
-        flush.fill_(1.0)                                     # L2 flush (untimed)
-        evs = new_events()
-        sweep(ann_opts, sl7.COLLOC_ANN, evs)
-        torch.cuda.synchronize()
-        kernel_ms.append([e0.elapsed_time(ek) for e0, _, ek in evs])
-        per_step_ms.append(sum(e0.elapsed_time(e1) for e0, e1, _ in evs))
-    barrier()
-    clk.stop()
+    # ---------------- timed region: K ANN sweeps (device-timed with CUDA events on the launch stream).
+    # A region that saw a hardware / thermal slowdown is measured once more (the contract's rule); the
+    # line reports the clocks of the region it keeps and whether it was a re-measurement.
+    for attempt in range(2):
+        clk = ClockSampler(local)
+        clk.start()
+        per_step_ms, kernel_ms = [], []
+        barrier()
+        for _ in range(a.steps):
+            flush.fill_(1.0)                                     # L2 flush (untimed)
+            evs = new_events()
+            sweep(ann_opts, sl7.COLLOC_ANN, evs)
+            torch.cuda.synchronize()
+            kernel_ms.append([e0.elapsed_time(ek) for e0, _, ek in evs])
+            per_step_ms.append(sum(e0.elapsed_time(e1) for e0, e1, _ in evs))
+        barrier()
+        clk.stop()
+        throttled = bool(set(clk.reasons) & THROTTLE_REJECT)
+        if dist:
+            flag = torch.tensor([1.0 if throttled else 0.0], device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+            throttled = flag.item() > 0
+        if not throttled:
+            break
+    remeasured = attempt > 0
     step_ms = max_over_ranks(statistics.mean(per_step_ms), dev)
     path_steps = N * sum(N_SWEEP)
     value = world * path_steps / (step_ms * 1e-3)
@@ -335,7 +350,7 @@ def main():
             "data": "synthetic (oracle-fitted weights)",
             "config": dict(config, prec=prec_name[prec], parallelism="dp%d" % world),
             "roofline": roof, "gpu_launches": a.steps * 2 * len(N_SWEEP),
-            "clocks": clk.summary(),
+            "clocks": dict(clk.summary(), remeasured=remeasured),
             "e2e": {"value": world * path_steps / (e2e_step * 1e-3), "unit": UNIT, "h2d_bytes_per_step": up_b,
                     "d2h_bytes_per_step": down_b, "ms_per_step": e2e_step},
             "modes": {"ann": {"path_steps_per_s": value, "strong_err_by_n": {ns: summ[ns]["strong_err"] for ns in N_SWEEP},
