@@ -141,38 +141,57 @@ __global__ void __launch_bounds__(256) exact_special_kernel(const __grid_constan
 // layers read from shared memory as float4 broadcasts (all lanes of a warp read the same row), one
 // FFMA per weight with the activation vector held in registers.
 // ------------------------------------------------------------------------------------------------
-template <int H, int HS, int MR, bool RT_M, int ACT>
+template <int H, int HS, int MR, bool RT_M, int ACT, int PP>
 __global__ void __launch_bounds__(128) ann_f32_step_kernel(const __grid_constant__ RunParams p) {
   extern __shared__ float4 smem4[];
   float* sw = reinterpret_cast<float*>(smem4);
   __shared__ double red[8];
   const int L = p.n_hidden;
   const size_t nw = f32_weight_floats(H, HS, L, MR);
-  float* gs = sw + ((nw + 3) & ~size_t(3));                  // [H][blockDim] activation scratch
-  uint32_t* hist = reinterpret_cast<uint32_t*>(gs + (size_t)H * blockDim.x);
+  float* gs = sw + ((nw + 3) & ~size_t(3));                  // [H][PP][blockDim] activation scratch
+  uint32_t* hist = reinterpret_cast<uint32_t*>(gs + (size_t)H * PP * blockDim.x);
   for (size_t k = threadIdx.x; k < nw; k += blockDim.x) sw[k] = p.wdev[k];
   hist_init(p, hist);
   __syncthreads();
   const float* wout = sw + (size_t)(L - 1) * f32_layer_floats(H, HS);
   const float* bout = wout + MR * HS;
 
+  // PP paths per thread (paths base + tid and base + blockDim + tid): every weight broadcast from shared
+  // memory feeds PP FFMAs.  With one path per thread the kernel was bound by shared-memory wavefronts
+  // (81% busy: a warp-wide broadcast LDS.128 costs two wavefronts per four weights).
   StatAcc acc;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < p.n_paths; q += stride) {
-    const uint64_t gp = p.path_offset + q;
-    float Y = p.y0;
-    if (p.out_mode == kFull) p.out[q] = Y;
-    RefState rs;
-    ref_init(rs, p);
-    float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
-    for (int i = 0; i < p.n_steps; ++i) {
-      if ((i & 3) == 0) normals4(p.key0, p.key1, gp, (uint32_t)(i >> 2), z0, z1, z2, z3);
-      const float Z = z0;
-      z0 = z1; z1 = z2; z2 = z3;
-      // step 3 (Eq. 6.4): y_hat = H_hat(Y_i, dt, theta)
-      float h[H];
+  const uint64_t tile = (uint64_t)PP * blockDim.x;
+  const uint64_t stride = (uint64_t)gridDim.x * tile;
+  for (uint64_t base = (uint64_t)blockIdx.x * tile; base < p.n_paths; base += stride) {
+    uint64_t q[PP], gp[PP];
+    bool ok[PP];
+    float Y[PP], z[PP][4];
+    RefState rs[PP];
 #pragma unroll
-      for (int k = 0; k < H; ++k) h[k] = activate<ACT>(fmaf(p.l1w[k], Y, p.l1b[k]));
+    for (int pp = 0; pp < PP; ++pp) {
+      q[pp] = base + (uint64_t)pp * blockDim.x + threadIdx.x;
+      ok[pp] = q[pp] < p.n_paths;
+      gp[pp] = p.path_offset + (ok[pp] ? q[pp] : 0);
+      Y[pp] = p.y0;
+      if (ok[pp] && p.out_mode == kFull) p.out[q[pp]] = Y[pp];
+      ref_init(rs[pp], p);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) z[pp][r] = 0.f;
+    }
+    for (int i = 0; i < p.n_steps; ++i) {
+      float Z[PP];
+#pragma unroll
+      for (int pp = 0; pp < PP; ++pp) {
+        if ((i & 3) == 0) normals4(p.key0, p.key1, gp[pp], (uint32_t)(i >> 2), z[pp][0], z[pp][1], z[pp][2], z[pp][3]);
+        Z[pp] = z[pp][0];
+        z[pp][0] = z[pp][1]; z[pp][1] = z[pp][2]; z[pp][2] = z[pp][3];
+      }
+      // step 3 (Eq. 6.4): y_hat = H_hat(Y_i, dt, theta)
+      float h[PP][H];
+#pragma unroll
+      for (int pp = 0; pp < PP; ++pp)
+#pragma unroll
+        for (int k = 0; k < H; ++k) h[pp][k] = activate<ACT>(fmaf(p.l1w[k], Y[pp], p.l1b[k]));
       for (int l = 0; l < L - 1; ++l) {
         const float* W = sw + (size_t)l * f32_layer_floats(H, HS);
         const float* b = W + H * HS;
@@ -182,42 +201,64 @@ __global__ void __launch_bounds__(128) ann_f32_step_kernel(const __grid_constant
 #pragma unroll 2
         for (int j = 0; j < H; ++j) {
           const float4* row = reinterpret_cast<const float4*>(W + j * HS);
-          float a0 = b[j], a1 = 0.f;
+          float a0[PP], a1[PP];
+#pragma unroll
+          for (int pp = 0; pp < PP; ++pp) { a0[pp] = b[j]; a1[pp] = 0.f; }
 #pragma unroll
           for (int kk = 0; kk < HS / 4; ++kk) {
             const float4 wv = row[kk];
-            if (4 * kk + 0 < H) a0 = fmaf(wv.x, h[4 * kk + 0], a0);
-            if (4 * kk + 1 < H) a1 = fmaf(wv.y, h[4 * kk + 1], a1);
-            if (4 * kk + 2 < H) a0 = fmaf(wv.z, h[4 * kk + 2], a0);
-            if (4 * kk + 3 < H) a1 = fmaf(wv.w, h[4 * kk + 3], a1);
+#pragma unroll
+            for (int pp = 0; pp < PP; ++pp) {
+              if (4 * kk + 0 < H) a0[pp] = fmaf(wv.x, h[pp][4 * kk + 0], a0[pp]);
+              if (4 * kk + 1 < H) a1[pp] = fmaf(wv.y, h[pp][4 * kk + 1], a1[pp]);
+              if (4 * kk + 2 < H) a0[pp] = fmaf(wv.z, h[pp][4 * kk + 2], a0[pp]);
+              if (4 * kk + 3 < H) a1[pp] = fmaf(wv.w, h[pp][4 * kk + 3], a1[pp]);
+            }
           }
-          gs[j * blockDim.x + threadIdx.x] = activate<ACT>(a0 + a1);
+#pragma unroll
+          for (int pp = 0; pp < PP; ++pp) gs[(j * PP + pp) * blockDim.x + threadIdx.x] = activate<ACT>(a0[pp] + a1[pp]);
         }
 #pragma unroll
-        for (int k = 0; k < H; ++k) h[k] = gs[k * blockDim.x + threadIdx.x];
+        for (int pp = 0; pp < PP; ++pp)
+#pragma unroll
+          for (int k = 0; k < H; ++k) h[pp][k] = gs[(k * PP + pp) * blockDim.x + threadIdx.x];
       }
-      float y[MR];
+      float y[PP][MR];
 #pragma unroll
       for (int j = 0; j < MR; ++j) {
         const float4* row = reinterpret_cast<const float4*>(wout + j * HS);
-        float a0 = bout[j], a1 = 0.f;
+        float a0[PP], a1[PP];
+#pragma unroll
+        for (int pp = 0; pp < PP; ++pp) { a0[pp] = bout[j]; a1[pp] = 0.f; }
 #pragma unroll
         for (int kk = 0; kk < HS / 4; ++kk) {
           const float4 wv = row[kk];
-          if (4 * kk + 0 < H) a0 = fmaf(wv.x, h[4 * kk + 0], a0);
-          if (4 * kk + 1 < H) a1 = fmaf(wv.y, h[4 * kk + 1], a1);
-          if (4 * kk + 2 < H) a0 = fmaf(wv.z, h[4 * kk + 2], a0);
-          if (4 * kk + 3 < H) a1 = fmaf(wv.w, h[4 * kk + 3], a1);
+#pragma unroll
+          for (int pp = 0; pp < PP; ++pp) {
+            if (4 * kk + 0 < H) a0[pp] = fmaf(wv.x, h[pp][4 * kk + 0], a0[pp]);
+            if (4 * kk + 1 < H) a1[pp] = fmaf(wv.y, h[pp][4 * kk + 1], a1[pp]);
+            if (4 * kk + 2 < H) a0[pp] = fmaf(wv.z, h[pp][4 * kk + 2], a0[pp]);
+            if (4 * kk + 3 < H) a1[pp] = fmaf(wv.w, h[pp][4 * kk + 3], a1[pp]);
+          }
         }
-        y[j] = fmaf(p.res_y, Y, fmaf(a0 + a1, p.out_scale[j], p.out_shift[j]));
+#pragma unroll
+        for (int pp = 0; pp < PP; ++pp)
+          y[pp][j] = fmaf(p.res_y, Y[pp], fmaf(a0[pp] + a1[pp], p.out_scale[j], p.out_shift[j]));
       }
       // steps 5-6: Y_{i+1} = g_m(X_hat)
-      Y = gm_eval<MR, RT_M>(p, Z, y);
-      ref_step(rs, p, Z);
-      if (p.out_mode == kFull) p.out[(uint64_t)(i + 1) * p.n_paths + q] = Y;
+#pragma unroll
+      for (int pp = 0; pp < PP; ++pp) {
+        Y[pp] = gm_eval<MR, RT_M>(p, Z[pp], y[pp]);
+        ref_step(rs[pp], p, Z[pp]);
+        if (ok[pp] && p.out_mode == kFull) p.out[(uint64_t)(i + 1) * p.n_paths + q[pp]] = Y[pp];
+      }
     }
-    if (p.out_mode == kTerminal) p.out[q] = Y;
-    if (p.has_stats) stat_add(acc, p, Y, ref_final(rs, p), hist);
+#pragma unroll
+    for (int pp = 0; pp < PP; ++pp) {
+      if (!ok[pp]) continue;
+      if (p.out_mode == kTerminal) p.out[q[pp]] = Y[pp];
+      if (p.has_stats) stat_add(acc, p, Y[pp], ref_final(rs[pp], p), hist);
+    }
   }
   if (p.has_stats) stat_flush(acc, p, hist, red);
 }
@@ -257,7 +298,8 @@ __global__ void zero_kernel(double* p, size_t n) {
 namespace {
 
 template <typename K>
-cudaError_t launch_persistent(K kernel, int threads, size_t smem, const RunParams& p, cudaStream_t st, int num_sms) {
+cudaError_t launch_persistent(K kernel, int threads, size_t smem, const RunParams& p, cudaStream_t st, int num_sms,
+                              int paths_per_cta = 0) {
   cudaError_t e;
   if (smem > 48 * 1024) {
     e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -267,7 +309,8 @@ cudaError_t launch_persistent(K kernel, int threads, size_t smem, const RunParam
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  const uint64_t need = (p.n_paths + threads - 1) / threads;
+  const uint64_t per_cta = (uint64_t)(paths_per_cta > 0 ? paths_per_cta : threads);
+  const uint64_t need = (p.n_paths + per_cta - 1) / per_cta;
   const uint64_t full = (uint64_t)per_sm * (uint64_t)num_sms;
   const unsigned grid = (unsigned)(need < full ? need : full);
   kernel<<<grid, threads, smem, st>>>(p);
@@ -312,18 +355,18 @@ cudaError_t launch_exact(const RunParams& p, cudaStream_t st, int num_sms) {
               : launch_exact_general<COLLOC, false>(p, st, num_sms, smem);
 }
 
-template <int H, int HS, int MR, bool RT, int ACT>
+template <int H, int HS, int MR, bool RT, int ACT, int PP>
 cudaError_t launch_ann_f32_t(const RunParams& p, cudaStream_t st, int num_sms) {
   const size_t nw = f32_weight_floats(H, HS, p.n_hidden, MR);
-  const size_t smem = (((nw + 3) & ~size_t(3)) + (size_t)H * 128) * sizeof(float) + hist_bytes(p);
-  return launch_persistent(ann_f32_step_kernel<H, HS, MR, RT, ACT>, 128, smem, p, st, num_sms);
+  const size_t smem = (((nw + 3) & ~size_t(3)) + (size_t)H * PP * 128) * sizeof(float) + hist_bytes(p);
+  return launch_persistent(ann_f32_step_kernel<H, HS, MR, RT, ACT, PP>, 128, smem, p, st, num_sms, 128 * PP);
 }
 
 template <int ACT>
 cudaError_t launch_ann_f32(const RunParams& p, cudaStream_t st, int num_sms) {
-  if (p.width == 50 && p.m == 5) return launch_ann_f32_t<50, 52, 5, false, ACT>(p, st, num_sms);
-  if (p.width == 50 && p.m == 7) return launch_ann_f32_t<50, 52, 7, false, ACT>(p, st, num_sms);
-  if (p.width == 64) return launch_ann_f32_t<64, 64, kMaxM, true, ACT>(p, st, num_sms);
+  if (p.width == 50 && p.m == 5) return launch_ann_f32_t<50, 52, 5, false, ACT, 2>(p, st, num_sms);
+  if (p.width == 50 && p.m == 7) return launch_ann_f32_t<50, 52, 7, false, ACT, 2>(p, st, num_sms);
+  if (p.width == 64) return launch_ann_f32_t<64, 64, kMaxM, true, ACT, 1>(p, st, num_sms);
   return cudaErrorInvalidValue;
 }
 
