@@ -334,7 +334,7 @@ def main():
                 "frac": achieved / peak,
                 # dram__bytes_read.sum + dram__bytes_write.sum of the n=64 launch (ncu --set full, recorded in
                 # profiles/r01_ann_tc_ncu.md): weights + stats only; the kernel reads no HBM per path-step
-                "traffic": 64512 + 93952, "traffic_note": "dram bytes read + written per n=64 launch (1e7 paths x 64 steps), profiles/r01_ann_tc_ncu.md",
+                "traffic": 73984 + 58112, "traffic_note": "dram bytes read + written per n=64 launch (1e7 paths x 64 steps), profiles/r01_ann_tc_ncu.md",
                 "peak_basis": "148 SM x 16 MUFU op/clk x %g MHz (max SM clock)" % sm_max,
                 "algorithmic": "%d transcendental activations per path-step (one per hidden unit); the kernel "
                                "spends one MUFU op per tanh (MUFU.TANH, measured max error 9.9e-6 relative) and "
