@@ -255,6 +255,13 @@ class Context:
 
     __del__ = close
 
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+        return False
+
     def load_weights(self, blob: bytes):
         _check(_lib.sl7_load_weights(self._h, blob, len(blob)), self._h)
 

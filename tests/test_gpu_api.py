@@ -255,3 +255,42 @@ def test_side_stream_equals_default_stream(gpu_lib, mode):
     torch.testing.assert_close(st[:2], ref_st[:2], rtol=0, atol=0)          # counts
     torch.testing.assert_close(st[8:], ref_st[8:], rtol=0, atol=0)          # histogram
     torch.testing.assert_close(st, ref_st, rtol=1e-12, atol=0)              # fp64 sums (atomic order)
+
+
+def test_contexts_release_their_device_memory(gpu_lib):
+    """Creating, using (every buffer-owning path: weights, 7L-CDC scratch and state, the pipelined host API's
+    staging slots and copy stream) and closing contexts in a loop leaves the device's free memory where it
+    was: sl7_destroy frees everything the context allocated."""
+    sl7 = gpu_lib
+    torch = _torch()
+    w = workloads()["cfg2_ou"]
+    blob = load_golden_blob(w.blob)
+    n = 200_000
+
+    def cycle():
+        with sl7.Context(w.m, list(w.dims), w.act) as ctx:
+            ctx.load_weights(blob)
+            st = torch.zeros(sl7.stats_elems(64), dtype=torch.float64, device="cuda")
+            kw = dict(n_bins=64, hist_lo=-3.0, hist_hi=3.0)
+            for prec in (sl7.PREC_BF16, sl7.PREC_FP32):
+                ctx.simulate(w.y0, w.dt, 4, w.theta, n, 1, sl7.OUT_STATS,
+                             sl7.make_opts(prec=prec, colloc=sl7.COLLOC_ANN, **kw), stats=st)
+            ctx.simulate(w.y0, w.dt, 4, w.theta, n, 1, sl7.OUT_STATS,
+                         sl7.make_opts(colloc=sl7.COLLOC_ANN, scheme=sl7.SCHEME_CDC, **kw), stats=st)
+            ctx.simulate_em(sl7.MODEL_OU, w.y0, w.dt, 4, 2, w.theta, n, 1, sl7.OUT_STATS, sl7.make_opts(**kw), stats=st)
+            ctx.simulate_host_async(w.y0, w.dt, 4, w.theta, n, 1, sl7.OUT_TERMINAL,
+                                    sl7.make_opts(prec=sl7.PREC_BF16, colloc=sl7.COLLOC_ANN, **kw),
+                                    h_out=np.empty(n, dtype=np.float32))
+            ctx.sync()
+            torch.cuda.synchronize()
+        del st
+        torch.cuda.empty_cache()
+
+    cycle()                                   # first use: lazy module / kernel loading
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    for _ in range(20):
+        cycle()
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 - free1 < 64 << 20, (free0, free1)
