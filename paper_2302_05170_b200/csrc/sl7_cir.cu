@@ -36,10 +36,14 @@ struct Ncx2 {
 __device__ double gamma_p(double a, double y, double lg_a1) {
   const double lpre = a * log(y) - y - lg_a1;   // log(y^a e^{-y} / Gamma(a + 1))
   if (y < a + 1.0) {
+    // two series terms per float64 reciprocal: y/(a+n) and y/(a+n+1) from 1/((a+n)(a+n+1))
     double term = 1.0, sum = 1.0, ap = a;
-    for (int n = 0; n < 2000; ++n) {
-      ap += 1.0;
-      term *= y / ap;
+    for (int n = 0; n < 1000; ++n) {
+      const double a1 = ap + 1.0, a2 = ap + 2.0, r = y / (a1 * a2);
+      ap = a2;
+      term *= a2 * r;
+      sum += term;
+      term *= a1 * r;
       sum += term;
       if (term < sum * 1e-17) break;
     }
@@ -80,9 +84,11 @@ __device__ void ncx2_cdf_pdf(const Ncx2& n, double x, double& F, double& f, doub
     double Pk = P, Gk = G, wk = n.w_m, ak = n.a_m;
     for (int k = n.k_m + 1; k < n.k_m + 100000; ++k) {
       Pk = fmax(Pk - Gk, 0.0);
-      Gk *= y / (ak + 1.0);
-      ak += 1.0;
-      wk *= n.mu / (double)k;
+      // y / (a + 1) and mu / k from one float64 reciprocal of (a + 1) k
+      const double a1 = ak + 1.0, kd = (double)k, r = 1.0 / (a1 * kd);
+      Gk *= y * kd * r;
+      ak = a1;
+      wk *= n.mu * a1 * r;
       Fs += wk * Pk;
       const double t = wk * Gk * ak;
       fs += t;
@@ -92,11 +98,12 @@ __device__ void ncx2_cdf_pdf(const Ncx2& n, double x, double& F, double& f, doub
   }
   {
     double Pk = P, Gk = G, wk = n.w_m, ak = n.a_m;
+    const double ry = 1.0 / y, rmu = 1.0 / n.mu;   // loop invariants: two float64 divisions per term saved
     for (int k = n.k_m - 1; k >= 0; --k) {
-      Gk *= ak / y;
+      Gk *= ak * ry;
       ak -= 1.0;
       Pk += Gk;
-      wk *= (double)(k + 1) / n.mu;
+      wk *= (double)(k + 1) * rmu;
       Fs += wk * Pk;
       const double t = wk * Gk * ak;
       fs += t;
