@@ -655,8 +655,14 @@ sl7_status run(sl7_ctx c, RunParams& p, const sl7_run_opts* o, float* d_out, dou
   } else if (p.colloc == kAnn && (o->prec == SL7_PREC_BF16 || o->prec == SL7_PREC_SPLIT || o->prec == SL7_PREC_TF32)) {
     // per-run part of the TC parameters: layer 1 folded (as in RunParams) and pre-scaled in double
     TcParams t = c->tcp;
+#ifdef SL7_AB_HOOKS
+    // experiment builds only (-DSL7_AB_HOOKS): SL7_TC_VARIANT selects the epilogue variants timed in
+    // DESIGN.md §6; variant 9 skips the MMAs (timing only, wrong results).  Product builds ignore it.
     const char* v = std::getenv("SL7_TC_VARIANT");
     t.variant = v ? std::atoi(v) : 0;
+#else
+    t.variant = 0;
+#endif
     t.split = (o->prec == SL7_PREC_SPLIT) ? 1 : 0;
     t.tf32 = (o->prec == SL7_PREC_TF32) ? 1 : 0;
     // tanh on MUFU.TANH by default (SL7_TC_VARIANT 1..9 select the ex2 + rcp epilogues of DESIGN.md §6 for

@@ -433,7 +433,9 @@ cudaError_t launch_tc_act(const RunParams& p, const TcParams& t, cudaStream_t st
       case 1: return launch_tc_t<NG, 50, 7, false, ACT, 0x00u>(p, t, st, num_sms);
       case 2: return launch_tc_t<NG, 50, 7, false, ACT, 0x25u>(p, t, st, num_sms);
       case 3: return launch_tc_t<NG, 50, 7, false, ACT, 0x77u>(p, t, st, num_sms);
-      case 9: return launch_tc_t<NG, 50, 7, false, ACT, NM, 1, true>(p, t, st, num_sms);
+#ifdef SL7_AB_HOOKS
+      case 9: return launch_tc_t<NG, 50, 7, false, ACT, NM, 1, true>(p, t, st, num_sms);   // timing only
+#endif
       default: return launch_tc_t<NG, 50, 7, false, ACT, NM>(p, t, st, num_sms);
     }
   }
