@@ -294,3 +294,21 @@ def test_contexts_release_their_device_memory(gpu_lib):
     torch.cuda.synchronize()
     free1, _ = torch.cuda.mem_get_info()
     assert free0 - free1 < 64 << 20, (free0, free1)
+
+
+def test_experiment_hook_is_ignored_by_product_builds(gpu_lib, monkeypatch):
+    """SL7_TC_VARIANT (the epilogue A/B hook; variant 9 skips the MMAs) is honoured only by -DSL7_AB_HOOKS
+    experiment builds: the product library gives bitwise the same results with it set."""
+    sl7 = gpu_lib
+    torch = _torch()
+    w = workloads()["cfg1"]
+    ctx = sl7.Context(w.m, list(w.dims), w.act)
+    ctx.load_weights(load_golden_blob(w.blob))
+    opts = sl7.make_opts(prec=sl7.PREC_BF16, colloc=sl7.COLLOC_ANN)
+    ref, _ = ctx.simulate(w.y0, 1 / 8, 8, (), 20_000, 3, sl7.OUT_TERMINAL, opts)
+    torch.cuda.synchronize()
+    for v in ("1", "9", "11"):
+        monkeypatch.setenv("SL7_TC_VARIANT", v)
+        out, _ = ctx.simulate(w.y0, 1 / 8, 8, (), 20_000, 3, sl7.OUT_TERMINAL, opts)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref), v
