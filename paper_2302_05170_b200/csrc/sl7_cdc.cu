@@ -56,16 +56,19 @@ __device__ __forceinline__ void warp_hist_add(uint32_t* h, int bin) {   // bin <
 // within that group.  Entries hold slot + 1 (0: no slot).
 constexpr int kCdcLutBytes = 65536 + kCdcMaxT * 256;
 
-template <int U>
-__global__ void __launch_bounds__(256) cdc_hist_kernel(const float* __restrict__ y, uint64_t n, int pass,
+// PASS is a template parameter: with a runtime pass the per-element code carried every pass's branches
+// (and their divergence bookkeeping) for each element.
+template <int U, int PASS>
+__global__ void __launch_bounds__(256) cdc_hist_kernel(const float* __restrict__ y, uint64_t n,
                                                        const CdcScratch* s, unsigned long long* __restrict__ hist) {
+  constexpr int pass = PASS;
   extern __shared__ uint4 lut4[];
   uint8_t* lut16 = reinterpret_cast<uint8_t*>(lut4);        // [65536] (pass 1 uses the first 256)
   uint8_t* lut3 = lut16 + 65536;                             // [groups][256] (pass 3)
   __shared__ uint32_t h[kCdcMaxT * 256];
   const int nslot = s->nslot;
   for (int i = threadIdx.x; i < nslot * 256; i += blockDim.x) h[i] = 0u;
-  if (pass > 0) {
+  if constexpr (PASS > 0) {
     const int words = (pass == 1) ? 256 / 16 : kCdcLutBytes / 16;
     for (int i = threadIdx.x; i < words; i += blockDim.x) lut4[i] = make_uint4(0u, 0u, 0u, 0u);
     __syncthreads();
@@ -89,37 +92,65 @@ __global__ void __launch_bounds__(256) cdc_hist_kernel(const float* __restrict__
   __syncthreads();
   const int shift = 24 - 8 * pass;
   const int lane = threadIdx.x & 31;
-  // each warp takes chunks of 32 U consecutive elements: U coalesced loads in flight per thread (the LUT
-  // passes run at 2 blocks per SM, so they need the deeper chunks to keep HBM busy)
-  const uint64_t wstride = (uint64_t)gridDim.x * blockDim.x * U;
-  for (uint64_t base = ((uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) * U; base < n; base += wstride) {
-    float v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint64_t q = base + 32 * u + lane;
-      v[u] = (q < n) ? y[q] : __int_as_float(0x7F800000);   // +inf: skipped below
+  // the bin of one element (-1: not counted in this pass)
+  auto bin_of = [&](float x) -> int {
+    if (!isfinite(x)) return -1;
+    const uint32_t key = f2key(x);
+    const int digit = (int)((key >> shift) & 255u);
+    if constexpr (PASS == 0) return digit;
+    int slot;
+    if constexpr (PASS < 3) {
+      slot = (int)lut16[key >> (shift + 8)] - 1;
+    } else {
+      const int g = (int)lut16[key >> 16];
+      slot = g ? (int)lut3[(g - 1) * 256 + ((key >> 8) & 255u)] - 1 : -1;
     }
+    return slot >= 0 ? slot * 256 + digit : -1;
+  };
+  auto count = [&](int bin) {   // all lanes of the warp call it (pass 0 aggregates per warp)
+    if constexpr (PASS == 0) warp_hist_add(h, bin);
+    else if (bin >= 0) atomicAdd(&h[bin], 1u);
+  };
+  if ((reinterpret_cast<uintptr_t>(y) & 15u) == 0) {
+    // 16-byte loads: each thread takes U/4 float4 per chunk (a warp reads 512 contiguous bytes per load),
+    // so the per-element index arithmetic and bounds checks are amortised over four elements
+    constexpr int V = (U + 3) / 4;
+    const float4* y4 = reinterpret_cast<const float4*>(y);
+    const uint64_t n4 = n >> 2;
+    const uint64_t wstride = (uint64_t)gridDim.x * blockDim.x * V;
+    for (uint64_t base = ((uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) * V; base < n4; base += wstride) {
+      float4 v[V];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      int bin = -1;
-      if (isfinite(v[u])) {
-        const uint32_t key = f2key(v[u]);
-        const int digit = (int)((key >> shift) & 255u);
-        if (pass == 0) {
-          bin = digit;
-        } else {
-          int slot;
-          if (pass < 3) {
-            slot = (int)lut16[key >> (shift + 8)] - 1;
-          } else {
-            const int g = (int)lut16[key >> 16];
-            slot = g ? (int)lut3[(g - 1) * 256 + ((key >> 8) & 255u)] - 1 : -1;
-          }
-          if (slot >= 0) bin = slot * 256 + digit;
-        }
+      for (int u = 0; u < V; ++u) {
+        const uint64_t q = base + 32 * u + lane;
+        const float inf = __int_as_float(0x7F800000);   // +inf: skipped
+        v[u] = (q < n4) ? y4[q] : make_float4(inf, inf, inf, inf);
       }
-      if (pass == 0) warp_hist_add(h, bin);              // few distinct bins: aggregate per warp
-      else if (bin >= 0) atomicAdd(&h[bin], 1u);
+#pragma unroll
+      for (int u = 0; u < V; ++u) {
+        count(bin_of(v[u].x));
+        count(bin_of(v[u].y));
+        count(bin_of(v[u].z));
+        count(bin_of(v[u].w));
+      }
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 32) {   // the n % 4 tail, one warp (all lanes call count)
+      const uint64_t q = (n4 << 2) + lane;
+      count(q < n ? bin_of(y[q]) : -1);
+    }
+  } else {
+    // each warp takes chunks of 32 U consecutive elements: U coalesced loads in flight per thread (the LUT
+    // passes run at 2 blocks per SM, so they need the deeper chunks to keep HBM busy)
+    const uint64_t wstride = (uint64_t)gridDim.x * blockDim.x * U;
+    for (uint64_t base = ((uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) * U; base < n; base += wstride) {
+      float v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t q = base + 32 * u + lane;
+        v[u] = (q < n) ? y[q] : __int_as_float(0x7F800000);   // +inf: skipped below
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) count(bin_of(v[u]));
     }
   }
   __syncthreads();
@@ -449,13 +480,16 @@ int cdc_hist(const RunParams& p, void* scratch, const float* y, int pass, unsign
     if (e != cudaSuccess) return (int)e;
   }
   const CdcScratch* sc = reinterpret_cast<const CdcScratch*>(scratch);
-  if (pass < 2) {
-    cdc_hist_kernel<4><<<cdc_grid(p.n_paths, num_sms), 256, pass ? 256 : 0, st>>>(y, p.n_paths, pass, sc, hist);
+  const unsigned grid = cdc_grid(p.n_paths, num_sms);
+  if (pass == 0) {
+    cdc_hist_kernel<4, 0><<<grid, 256, 0, st>>>(y, p.n_paths, sc, hist);
+  } else if (pass == 1) {
+    cdc_hist_kernel<4, 1><<<grid, 256, 256, st>>>(y, p.n_paths, sc, hist);
   } else {
-    const cudaError_t e = cudaFuncSetAttribute(cdc_hist_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               kCdcLutBytes);
+    auto k = (pass == 2) ? cdc_hist_kernel<16, 2> : cdc_hist_kernel<16, 3>;
+    const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kCdcLutBytes);
     if (e != cudaSuccess) return (int)e;
-    cdc_hist_kernel<16><<<cdc_grid(p.n_paths, num_sms), 256, kCdcLutBytes, st>>>(y, p.n_paths, pass, sc, hist);
+    k<<<grid, 256, kCdcLutBytes, st>>>(y, p.n_paths, sc, hist);
   }
   return (int)cudaGetLastError();
 }
