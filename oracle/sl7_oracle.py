@@ -494,6 +494,11 @@ def cdc_step_error_scale(spec: Spec, Y, Z) -> np.ndarray:
     the table entries (as in step_error_scale)."""
     Y = np.asarray(Y, dtype=np.float64)
     z, C = cdc_table(spec, Y)
+    return _cdc_error_scale(spec, z, C, Y, Z)
+
+
+def _cdc_error_scale(spec: Spec, z, C, Y, Z) -> np.ndarray:
+    Y = np.asarray(Y, dtype=np.float64)
     if spec.colloc == "ann":
         S = mlp_abs_scale(spec.net, ann_features(z, spec.dt, spec.theta), spec.quant)
     elif spec.colloc == "ou":
@@ -514,6 +519,53 @@ def cdc_step(spec: Spec, Y, Z) -> np.ndarray:
     """One CDC step of every path from the states Y (all paths) with normals Z."""
     z, C = cdc_table(spec, Y)
     return lagrange_eval(Z, spec.x, cdc_points(z, C, Y))
+
+
+# 7L-CDC with predicted marginal points (SL7_SCHEME_CDC_PRED, reading R-26 of DESIGN.md): PAPER.md:106
+# "only requires the ANNs to compute a small number of marginal collocation points" read literally --
+# the marginal collocation points of Y(t_i) are the predictor's own at (Y0, horizon t_i = i dt, theta);
+# the table and the per-path interpolation are those of cdc_step, at the path's state clamped to the
+# marginal hull [z_0, z_{m-1}].  At t_0 every path is at Y0 (the repeated-point rule R-20 gives row 0).
+# The paths are independent: any subset can be simulated alone.
+
+
+def cdc_pred_marginals(spec: Spec, i: int) -> np.ndarray:
+    """Marginal collocation points z (m,) of Y(t_i) given Y(0) = y0."""
+    if i == 0:
+        return np.full(spec.m, spec.y0)
+    horizon = Spec(spec.m, spec.colloc, spec.theta, spec.y0, i * spec.dt, spec.n_steps, spec.net, spec.quant)
+    return horizon.points(np.array([spec.y0]))[0]
+
+
+def cdc_pred_state(z, Y) -> np.ndarray:
+    """The state at which a path reads the table: clamped to the marginal hull [z_0, z_{m-1}] (R-26: the
+    table is extended flat beyond its extreme rows instead of by the degree-(m-1) polynomial); NaN stays
+    NaN.  Repeated or unordered z (nearest-row rule R-20): the state as it is."""
+    Y = np.asarray(Y, dtype=np.float64)
+    return np.clip(Y, z[0], z[-1]) if np.all(np.diff(z) > 0) else Y
+
+
+def cdc_pred_step(spec: Spec, i: int, Y, Z) -> np.ndarray:
+    """Step i of every path: table C[k] = H(z_k, dt, theta) on the predicted marginal points."""
+    z = cdc_pred_marginals(spec, i)
+    return lagrange_eval(Z, spec.x, cdc_points(z, spec.points(z), cdc_pred_state(z, Y)))
+
+
+def simulate_cdc_pred(spec: Spec, seed: int, paths) -> tuple[np.ndarray, np.ndarray]:
+    """7L-CDC with predicted marginal points over the paths `paths` (global ids)."""
+    paths = np.asarray(paths, dtype=np.uint64)
+    Z = normals(seed, paths, spec.n_steps)
+    Y = np.empty((spec.n_steps + 1, len(paths)))
+    Y[0] = spec.y0
+    for i in range(spec.n_steps):
+        Y[i + 1] = cdc_pred_step(spec, i, Y[i], Z[i])
+    return Y, Z
+
+
+def cdc_pred_step_error_scale(spec: Spec, i: int, Y, Z) -> np.ndarray:
+    """Forward-error scale of cdc_pred_step (tolerance helper): as cdc_step_error_scale on z_i."""
+    z = cdc_pred_marginals(spec, i)
+    return _cdc_error_scale(spec, z, spec.points(z), cdc_pred_state(z, Y), Z)
 
 
 def exact_reference(process: str, theta, y0, dt, Z) -> np.ndarray:

@@ -1,0 +1,99 @@
+"""Pins of the 7L-CDC oracle with predicted marginal points (SL7_SCHEME_CDC_PRED; "only
+requires the ANNs to compute a small number of marginal collocation points"; reading R-26 of DESIGN.md),
+CPU only."""
+import numpy as np
+import pytest
+import scipy.stats
+
+from oracle import sl7_oracle as O
+from sl7_inputs import load_golden_blob, workloads
+
+
+def test_gbm_marginals_are_lognormal_quantiles():
+    # the exact GBM predictor at horizon t_i from Y0: the quantiles of the lognormal law of Y(t_i) at
+    # Phi(x_k) (library: scipy.stats.lognorm.ppf)
+    mu, s, y0, dt = 0.05, 0.2, 1.3, 0.25
+    spec = O.Spec(7, "gbm", (mu, s), y0, dt, 8)
+    for i in (1, 3, 7):
+        t = i * dt
+        ref = scipy.stats.lognorm.ppf(scipy.stats.norm.cdf(spec.x), s=s * np.sqrt(t),
+                                      scale=y0 * np.exp((mu - 0.5 * s * s) * t))
+        np.testing.assert_allclose(O.cdc_pred_marginals(spec, i), ref, rtol=1e-12)
+
+
+def test_ou_marginals_are_normal_quantiles():
+    # Eq. 6.6 at horizon t_i: N(Ybar + (Y0 - Ybar) e^{-lam t}, s^2 (1 - e^{-2 lam t}) / (2 lam))
+    ybar, lam, s, y0, dt = 0.3, 1.5, 0.5, 1.0, 0.125
+    spec = O.Spec(5, "ou", (ybar, lam, s), y0, dt, 16)
+    for i in (1, 5, 15):
+        t = i * dt
+        e = np.exp(-lam * t)
+        ref = scipy.stats.norm.ppf(scipy.stats.norm.cdf(spec.x), loc=ybar + (y0 - ybar) * e,
+                                   scale=s * np.sqrt((1 - e * e) / (2 * lam)))
+        np.testing.assert_allclose(O.cdc_pred_marginals(spec, i), ref, rtol=1e-12, atol=1e-14)
+
+
+def test_step_zero_is_row_zero():
+    # t_0: every path at Y0, so all marginal points repeat and R-20's nearest row (row 0 = H(Y0)) applies
+    spec = O.Spec(5, "ou", (0.0, 1.0, 0.5), 1.0, 0.25, 3)
+    assert np.all(O.cdc_pred_marginals(spec, 0) == 1.0)
+    Y = np.full(4, 1.0)
+    Z = np.array([-2.0, -0.1, 0.3, 4.0])
+    ref = O.lagrange_eval(Z, spec.x, np.tile(spec.points(np.array([1.0]))[0], (4, 1)))
+    np.testing.assert_allclose(O.cdc_pred_step(spec, 0, Y, Z), ref, rtol=1e-15)
+
+
+@pytest.mark.parametrize("colloc, theta, m", [("ou", (0.0, 1.0, 0.5), 7), ("ou", (0.4, 0.3, 1.2), 5),
+                                              ("gbm", (0.05, 0.2), 5), ("gbm", (0.1, 0.4), 7)])
+def test_cdc_pred_equals_7l_step_for_affine_collocation(colloc, theta, m):
+    # exact OU (affine in the state) and exact GBM (linear): the Lagrange interpolant of the table in the
+    # state reproduces it exactly, so a CDC_PRED step is the 7L step from the state clamped to the hull
+    # (the same 7L step inside it); checked one step at a time on 7L's own states
+    spec = O.Spec(m, colloc, theta, 1.0, 0.25, 8)
+    paths = np.arange(4000, dtype=np.uint64) * np.uint64(7919)
+    Y7, Z = O.simulate(spec, 11, paths)
+    outside = 0
+    for i in range(spec.n_steps):
+        z = O.cdc_pred_marginals(spec, i)
+        Yc = np.clip(Y7[i], z[0], z[-1]) if i > 0 else Y7[i]
+        outside += int(np.sum(Yc != Y7[i]))
+        ref = O.step(spec, Yc, Z[i])
+        np.testing.assert_allclose(O.cdc_pred_step(spec, i, Y7[i], Z[i]), ref, rtol=1e-9, atol=1e-11)
+        inside = Yc == Y7[i]
+        np.testing.assert_allclose(O.cdc_pred_step(spec, i, Y7[i], Z[i])[inside], Y7[i + 1][inside], rtol=1e-9,
+                                   atol=1e-11)
+    assert outside > 0          # the clamp was exercised
+
+
+def test_hull_clamp_is_flat_extension():
+    # beyond the extreme marginal points a path reads the extreme table row (hand-built table)
+    spec = O.Spec(5, "ou", (0.0, 1.0, 0.5), 1.0, 0.25, 3)
+    z = O.cdc_pred_marginals(spec, 2)
+    C = spec.points(z)
+    Y = np.array([z[0] - 5.0, z[-1] + 3.0, np.nan])
+    P = O.cdc_points(z, C, O.cdc_pred_state(z, Y))
+    np.testing.assert_allclose(P[0], C[0], rtol=1e-13)
+    np.testing.assert_allclose(P[1], C[-1], rtol=1e-13)
+    assert np.all(np.isnan(P[2]))
+
+
+def test_paths_are_independent():
+    # no cross-path coupling: a subset simulated alone equals the same paths inside a larger set
+    w = workloads()["cfg0"]
+    spec = O.Spec(w.m, "ann", (), w.y0, w.dt, w.n_steps, net=O.parse_blob(load_golden_blob(w.blob)))
+    big = np.arange(500, dtype=np.uint64)
+    Yb, _ = O.simulate_cdc_pred(spec, 5, big)
+    Ys, _ = O.simulate_cdc_pred(spec, 5, big[123:130])
+    np.testing.assert_array_equal(Ys, Yb[:, 123:130])
+
+
+def test_cir_network_stays_bounded():
+    # the motivating property (R-25/R-26): on cfg2's CIR network the empirical-quantile CDC
+    # diverges; with predicted marginal points every state stays finite and within the network's range
+    w = workloads()["cfg2_cir"]
+    spec = O.Spec(w.m, "ann", tuple(w.theta), w.y0, w.dt, w.n_steps, net=O.parse_blob(load_golden_blob(w.blob)))
+    with np.errstate(all="ignore"):
+        Y, _ = O.simulate_cdc_pred(spec, w.seed, np.arange(20_000, dtype=np.uint64))
+    assert np.all(np.isfinite(Y))
+    assert np.abs(Y).max() < 2.0
+    assert abs(Y[-1].mean() - 0.1) < 0.02          # analytic CIR mean 0.1 (network extrapolated to t > 1)
