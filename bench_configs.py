@@ -236,7 +236,9 @@ def main():
                      ("ann_split_bf16x3_tcgen05", ctx, sl7.COLLOC_ANN, sl7.PREC_SPLIT, 0, w.theta, N),
                      ("ann_fp32", ctx, sl7.COLLOC_ANN, sl7.PREC_FP32, 0, w.theta, N // 10),
                      ("cdc_ann_fp32_table", ctx, sl7.COLLOC_ANN, sl7.PREC_FP32, -1, w.theta, N),
-                     ("cdc_ann_fp32_table_fast_normals", ctx, sl7.COLLOC_ANN, sl7.PREC_FP32, -2, w.theta, N)]
+                     ("cdc_ann_fp32_table_fast_normals", ctx, sl7.COLLOC_ANN, sl7.PREC_FP32, -2, w.theta, N),
+                     ("cdc_pred_ann_fp32_table", ctx, sl7.COLLOC_ANN, sl7.PREC_FP32, -3, w.theta, N),
+                     ("cdc_pred_ann_fp32_table_fast_normals", ctx, sl7.COLLOC_ANN, sl7.PREC_FP32, -4, w.theta, N)]
             if w.process == "cir":
                 ex = sl7.Context(w.m, device=0)
                 modes += [("exact_cir_ncx2_fp64", ex, sl7.COLLOC_EXACT_CIR, sl7.PREC_FP32, 0, w.theta, N // 100)]
@@ -246,12 +248,14 @@ def main():
                           ("exact_ou_fast_specialized", ex, sl7.COLLOC_EXACT_OU, sl7.PREC_FP32,
                            sl7.FLAG_FAST_NORMALS | sl7.FLAG_SPECIALIZED, w.theta, N)]
             for label, c, colloc, prec, flags, theta, n_paths in modes:
-                cdc = flags < 0              # markers: 7L-CDC scheme (-2: with SL7_FLAG_FAST_NORMALS)
+                # markers: 7L-CDC scheme (-1, -2) or CDC_PRED (-3, -4); -2, -4 with SL7_FLAG_FAST_NORMALS
+                cdc = flags < 0
+                scheme = (sl7.SCHEME_CDC if flags in (-1, -2) else sl7.SCHEME_CDC_PRED) if cdc else sl7.SCHEME_7L
                 ref = sl7.REF_OU if (w.process == "ou" and not cdc) else sl7.REF_NONE
-                fl = (sl7.FLAG_FAST_NORMALS if flags == -2 else 0) if cdc else flags
+                fl = (sl7.FLAG_FAST_NORMALS if flags in (-2, -4) else 0) if cdc else flags
                 opts = sl7.make_opts(prec=prec, colloc=colloc, stream=stream, flags=fl, n_bins=4096,
                                      hist_lo=lo, hist_hi=hi, shift=w.y0, ref=ref, ref_theta=w.theta,
-                                     scheme=sl7.SCHEME_CDC if cdc else sl7.SCHEME_7L)
+                                     scheme=scheme)
                 fn = (lambda c=c, theta=theta, opts=opts, n_paths=n_paths:
                       c.simulate(w.y0, w.dt, w.n_steps, theta, n_paths, w.seed, sl7.OUT_STATS, opts, stats=stats))
                 clk = ClockSampler(0)

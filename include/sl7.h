@@ -107,8 +107,13 @@ typedef enum { SL7_REF_NONE = 0, SL7_REF_GBM = 1, SL7_REF_OU = 2 } sl7_ref;
  * select on the device), and each path's conditional points are the Lagrange interpolant of the table
  * rows on the z_k at its own state; repeated z_k (step 0) use the nearest row.  The marginal points
  * couple the paths, so one sl7_simulate CDC call holds the whole path set (opts->ref must be NONE); runs
- * sharded over ranks use the sl7_cdc_* calls below. */
-typedef enum { SL7_SCHEME_7L = 0, SL7_SCHEME_CDC = 1 } sl7_scheme;
+ * sharded over ranks use the sl7_cdc_* calls below.
+ * CDC_PRED: the 7L-CDC variant with the marginal collocation points taken from the predictor itself,
+ * z_k(t_i) = H(Y0, t_i = i dt, theta)_k ("only requires the ANNs to compute a small number of marginal
+ * collocation points"; reading R-26 of DESIGN.md); t_0 has every path at Y0 (nearest row).
+ * The table is then the same for every path set, so there are no selection passes and no exchange:
+ * shard it like SL7_SCHEME_7L with path_offset.  The network must be fitted for horizons up to T. */
+typedef enum { SL7_SCHEME_7L = 0, SL7_SCHEME_CDC = 1, SL7_SCHEME_CDC_PRED = 2 } sl7_scheme;
 
 typedef struct {
   sl7_prec prec;            /* ANN arithmetic (ignored by the exact modes) */
@@ -122,7 +127,7 @@ typedef struct {
   sl7_ref ref;              /* strong-error reference (SL7_REF_NONE: E1 = E2 = 0) */
   double ref_theta[3];
   uint32_t flags;           /* SL7_FLAG_* below; 0 = defaults */
-  sl7_scheme scheme;        /* SL7_SCHEME_7L (Algorithm I) or SL7_SCHEME_CDC */
+  sl7_scheme scheme;        /* SL7_SCHEME_7L (Algorithm I), SL7_SCHEME_CDC or SL7_SCHEME_CDC_PRED */
 } sl7_run_opts;
 
 /* opts->flags (exact-collocation modes and 7L-CDC (FAST_NORMALS only); ignored by the 7L ANN kernels):

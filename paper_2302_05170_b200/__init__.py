@@ -38,7 +38,7 @@ class sl7_run_opts(ctypes.Structure):
                 ("scheme", ctypes.c_int)]
 
 
-SCHEME_7L, SCHEME_CDC = 0, 1
+SCHEME_7L, SCHEME_CDC, SCHEME_CDC_PRED = 0, 1, 2
 
 
 FLAG_FAST_NORMALS = 1

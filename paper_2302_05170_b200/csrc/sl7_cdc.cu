@@ -39,6 +39,25 @@ struct CdcScratch {
   double zd[kMaxM];
 };
 
+// From the double marginal points s->zd[0..m): the fp32 hi/lo split, the scaled barycentric weights and
+// the degenerate flag the step kernel reads (one thread).
+__device__ void cdc_finalize_marginals(CdcScratch* s, int m, int degen) {
+  s->degenerate = degen;
+  for (int k = 0; k < m; ++k) {
+    s->z[k] = (float)s->zd[k];
+    s->zlo[k] = (float)(s->zd[k] - (double)s->z[k]);
+    // barycentric weights of the nodes scaled to O(1) spacing: the normalised formula is invariant to a
+    // common scale of all (Y - z_k), and for m up to 16 nodes the unscaled products under/overflow fp32
+    const double sc = (!degen && m > 1) ? 0.5 * (s->zd[m - 1] - s->zd[0]) : 1.0;
+    double w = 1.0;
+    if (!degen)
+      for (int l = 0; l < m; ++l)
+        if (l != k) w *= (s->zd[k] - s->zd[l]) / sc;
+    s->v[k] = degen ? 0.0f : (float)(1.0 / w);
+    if (k == 0) s->sinv = (float)(1.0 / sc);
+  }
+}
+
 // ---- pass p: histogram of digit p (bits [24 - 8p, 32 - 8p)) of the elements matching a slot prefix.
 // The states of one step are concentrated in a few digit bins, so the shared-memory increments are
 // warp-aggregated (__match_any_sync: one atomic per distinct bin per warp) instead of one per element.
@@ -261,20 +280,7 @@ __global__ void __launch_bounds__(1024) cdc_scan_kernel(int pass, int m, CdcScra
                               : __longlong_as_double(0x7FF8000000000000ll);
         if (k > 0 && !(s->zd[k] > s->zd[k - 1])) degen = 1;   // repeated (or NaN) marginal points
       }
-      s->degenerate = degen;
-      for (int k = 0; k < m; ++k) {
-        s->z[k] = (float)s->zd[k];
-        s->zlo[k] = (float)(s->zd[k] - (double)s->z[k]);
-        // barycentric weights of the nodes scaled to O(1) spacing: the normalised formula is invariant to a
-        // common scale of all (Y - z_k), and for m up to 16 nodes the unscaled products under/overflow fp32
-        const double sc = (!degen && m > 1) ? 0.5 * (s->zd[m - 1] - s->zd[0]) : 1.0;
-        double w = 1.0;
-        if (!degen)
-          for (int l = 0; l < m; ++l)
-            if (l != k) w *= (s->zd[k] - s->zd[l]) / sc;
-        s->v[k] = degen ? 0.0f : (float)(1.0 / w);
-        if (k == 0) s->sinv = (float)(1.0 / sc);
-      }
+      cdc_finalize_marginals(s, m, degen);
     }
   }
   __syncthreads();
@@ -295,22 +301,25 @@ __global__ void cdc_table_exact_kernel(const __grid_constant__ RunParams p, CdcS
   s->C[k][j] = (p.colloc == kExactGbm) ? zk * p.c[j] : fmaf(p.ou_a, zk, p.ou_b) + p.c[j];
 }
 
-// MLP on the m marginal points, fp32 with the accurate activations of the FP32 kernel.  The weight
-// image is the FP32 kernel's (hidden layers W[H][HS] + b, then output rows).
+// MLP on `rows` states zin[0..rows), fp32 with the accurate activations of the FP32 kernel, layer 1 folded
+// with the bias l1b (the horizon's dt and theta); out[k][j] = res_y zin[k] + a_j osc_j + osh_j.  The weight
+// image is the FP32 kernel's (hidden layers W[H][HS] + b, then output rows).  Block-wide (all threads call).
 template <int ACT>
-__global__ void __launch_bounds__(256) cdc_table_mlp_kernel(const __grid_constant__ RunParams p, CdcScratch* s) {
+__device__ void cdc_mlp_rows(const RunParams& p, const float* l1b, const float* osc, const float* osh,
+                             const float* zin, int rows, float (*out)[kMaxM]) {
   __shared__ float h[kMaxM][kMaxW], g[kMaxM][kMaxW];
   const int m = p.m, H = p.width, HS = (H == 50) ? 52 : 64, L = p.n_hidden;
   const int MR = (H == 50) ? m : kMaxM;
-  for (int i = threadIdx.x; i < m * kMaxW; i += blockDim.x) {
+  __syncthreads();
+  for (int i = threadIdx.x; i < rows * kMaxW; i += blockDim.x) {
     const int k = i / kMaxW, u = i % kMaxW;
-    h[k][u] = (u < H) ? activate<ACT>(fmaf(p.l1w[u], s->z[k], p.l1b[u])) : 0.0f;
+    h[k][u] = (u < H) ? activate<ACT>(fmaf(p.l1w[u], zin[k], l1b[u])) : 0.0f;
   }
   __syncthreads();
   for (int l = 0; l < L - 1; ++l) {
     const float* W = p.wdev + (size_t)l * f32_layer_floats(H, HS);
     const float* b = W + (size_t)H * HS;
-    for (int i = threadIdx.x; i < m * kMaxW; i += blockDim.x) {
+    for (int i = threadIdx.x; i < rows * kMaxW; i += blockDim.x) {
       const int k = i / kMaxW, u = i % kMaxW;
       float a = 0.0f;
       if (u < H) {
@@ -321,16 +330,60 @@ __global__ void __launch_bounds__(256) cdc_table_mlp_kernel(const __grid_constan
       g[k][u] = a;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < m * kMaxW; i += blockDim.x) h[i / kMaxW][i % kMaxW] = g[i / kMaxW][i % kMaxW];
+    for (int i = threadIdx.x; i < rows * kMaxW; i += blockDim.x) h[i / kMaxW][i % kMaxW] = g[i / kMaxW][i % kMaxW];
     __syncthreads();
   }
   const float* Wo = p.wdev + (size_t)(L - 1) * f32_layer_floats(H, HS);
   const float* bo = Wo + (size_t)MR * HS;
-  for (int i = threadIdx.x; i < m * m; i += blockDim.x) {
+  for (int i = threadIdx.x; i < rows * m; i += blockDim.x) {
     const int k = i / m, j = i % m;
     float a = bo[j];
     for (int v = 0; v < H; ++v) a = fmaf(Wo[(size_t)j * HS + v], h[k][v], a);
-    s->C[k][j] = fmaf(p.res_y, s->z[k], fmaf(a, p.out_scale[j], p.out_shift[j]));
+    out[k][j] = fmaf(p.res_y, zin[k], fmaf(a, osc[j], osh[j]));
+  }
+  __syncthreads();
+}
+
+// table rows C[k][.] = H(z_k) with the network (the run's dt)
+template <int ACT>
+__global__ void __launch_bounds__(256) cdc_table_mlp_kernel(const __grid_constant__ RunParams p, CdcScratch* s) {
+  cdc_mlp_rows<ACT>(p, p.l1b, p.out_scale, p.out_shift, s->z, p.m, s->C);
+}
+
+// SL7_SCHEME_CDC_PRED (reading R-26): the marginal collocation points of Y(t_i) are the predictor's at
+// (Y0, t_i = i dt, theta) -- the horizon's folded constants hz -- instead of quantiles of the paths
+// (t_0: every path at Y0, a degenerate table); then the table rows as above.  One block.
+template <int ACT>
+__global__ void __launch_bounds__(256) cdc_table_pred_kernel(const __grid_constant__ RunParams p,
+                                                             const __grid_constant__ CdcHorizon hz, CdcScratch* s,
+                                                             int step) {
+  __shared__ float zr[1][kMaxM];
+  const int m = p.m;
+  if (step > 0 && p.colloc == kAnn) {
+    cdc_mlp_rows<ACT>(p, hz.l1b, hz.osc, hz.osh, &p.y0, 1, zr);
+  } else if (threadIdx.x < m) {
+    const int j = threadIdx.x;
+    zr[0][j] = (step == 0) ? p.y0
+             : (p.colloc == kExactGbm) ? p.y0 * hz.c[j] : fmaf(hz.ou_a, p.y0, hz.ou_b) + hz.c[j];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int degen = 0;
+    for (int k = 0; k < m; ++k) {
+      s->zd[k] = (double)zr[0][k];
+      if (k > 0 && !(s->zd[k] > s->zd[k - 1])) degen = 1;   // repeated, unordered or NaN points
+    }
+    cdc_finalize_marginals(s, m, degen);
+  }
+  __syncthreads();
+  if (p.colloc == kAnn) {
+    cdc_mlp_rows<ACT>(p, p.l1b, p.out_scale, p.out_shift, s->z, m, s->C);
+  } else {
+    for (int i = threadIdx.x; i < m * m; i += blockDim.x) {
+      const int k = i / m, j = i % m;
+      const float zk = s->z[k];
+      s->C[k][j] = (p.colloc == kExactGbm) ? zk * p.c[j] : fmaf(p.ou_a, zk, p.ou_b) + p.c[j];
+    }
   }
 }
 
@@ -338,7 +391,8 @@ __global__ void __launch_bounds__(256) cdc_table_mlp_kernel(const __grid_constan
 template <int MR, bool RT_M, bool FAST = false>
 __global__ void __launch_bounds__(256) cdc_step_kernel(const __grid_constant__ RunParams p, const CdcScratch* s,
                                                        const float* yin, float* yout,   // may alias (in place)
-                                                       int step, int last, unsigned long long* next_hist) {
+                                                       int step, int last, unsigned long long* next_hist,
+                                                       int clamp_hull) {
   extern __shared__ uint32_t hist[];
   __shared__ double red[8];
   __shared__ float sz[kMaxM], szlo[kMaxM], sv[kMaxM], sC[kMaxM][kMaxM], ssinv;
@@ -398,7 +452,9 @@ __global__ void __launch_bounds__(256) cdc_step_kernel(const __grid_constant__ R
       float d[MR], pre[MR];
 #pragma unroll
       // Y - z_k with the marginal point carried as z + zlo (double-accurate nodes, as the GH grid's hi/lo)
-      for (int k = 0; k < MR; ++k) d[k] = (RT_M && k >= m) ? 1.0f : ((Y - sz[k]) - szlo[k]) * ssinv;
+      // CDC_PRED (R-26): the state clamped to the marginal hull (zlo = 0 there: the points are fp32); NaN stays
+      const float Yb = !clamp_hull ? Y : (Y < sz[0]) ? sz[0] : (Y > sz[m - 1]) ? sz[m - 1] : Y;
+      for (int k = 0; k < MR; ++k) d[k] = (RT_M && k >= m) ? 1.0f : ((Yb - sz[k]) - szlo[k]) * ssinv;
       pre[0] = 1.0f;
 #pragma unroll
       for (int k = 1; k < MR; ++k) pre[k] = pre[k - 1] * d[k - 1];
@@ -520,7 +576,7 @@ int cdc_advance(const RunParams& p, void* scratch, const float* yin, float* yout
     const cudaError_t e = cudaFuncSetAttribute(step_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hist);
     if (e != cudaSuccess) return (int)e;
   }
-  step_k<<<cdc_grid(p.n_paths, num_sms), 256, hist, st>>>(p, s, yin, yout, step, stats ? 1 : 0, next_hist);
+  step_k<<<cdc_grid(p.n_paths, num_sms), 256, hist, st>>>(p, s, yin, yout, step, stats ? 1 : 0, next_hist, 0);
   return (int)cudaGetLastError();
 }
 
@@ -544,6 +600,37 @@ int launch_cdc(const RunParams& p, const CdcLevels& lv, void* scratch, float* co
     }
     const bool last = (i == p.n_steps - 1);
     e = cdc_advance(p, scratch, yin, yout, i, last && p.has_stats, stream, num_sms, last ? nullptr : hist);
+    if (e) return e;
+  }
+  return 0;
+}
+
+// SL7_SCHEME_CDC_PRED: per step the predicted-marginal table, then the (unchanged) per-path step kernel.
+// No selection passes: paths are coupled only through the table, which is the same for any path set.
+int launch_cdc_pred(const RunParams& p, const CdcHorizon* hz, void* scratch, float* const* rows, int nrows,
+                    void* stream, int num_sms) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CdcScratch* s = reinterpret_cast<CdcScratch*>(scratch);
+  int e = cdc_fill(rows[0], p.n_paths, p.y0, stream, num_sms);   // row 0 = Y0
+  if (e) return e;
+  const size_t hist = (p.has_stats && p.n_bins > 0) ? sizeof(uint32_t) * (size_t)(p.n_bins + 2) : 0;
+  const bool fast = p.flags & SL7_FLAG_FAST_NORMALS;
+  auto step_k = (p.m == 5) ? (fast ? cdc_step_kernel<5, false, true> : cdc_step_kernel<5, false>)
+              : (p.m == 7) ? (fast ? cdc_step_kernel<7, false, true> : cdc_step_kernel<7, false>)
+                           : (fast ? cdc_step_kernel<kMaxM, true, true> : cdc_step_kernel<kMaxM, true>);
+  if (hist > 48 * 1024) {
+    const cudaError_t ce = cudaFuncSetAttribute(step_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hist);
+    if (ce != cudaSuccess) return (int)ce;
+  }
+  for (int i = 0; i < p.n_steps; ++i) {
+    if (p.act == SL7_ACT_TANH) cdc_table_pred_kernel<SL7_ACT_TANH><<<1, 256, 0, st>>>(p, hz[i], s, i);
+    else cdc_table_pred_kernel<SL7_ACT_SOFTPLUS><<<1, 256, 0, st>>>(p, hz[i], s, i);
+    const float* yin = rows[(nrows == 1) ? 0 : i];
+    float* yout = rows[(nrows == 1) ? 0 : i + 1];
+    const bool last = (i == p.n_steps - 1);
+    step_k<<<cdc_grid(p.n_paths, num_sms), 256, last ? hist : 0, st>>>(p, s, yin, yout, i, last && p.has_stats ? 1 : 0,
+                                                                       nullptr, 1);
+    e = (int)cudaGetLastError();
     if (e) return e;
   }
   return 0;

@@ -75,6 +75,7 @@ struct sl7_ctx_s {
   // sharded 7L-CDC run in progress (sl7_cdc_*)
   RunParams cdc_p;
   CdcLevels cdc_lv;
+  std::vector<CdcHorizon> cdc_hz;   // SL7_SCHEME_CDC_PRED: per-step predictor constants of the last call
   void* cdc_stream = nullptr;
   bool cdc_ready = false;
   // 7L-CDC scratch (selection histograms + table) and state buffer for STATS-only runs
@@ -496,7 +497,7 @@ sl7_status prepare(sl7_ctx c, double Y0, double dt, int32_t n_steps, const doubl
       const double kappa = theta[0], ybar = theta[1], s = theta[2];
       if (!(kappa > 0) || !(ybar > 0) || !(s > 0)) return fail(c, SL7_EINVAL, "theta: kappa, Ybar, sigma > 0");
       if (o->flags & SL7_FLAG_SPECIALIZED) return fail(c, SL7_EUNSUPPORTED, "EXACT_CIR: SL7_FLAG_SPECIALIZED");
-      if (o->scheme == SL7_SCHEME_CDC) return fail(c, SL7_EUNSUPPORTED, "EXACT_CIR: scheme CDC");
+      if (o->scheme != SL7_SCHEME_7L) return fail(c, SL7_EUNSUPPORTED, "EXACT_CIR: scheme CDC");
       p.cir_c = s * s * (-std::expm1(-kappa * dt)) / (4.0 * kappa);
       p.cir_d = 4.0 * kappa * ybar / (s * s);
       p.cir_lscale = std::exp(-kappa * dt) / p.cir_c;
@@ -551,15 +552,16 @@ sl7_status prepare(sl7_ctx c, double Y0, double dt, int32_t n_steps, const doubl
       return fail(c, SL7_EINVAL, "colloc");
   }
   if (o->flags & ~(SL7_FLAG_FAST_NORMALS | SL7_FLAG_SPECIALIZED)) return fail(c, SL7_EINVAL, "flags");
-  if (o->scheme != SL7_SCHEME_7L && o->scheme != SL7_SCHEME_CDC) return fail(c, SL7_EINVAL, "scheme");
-  if (o->scheme == SL7_SCHEME_CDC) {
+  if (o->scheme != SL7_SCHEME_7L && o->scheme != SL7_SCHEME_CDC && o->scheme != SL7_SCHEME_CDC_PRED)
+    return fail(c, SL7_EINVAL, "scheme");
+  if (o->scheme != SL7_SCHEME_7L) {
     if (o->ref != SL7_REF_NONE) return fail(c, SL7_EUNSUPPORTED, "scheme CDC: ref must be SL7_REF_NONE");
     if (o->flags & ~SL7_FLAG_FAST_NORMALS)
       return fail(c, SL7_EUNSUPPORTED, "scheme CDC: flags may only hold SL7_FLAG_FAST_NORMALS");
     if (p.colloc == kAnn && o->prec != SL7_PREC_FP32)
       return fail(c, SL7_EUNSUPPORTED, "scheme CDC: the m-row table runs in fp32 (prec must be SL7_PREC_FP32)");
   }
-  p.flags = (p.colloc == kAnn && o->scheme != SL7_SCHEME_CDC) ? 0u : o->flags;
+  p.flags = (p.colloc == kAnn && o->scheme == SL7_SCHEME_7L) ? 0u : o->flags;
   return SL7_OK;
 }
 
@@ -625,7 +627,7 @@ sl7_status run(sl7_ctx c, RunParams& p, const sl7_run_opts* o, float* d_out, dou
   int e;
   if (p.em_model != 0) {
     e = launch_em(p, o->stream, c->num_sms);
-  } else if (o->scheme == SL7_SCHEME_CDC) {
+  } else if (o->scheme == SL7_SCHEME_CDC || o->scheme == SL7_SCHEME_CDC_PRED) {
     // 7L-CDC: states in HBM between steps (FULL rows, the TERMINAL output, or context scratch)
     if (!c->d_cdc) {
       cudaError_t ce = cudaMalloc(&c->d_cdc, cdc_scratch_bytes());
@@ -651,7 +653,10 @@ sl7_status run(sl7_ctx c, RunParams& p, const sl7_run_opts* o, float* d_out, dou
     }
     CdcLevels lv;
     for (int k = 0; k < kMaxM; ++k) lv.p[k] = (k < c->m) ? 0.5 * std::erfc(-c->x[k] / std::sqrt(2.0)) : 0.0;
-    e = launch_cdc(p, lv, c->d_cdc, rows.data(), (int)rows.size(), o->stream, c->num_sms);
+    if (o->scheme == SL7_SCHEME_CDC_PRED)
+      e = launch_cdc_pred(p, c->cdc_hz.data(), c->d_cdc, rows.data(), (int)rows.size(), o->stream, c->num_sms);
+    else
+      e = launch_cdc(p, lv, c->d_cdc, rows.data(), (int)rows.size(), o->stream, c->num_sms);
   } else if (p.colloc == kAnn && (o->prec == SL7_PREC_BF16 || o->prec == SL7_PREC_SPLIT || o->prec == SL7_PREC_TF32)) {
     // per-run part of the TC parameters: layer 1 folded (as in RunParams) and pre-scaled in double
     TcParams t = c->tcp;
@@ -835,6 +840,24 @@ sl7_status sl7_simulate(sl7_ctx c, double Y0, double dt, int32_t n_steps, const 
   sl7_status s = prepare(c, Y0, dt, n_steps, theta, n_theta, n_paths, seed, out_mode, opts, p, d_out != nullptr,
                          d_stats != nullptr);
   if (s != SL7_OK) return s;
+  if (opts->scheme == SL7_SCHEME_CDC_PRED) {
+    // the predictor's constants at each horizon t_i = i dt (reading R-26), folded by the same code as the
+    // run's own (prepare with dt -> t_i); step 0 needs none (every path at Y0)
+    c->cdc_hz.assign((size_t)n_steps, CdcHorizon{});
+    for (int32_t i = 1; i < n_steps; ++i) {
+      RunParams q;
+      s = prepare(c, Y0, dt * (double)i, n_steps, theta, n_theta, n_paths, seed, out_mode, opts, q, d_out != nullptr,
+                  d_stats != nullptr);
+      if (s != SL7_OK) return s;
+      CdcHorizon& h = c->cdc_hz[(size_t)i];
+      std::memcpy(h.l1b, q.l1b, sizeof h.l1b);
+      std::memcpy(h.osc, q.out_scale, sizeof h.osc);
+      std::memcpy(h.osh, q.out_shift, sizeof h.osh);
+      std::memcpy(h.c, q.c, sizeof h.c);
+      h.ou_a = q.ou_a;
+      h.ou_b = q.ou_b;
+    }
+  }
   DeviceGuard g(c->device);
   if (!g.ok) return fail(c, SL7_ECUDA, "cudaSetDevice(%d)", c->device);
   return run(c, p, opts, out_mode == SL7_OUT_STATS ? nullptr : d_out, d_stats);

@@ -119,6 +119,17 @@ struct TcParams {
 struct CdcLevels {
   double p[kMaxM];
 };
+// SL7_SCHEME_CDC_PRED: the horizon-dependent constants of the predictor at (Y0, t_i = i dt), folded on
+// the host exactly as RunParams folds the run's dt (layer-1 bias, residual output scale; exact modes'
+// c_j and OU coefficients).  One per step, passed by value to the table kernel.
+struct CdcHorizon {
+  float l1b[kMaxW];
+  float osc[kMaxM], osh[kMaxM];
+  float c[kMaxM];
+  float ou_a, ou_b;
+};
+int launch_cdc_pred(const RunParams& p, const CdcHorizon* hz, void* scratch, float* const* rows, int nrows,
+                    void* stream, int num_sms);
 size_t cdc_scratch_bytes();
 int cdc_init_scratch(void* scratch, void* stream);
 // rows: nrows == 1 -> one in-place state buffer; nrows == n_steps + 1 -> FULL output rows.

@@ -1,0 +1,124 @@
+"""GPU parity of the 7L-CDC scheme with predicted marginal points (SL7_SCHEME_CDC_PRED, reading R-26 of
+DESIGN.md) against the float64 oracle, teacher-forced: per step the oracle recomputes the marginal
+points from the predictor at (Y0, t_i), the table and the per-path step from the device's stored states
+and the same normals; tolerance 1e-5 * kappa with the CDC forward-error scale.  The scheme couples no
+paths, so shards (path_offset) must reproduce the one-call run bit for bit."""
+import numpy as np
+import pytest
+
+from oracle import sl7_oracle as O
+from sl7_inputs import load_golden_blob, workloads
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    ("ou_exact", 7, "ou", (0.0, 1.0, 0.5), 1.0, 0.125, 16),
+    ("gbm_exact", 5, "gbm", (0.05, 0.2), 1.0, 0.25, 4),
+    ("cfg2_ou_ann", 7, "ann", None, None, None, 16),
+    ("cfg0_ann", 5, "ann", None, None, None, 2),
+    ("cfg2_cir_ann", 7, "ann", None, None, None, 16),
+]
+
+
+def _setup(sl7, name, m, colloc, theta, y0, dt, n_steps):
+    W = workloads()
+    if colloc == "ann":
+        w = W[{"cfg2_ou_ann": "cfg2_ou", "cfg0_ann": "cfg0", "cfg2_cir_ann": "cfg2_cir"}[name]]
+        blob = load_golden_blob(w.blob)
+        ctx = sl7.Context(w.m, list(w.dims), w.act)
+        ctx.load_weights(blob)
+        th = tuple(w.theta) if w.process != "gbm" else ()
+        return ctx, sl7.COLLOC_ANN, th, O.Spec(w.m, "ann", th, w.y0, w.dt, n_steps, net=O.parse_blob(blob))
+    ctx = sl7.Context(m)
+    code = sl7.COLLOC_EXACT_OU if colloc == "ou" else sl7.COLLOC_EXACT_GBM
+    return ctx, code, theta, O.Spec(m, colloc, theta, y0, dt, n_steps)
+
+
+@pytest.mark.parametrize("fast", [False, True])
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_cdc_pred_teacher_forced(gpu_lib, case, fast):
+    import torch
+    sl7 = gpu_lib
+    name, m, colloc, theta, y0, dt, n_steps = case
+    ctx, code, th, spec = _setup(sl7, name, m, colloc, theta, y0, dt, n_steps)
+    n_paths = 20_011
+    flags = sl7.FLAG_FAST_NORMALS if fast else 0
+    opts = sl7.make_opts(prec=sl7.PREC_FP32, colloc=code, scheme=sl7.SCHEME_CDC_PRED, flags=flags)
+    out, _ = ctx.simulate(spec.y0, spec.dt, n_steps, th, n_paths, 9, sl7.OUT_FULL, opts)
+    torch.cuda.synchronize()
+    Yd = out.double().cpu().numpy().reshape(n_steps + 1, n_paths)
+    assert np.all(Yd[0] == np.float32(spec.y0))
+    assert np.all(np.isfinite(Yd))
+    if fast:   # the fast Box-Muller is its own approximation: drive the oracle with the device's normals
+        z = torch.empty(n_steps * n_paths, dtype=torch.float32, device="cuda")
+        sl7.normals(9, 0, n_paths, n_steps, z, flags=sl7.FLAG_FAST_NORMALS)
+        torch.cuda.synchronize()
+        Z = z.double().cpu().numpy().reshape(n_steps, n_paths)
+    else:
+        Z = O.normals(9, np.arange(n_paths, dtype=np.uint64), n_steps)
+    worst = 0.0
+    with np.errstate(all="ignore"):
+        for i in range(n_steps):
+            ref = O.cdc_pred_step(spec, i, Yd[i], Z[i])
+            kappa = O.cdc_pred_step_error_scale(spec, i, Yd[i], Z[i])
+            r = np.abs(Yd[i + 1] - ref) / kappa
+            worst = max(worst, float(r.max()))
+            assert not (r > 1e-5).any(), "step %d: %d paths off, worst %.3g" % (i, int((r > 1e-5).sum()), r.max())
+    print("%s CDC_PRED teacher-forced worst |err|/kappa = %.3g" % (name, worst))
+
+
+def test_cdc_pred_shards_equal_one_call(gpu_lib):
+    # no exchange: two path_offset shards reproduce the one-call FULL output bit for bit
+    import torch
+    sl7 = gpu_lib
+    ctx, code, th, spec = _setup(sl7, "cfg2_cir_ann", 7, "ann", None, None, None, 16)
+    n, cut = 50_001, 17_389
+    o = sl7.make_opts(colloc=code, scheme=sl7.SCHEME_CDC_PRED)
+    full, _ = ctx.simulate(spec.y0, spec.dt, 16, th, n, 3, sl7.OUT_FULL, o)
+    a, _ = ctx.simulate(spec.y0, spec.dt, 16, th, cut, 3, sl7.OUT_FULL, o)
+    ob = sl7.make_opts(colloc=code, scheme=sl7.SCHEME_CDC_PRED, path_offset=cut)
+    b, _ = ctx.simulate(spec.y0, spec.dt, 16, th, n - cut, 3, sl7.OUT_FULL, ob)
+    torch.cuda.synchronize()
+    F = full.view(17, n).cpu()
+    assert torch.equal(F[:, :cut], a.view(17, cut).cpu())
+    assert torch.equal(F[:, cut:], b.view(17, n - cut).cpu())
+
+
+def test_cdc_pred_stats_match_full(gpu_lib):
+    import torch
+    sl7 = gpu_lib
+    ctx, code, th, spec = _setup(sl7, "cfg2_ou_ann", 7, "ann", None, None, None, 16)
+    n = 30_000
+    o = sl7.make_opts(colloc=code, scheme=sl7.SCHEME_CDC_PRED)
+    full, _ = ctx.simulate(spec.y0, spec.dt, 16, th, n, 4, sl7.OUT_FULL, o)
+    term, _ = ctx.simulate(spec.y0, spec.dt, 16, th, n, 4, sl7.OUT_TERMINAL, o)
+    st = torch.zeros(sl7.stats_elems(64), dtype=torch.float64, device="cuda")
+    os_ = sl7.make_opts(colloc=code, scheme=sl7.SCHEME_CDC_PRED, n_bins=64, hist_lo=-3, hist_hi=3, shift=0.0)
+    ctx.simulate(spec.y0, spec.dt, 16, th, n, 4, sl7.OUT_STATS, os_, stats=st)
+    torch.cuda.synchronize()
+    last = full[-n:].double().cpu().numpy()
+    assert np.array_equal(last, term.double().cpu().numpy())
+    v = O.stats_vector(last, 0.0, -3.0, 3.0, 64)
+    s = st.cpu().numpy()
+    assert s[0] == n and np.array_equal(s[8:], v[8:])
+    np.testing.assert_allclose(s[2:6], v[2:6], rtol=1e-12, atol=1e-9)
+
+
+def test_cdc_pred_cir_full_size_moments(gpu_lib):
+    # cfg2's CIR at its full 1e8 paths: finite and near the analytic mean (where the empirical-quantile
+    # CDC diverges, R-25); terminal moments vs the oracle on a 2e5-path prefix within MC noise
+    import torch
+    sl7 = gpu_lib
+    w = workloads()["cfg2_cir"]
+    ctx, code, th, spec = _setup(sl7, "cfg2_cir_ann", 7, "ann", None, None, None, w.n_steps)
+    st = torch.zeros(sl7.stats_elems(4096), dtype=torch.float64, device="cuda")
+    o = sl7.make_opts(colloc=code, scheme=sl7.SCHEME_CDC_PRED, n_bins=4096, hist_lo=0.0, hist_hi=0.6, shift=0.1)
+    ctx.simulate(w.y0, w.dt, w.n_steps, th, 100_000_000, w.seed, sl7.OUT_STATS, o, stats=st)
+    torch.cuda.synchronize()
+    v = st.cpu().numpy()
+    assert v[0] == 100_000_000 and v[1] == 0                     # count, non-finite count
+    mean = 0.1 + v[2] / v[0]
+    with np.errstate(all="ignore"):
+        Y, _ = O.simulate_cdc_pred(spec, w.seed, np.arange(200_000, dtype=np.uint64))
+    sd = Y[-1].std()
+    assert abs(mean - Y[-1].mean()) < 5 * sd / np.sqrt(2e5)
