@@ -39,9 +39,18 @@ struct CdcScratch {
   double zd[kMaxM];
 };
 
+// One step's CDC_PRED table (the fused kernel stages all steps' tables; same fields as CdcScratch's).
+struct CdcTable {
+  float z[kMaxM], zlo[kMaxM], v[kMaxM], C[kMaxM][kMaxM];
+  float sinv;
+  int degenerate;
+  double zd[kMaxM];
+};
+
 // From the double marginal points s->zd[0..m): the fp32 hi/lo split, the scaled barycentric weights and
 // the degenerate flag the step kernel reads (one thread).
-__device__ void cdc_finalize_marginals(CdcScratch* s, int m, int degen) {
+template <class T>
+__device__ void cdc_finalize_marginals(T* s, int m, int degen) {
   s->degenerate = degen;
   for (int k = 0; k < m; ++k) {
     s->z[k] = (float)s->zd[k];
@@ -353,10 +362,9 @@ __global__ void __launch_bounds__(256) cdc_table_mlp_kernel(const __grid_constan
 // SL7_SCHEME_CDC_PRED (reading R-26): the marginal collocation points of Y(t_i) are the predictor's at
 // (Y0, t_i = i dt, theta) -- the horizon's folded constants hz -- instead of quantiles of the paths
 // (t_0: every path at Y0, a degenerate table); then the table rows as above.  One block.
-template <int ACT>
+template <int ACT, class T>
 __global__ void __launch_bounds__(256) cdc_table_pred_kernel(const __grid_constant__ RunParams p,
-                                                             const __grid_constant__ CdcHorizon hz, CdcScratch* s,
-                                                             int step) {
+                                                             const __grid_constant__ CdcHorizon hz, T* s, int step) {
   __shared__ float zr[1][kMaxM];
   const int m = p.m;
   if (step > 0 && p.colloc == kAnn) {
@@ -500,6 +508,144 @@ __global__ void __launch_bounds__(256) cdc_step_kernel(const __grid_constant__ R
   }
 }
 
+// ---- CDC_PRED fused over all steps: the tables do not depend on the paths, so each thread carries P paths
+// through every step in registers (no state round trip through HBM, one launch), draws each Philox block once
+// per 4 steps (all four normals used, where the per-step kernel draws a block per step and keeps one), and
+// reads a step's table into registers once for its P paths.  All steps' tables are staged in shared memory.
+template <int MR>
+struct CdcSTab {
+  float C[MR][MR];
+  float z[MR], v[MR];
+  float sinv;
+  int deg;
+};
+constexpr int kCdcFusedP = 4;
+
+template <int MR, bool FAST>
+__device__ __forceinline__ float cdc_pred_path_step(const RunParams& p, const CdcSTab<MR>& T, const float (&Cr)[MR][MR],
+                                                    const float (&zr)[MR], const float (&vr)[MR], float sinv,
+                                                    float Y, float Z) {
+  float y[MR];
+  if (T.deg) {   // repeated / unordered marginal points (step 0): the nearest row, ties -> lowest k (R-20)
+    int kb = 0;
+    float db = fabsf(Y - zr[0]);
+#pragma unroll
+    for (int k = 1; k < MR; ++k) {
+      const float d = fabsf(Y - zr[k]);
+      if (d < db) { db = d; kb = k; }
+    }
+#pragma unroll
+    for (int j = 0; j < MR; ++j) y[j] = T.C[kb][j];
+  } else {
+    const float Yb = (Y < zr[0]) ? zr[0] : (Y > zr[MR - 1]) ? zr[MR - 1] : Y;   // hull clamp (R-26); NaN stays
+    float d[MR], pre[MR], lk[MR];
+#pragma unroll
+    for (int k = 0; k < MR; ++k) d[k] = (Yb - zr[k]) * sinv;
+    pre[0] = 1.0f;
+#pragma unroll
+    for (int k = 1; k < MR; ++k) pre[k] = pre[k - 1] * d[k - 1];
+    float suf = 1.0f, den = 0.0f;
+#pragma unroll
+    for (int k = MR - 1; k >= 0; --k) {
+      lk[k] = vr[k] * (pre[k] * suf);
+      den += lk[k];
+      suf *= d[k];
+    }
+    const float rden = __fdividef(1.0f, den);
+#pragma unroll
+    for (int j = 0; j < MR; ++j) {
+      float a = 0.0f;
+#pragma unroll
+      for (int k = 0; k < MR; ++k) a = fmaf(lk[k], Cr[k][j], a);
+      y[j] = a * rden;
+    }
+  }
+  return gm_eval<MR, false>(p, Z, y);
+}
+
+template <int MR, bool FAST>
+__global__ void __launch_bounds__(256, 2) cdc_pred_fused_kernel(const __grid_constant__ RunParams p,
+                                                             const CdcTable* __restrict__ tabs, float* __restrict__ out) {
+  constexpr int P = kCdcFusedP;
+  extern __shared__ __align__(16) unsigned char smem[];
+  CdcSTab<MR>* st = reinterpret_cast<CdcSTab<MR>*>(smem);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem + sizeof(CdcSTab<MR>) * (size_t)p.n_steps);
+  __shared__ double red[8];
+  const int n = p.n_steps;
+  for (int i = threadIdx.x; i < n * MR * MR; i += blockDim.x) {
+    const int t = i / (MR * MR), r = i % (MR * MR);
+    st[t].C[r / MR][r % MR] = tabs[t].C[r / MR][r % MR];
+  }
+  for (int i = threadIdx.x; i < n * MR; i += blockDim.x) {
+    const int t = i / MR, k = i % MR;
+    st[t].z[k] = tabs[t].z[k];
+    st[t].v[k] = tabs[t].v[k];
+  }
+  for (int t = threadIdx.x; t < n; t += blockDim.x) {
+    st[t].sinv = tabs[t].sinv;
+    st[t].deg = tabs[t].degenerate;
+  }
+  hist_init(p, hist);
+  __syncthreads();
+  const bool full = (p.out_mode == kFull);
+  const uint64_t N = p.n_paths, chunk = (uint64_t)blockDim.x * P;
+  StatAcc acc;
+  for (uint64_t base = (uint64_t)blockIdx.x * chunk; base < N; base += (uint64_t)gridDim.x * chunk) {
+    float Y[P], zn[P][4];
+    bool ok[P];
+#pragma unroll
+    for (int u = 0; u < P; ++u) {
+      const uint64_t q = base + (uint64_t)u * blockDim.x + threadIdx.x;
+      ok[u] = q < N;
+      Y[u] = p.y0;
+      if (full && ok[u]) out[q] = p.y0;
+    }
+    for (int i0 = 0; i0 < n; i0 += 4) {
+      // one Philox block per path gives the normals of steps i0..i0+3 (Z_{4b+r}, cos before sin)
+#pragma unroll
+      for (int u = 0; u < P; ++u) {
+        const uint64_t q = base + (uint64_t)u * blockDim.x + threadIdx.x;
+        const uint4 rr = philox_path_block_rk(p.rk0, p.rk1, p.path_offset + q, (uint32_t)(i0 >> 2));
+        if constexpr (FAST) {
+          box_muller_fast(rr.x, rr.y, zn[u][0], zn[u][1]);
+          box_muller_fast(rr.z, rr.w, zn[u][2], zn[u][3]);
+        } else {
+          box_muller(rr.x, rr.y, zn[u][0], zn[u][1]);
+          box_muller(rr.z, rr.w, zn[u][2], zn[u][3]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int i = i0 + r;
+        if (i >= n) break;
+        const CdcSTab<MR>& T = st[i];
+        float Cr[MR][MR], zr[MR], vr[MR];
+#pragma unroll
+        for (int k = 0; k < MR; ++k) {
+          zr[k] = T.z[k];
+          vr[k] = T.v[k];
+#pragma unroll
+          for (int j = 0; j < MR; ++j) Cr[k][j] = T.C[k][j];
+        }
+        const float sinv = T.sinv;
+#pragma unroll
+        for (int u = 0; u < P; ++u) {
+          Y[u] = cdc_pred_path_step<MR, FAST>(p, T, Cr, zr, vr, sinv, Y[u], zn[u][r]);
+          if (full && ok[u]) out[(uint64_t)(i + 1) * N + base + (uint64_t)u * blockDim.x + threadIdx.x] = Y[u];
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < P; ++u) {
+      if (!ok[u]) continue;
+      const uint64_t q = base + (uint64_t)u * blockDim.x + threadIdx.x;
+      if (p.out_mode == kTerminal) out[q] = Y[u];
+      if (p.has_stats) stat_add(acc, p, Y[u], 0.0, hist);
+    }
+  }
+  if (p.has_stats) stat_flush(acc, p, hist, red);
+}
+
 __global__ void fill_kernel(float* y, uint64_t n, float v) {
   for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (uint64_t)gridDim.x * blockDim.x)
     y[q] = v;
@@ -607,10 +753,31 @@ int launch_cdc(const RunParams& p, const CdcLevels& lv, void* scratch, float* co
 
 // SL7_SCHEME_CDC_PRED: per step the predicted-marginal table, then the (unchanged) per-path step kernel.
 // No selection passes: paths are coupled only through the table, which is the same for any path set.
+size_t cdc_table_bytes() { return sizeof(CdcTable); }
+
 int launch_cdc_pred(const RunParams& p, const CdcHorizon* hz, void* scratch, float* const* rows, int nrows,
-                    void* stream, int num_sms) {
+                    void* stream, int num_sms, void* tables) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   CdcScratch* s = reinterpret_cast<CdcScratch*>(scratch);
+  if (tables && (p.m == 5 || p.m == 7)) {
+    // fused path: the n_steps tables (one block each), then one kernel over all steps
+    CdcTable* tb = reinterpret_cast<CdcTable*>(tables);
+    for (int i = 0; i < p.n_steps; ++i) {
+      if (p.act == SL7_ACT_TANH) cdc_table_pred_kernel<SL7_ACT_TANH><<<1, 256, 0, st>>>(p, hz[i], tb + i, i);
+      else cdc_table_pred_kernel<SL7_ACT_SOFTPLUS><<<1, 256, 0, st>>>(p, hz[i], tb + i, i);
+    }
+    const bool fast = p.flags & SL7_FLAG_FAST_NORMALS;
+    auto k = (p.m == 5) ? (fast ? cdc_pred_fused_kernel<5, true> : cdc_pred_fused_kernel<5, false>)
+                        : (fast ? cdc_pred_fused_kernel<7, true> : cdc_pred_fused_kernel<7, false>);
+    const size_t tab = (p.m == 5 ? sizeof(CdcSTab<5>) : sizeof(CdcSTab<7>)) * (size_t)p.n_steps;
+    const size_t smem = tab + ((p.has_stats && p.n_bins > 0) ? sizeof(uint32_t) * (size_t)(p.n_bins + 2) : 0);
+    const cudaError_t ce = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (ce != cudaSuccess) return (int)ce;
+    const uint64_t groups = (p.n_paths + 256 * kCdcFusedP - 1) / (256 * kCdcFusedP);
+    const unsigned grid = (unsigned)(groups < (uint64_t)num_sms * 2 * 8 ? groups : (uint64_t)num_sms * 2 * 8);
+    k<<<grid, 256, smem, st>>>(p, tb, rows[0]);
+    return (int)cudaGetLastError();
+  }
   int e = cdc_fill(rows[0], p.n_paths, p.y0, stream, num_sms);   // row 0 = Y0
   if (e) return e;
   const size_t hist = (p.has_stats && p.n_bins > 0) ? sizeof(uint32_t) * (size_t)(p.n_bins + 2) : 0;

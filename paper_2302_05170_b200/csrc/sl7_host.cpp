@@ -80,6 +80,8 @@ struct sl7_ctx_s {
   bool cdc_ready = false;
   // 7L-CDC scratch (selection histograms + table) and state buffer for STATS-only runs
   void* d_cdc = nullptr;
+  void* d_cdc_tabs = nullptr;   // SL7_SCHEME_CDC_PRED fused kernel: per-step tables
+  int32_t cdc_tab_cap = 0;
   float* d_state = nullptr;
   size_t state_cap = 0;
   std::string err;
@@ -653,8 +655,21 @@ sl7_status run(sl7_ctx c, RunParams& p, const sl7_run_opts* o, float* d_out, dou
     }
     CdcLevels lv;
     for (int k = 0; k < kMaxM; ++k) lv.p[k] = (k < c->m) ? 0.5 * std::erfc(-c->x[k] / std::sqrt(2.0)) : 0.0;
-    if (o->scheme == SL7_SCHEME_CDC_PRED)
-      e = launch_cdc_pred(p, c->cdc_hz.data(), c->d_cdc, rows.data(), (int)rows.size(), o->stream, c->num_sms);
+    if (o->scheme == SL7_SCHEME_CDC_PRED) {
+      void* tabs = nullptr;
+      if ((c->m == 5 || c->m == 7) && p.n_steps <= kCdcFusedMaxSteps) {   // fused all-steps kernel
+        if (c->cdc_tab_cap < p.n_steps) {
+          if (c->d_cdc_tabs) cudaFree(c->d_cdc_tabs);
+          c->d_cdc_tabs = nullptr;
+          c->cdc_tab_cap = 0;
+          cudaError_t ce = cudaMalloc(&c->d_cdc_tabs, (size_t)p.n_steps * cdc_table_bytes());
+          if (ce != cudaSuccess) return cuda_fail(c, ce, "cudaMalloc(cdc tables)");
+          c->cdc_tab_cap = p.n_steps;
+        }
+        tabs = c->d_cdc_tabs;
+      }
+      e = launch_cdc_pred(p, c->cdc_hz.data(), c->d_cdc, rows.data(), (int)rows.size(), o->stream, c->num_sms, tabs);
+    }
     else
       e = launch_cdc(p, lv, c->d_cdc, rows.data(), (int)rows.size(), o->stream, c->num_sms);
   } else if (p.colloc == kAnn && (o->prec == SL7_PREC_BF16 || o->prec == SL7_PREC_SPLIT || o->prec == SL7_PREC_TF32)) {
@@ -1254,6 +1269,7 @@ void sl7_destroy(sl7_ctx c) {
     if (c->d_wtc_split) cudaFree(c->d_wtc_split);
     if (c->d_wtc_tf32) cudaFree(c->d_wtc_tf32);
     if (c->d_cdc) cudaFree(c->d_cdc);
+    if (c->d_cdc_tabs) cudaFree(c->d_cdc_tabs);
     if (c->d_state) cudaFree(c->d_state);
     if (c->d_out_scratch) cudaFree(c->d_out_scratch);
     if (c->d_stats_scratch) cudaFree(c->d_stats_scratch);

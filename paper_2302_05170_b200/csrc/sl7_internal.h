@@ -128,8 +128,12 @@ struct CdcHorizon {
   float c[kMaxM];
   float ou_a, ou_b;
 };
+// tables: device buffer of n_steps * cdc_table_bytes() (the fused all-steps kernel, m = 5 or 7), or NULL
+// for the per-step path (table kernel + step kernel per step, any m)
 int launch_cdc_pred(const RunParams& p, const CdcHorizon* hz, void* scratch, float* const* rows, int nrows,
-                    void* stream, int num_sms);
+                    void* stream, int num_sms, void* tables);
+size_t cdc_table_bytes();
+constexpr int kCdcFusedMaxSteps = 256;
 size_t cdc_scratch_bytes();
 int cdc_init_scratch(void* scratch, void* stream);
 // rows: nrows == 1 -> one in-place state buffer; nrows == n_steps + 1 -> FULL output rows.

@@ -2,7 +2,8 @@
 DESIGN.md) against the float64 oracle, teacher-forced: per step the oracle recomputes the marginal
 points from the predictor at (Y0, t_i), the table and the per-path step from the device's stored states
 and the same normals; tolerance 1e-5 * kappa with the CDC forward-error scale.  The scheme couples no
-paths, so shards (path_offset) must reproduce the one-call run bit for bit."""
+paths, so shards (path_offset) must reproduce the one-call run bit for bit.  m = 5 and 7 run the fused
+all-steps kernel, other m the per-step launches."""
 import numpy as np
 import pytest
 
@@ -14,6 +15,7 @@ pytestmark = pytest.mark.gpu
 CASES = [
     ("ou_exact", 7, "ou", (0.0, 1.0, 0.5), 1.0, 0.125, 16),
     ("gbm_exact", 5, "gbm", (0.05, 0.2), 1.0, 0.25, 4),
+    ("ou_exact_m6_per_step", 6, "ou", (0.3, 0.7, 0.9), 0.5, 0.25, 7),   # m = 6: the per-step launch path
     ("cfg2_ou_ann", 7, "ann", None, None, None, 16),
     ("cfg0_ann", 5, "ann", None, None, None, 2),
     ("cfg2_cir_ann", 7, "ann", None, None, None, 16),
@@ -122,3 +124,23 @@ def test_cdc_pred_cir_full_size_moments(gpu_lib):
         Y, _ = O.simulate_cdc_pred(spec, w.seed, np.arange(200_000, dtype=np.uint64))
     sd = Y[-1].std()
     assert abs(mean - Y[-1].mean()) < 5 * sd / np.sqrt(2e5)
+
+
+@pytest.mark.parametrize("mode", ["full", "terminal"])
+def test_cdc_pred_fused_edge_sizes(gpu_lib, mode):
+    # ragged path counts around the fused kernel's 1024-path groups and step counts not a multiple of 4:
+    # terminal values equal the oracle's free-running paths within the fp32 tolerance
+    import torch
+    sl7 = gpu_lib
+    ctx = sl7.Context(5)
+    th = (0.4, 0.8, 0.6)
+    for n_paths, n_steps in [(1, 1), (1023, 3), (1025, 5), (4097, 9)]:
+        o = sl7.make_opts(colloc=sl7.COLLOC_EXACT_OU, scheme=sl7.SCHEME_CDC_PRED)
+        out_mode = sl7.OUT_FULL if mode == "full" else sl7.OUT_TERMINAL
+        out, _ = ctx.simulate(0.7, 0.2, n_steps, th, n_paths, 21, out_mode, o)
+        torch.cuda.synchronize()
+        spec = O.Spec(5, "ou", th, 0.7, 0.2, n_steps)
+        Y, _ = O.simulate_cdc_pred(spec, 21, np.arange(n_paths, dtype=np.uint64))
+        got = out.double().cpu().numpy().reshape(-1, n_paths)
+        ref = Y if mode == "full" else Y[-1:]
+        np.testing.assert_allclose(got, ref, rtol=2e-5, atol=2e-5)
