@@ -363,8 +363,7 @@ __global__ void __launch_bounds__(256) cdc_table_mlp_kernel(const __grid_constan
 // (Y0, t_i = i dt, theta) -- the horizon's folded constants hz -- instead of quantiles of the paths
 // (t_0: every path at Y0, a degenerate table); then the table rows as above.  One block.
 template <int ACT, class T>
-__global__ void __launch_bounds__(256) cdc_table_pred_kernel(const __grid_constant__ RunParams p,
-                                                             const __grid_constant__ CdcHorizon hz, T* s, int step) {
+__device__ void cdc_pred_table_body(const RunParams& p, const CdcHorizon& hz, T* s, int step) {
   __shared__ float zr[1][kMaxM];
   const int m = p.m;
   if (step > 0 && p.colloc == kAnn) {
@@ -393,6 +392,24 @@ __global__ void __launch_bounds__(256) cdc_table_pred_kernel(const __grid_consta
       s->C[k][j] = (p.colloc == kExactGbm) ? zk * p.c[j] : fmaf(p.ou_a, zk, p.ou_b) + p.c[j];
     }
   }
+}
+
+template <int ACT, class T>
+__global__ void __launch_bounds__(256) cdc_table_pred_kernel(const __grid_constant__ RunParams p,
+                                                             const __grid_constant__ CdcHorizon hz, T* s, int step) {
+  cdc_pred_table_body<ACT>(p, hz, s, step);
+}
+
+// the tables of up to kCdcHzPack steps in one launch (block b: step first + b), horizons in the parameters
+constexpr int kCdcHzPack = 32;
+struct CdcHorizonPack {
+  CdcHorizon h[kCdcHzPack];
+};
+template <int ACT>
+__global__ void __launch_bounds__(256) cdc_tables_pred_kernel(const __grid_constant__ RunParams p,
+                                                              const __grid_constant__ CdcHorizonPack hz,
+                                                              CdcTable* tb, int first) {
+  cdc_pred_table_body<ACT>(p, hz.h[blockIdx.x], tb + first + blockIdx.x, first + (int)blockIdx.x);
 }
 
 // ---- per-path CDC step: conditional points by interpolation in the state, then g_m(X_hat)
@@ -760,11 +777,14 @@ int launch_cdc_pred(const RunParams& p, const CdcHorizon* hz, void* scratch, flo
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   CdcScratch* s = reinterpret_cast<CdcScratch*>(scratch);
   if (tables && (p.m == 5 || p.m == 7)) {
-    // fused path: the n_steps tables (one block each), then one kernel over all steps
+    // fused path: the n_steps tables (one block each, up to 32 per launch), then one kernel over all steps
     CdcTable* tb = reinterpret_cast<CdcTable*>(tables);
-    for (int i = 0; i < p.n_steps; ++i) {
-      if (p.act == SL7_ACT_TANH) cdc_table_pred_kernel<SL7_ACT_TANH><<<1, 256, 0, st>>>(p, hz[i], tb + i, i);
-      else cdc_table_pred_kernel<SL7_ACT_SOFTPLUS><<<1, 256, 0, st>>>(p, hz[i], tb + i, i);
+    for (int first = 0; first < p.n_steps; first += kCdcHzPack) {
+      const int cnt = (p.n_steps - first < kCdcHzPack) ? p.n_steps - first : kCdcHzPack;
+      CdcHorizonPack pack;
+      std::memcpy(pack.h, hz + first, sizeof(CdcHorizon) * (size_t)cnt);
+      if (p.act == SL7_ACT_TANH) cdc_tables_pred_kernel<SL7_ACT_TANH><<<cnt, 256, 0, st>>>(p, pack, tb, first);
+      else cdc_tables_pred_kernel<SL7_ACT_SOFTPLUS><<<cnt, 256, 0, st>>>(p, pack, tb, first);
     }
     const bool fast = p.flags & SL7_FLAG_FAST_NORMALS;
     auto k = (p.m == 5) ? (fast ? cdc_pred_fused_kernel<5, true> : cdc_pred_fused_kernel<5, false>)

@@ -1,6 +1,8 @@
 """One 7L-CDC run of cfg2 OU (ANN fp32 table, 1e8 paths x 16 steps, STATS) for ncu launch lists:
 
-  ncu --metrics gpu__time_duration.sum -k regex:cdc_ --csv python profiles/cdc_probe.py
+  ncu --metrics gpu__time_duration.sum -k regex:cdc_ --csv python profiles/cdc_probe.py [N] [pred]
+
+With a second argument "pred": SL7_SCHEME_CDC_PRED (the fused all-steps kernel).
 """
 import os
 import sys
@@ -18,7 +20,8 @@ N = int(sys.argv[1]) if len(sys.argv) > 1 else 100_000_000
 ctx = sl7.Context(w.m, list(w.dims), w.act, device=0)
 ctx.load_weights(load_golden_blob(w.blob))
 st = torch.zeros(sl7.stats_elems(4096), dtype=torch.float64, device="cuda")
-opts = sl7.make_opts(prec=sl7.PREC_FP32, colloc=sl7.COLLOC_ANN, scheme=sl7.SCHEME_CDC, n_bins=4096, hist_lo=-3.0,
+scheme = sl7.SCHEME_CDC_PRED if (len(sys.argv) > 2 and sys.argv[2] == "pred") else sl7.SCHEME_CDC
+opts = sl7.make_opts(prec=sl7.PREC_FP32, colloc=sl7.COLLOC_ANN, scheme=scheme, n_bins=4096, hist_lo=-3.0,
                      hist_hi=3.0, shift=1.0)
 ctx.simulate(w.y0, w.dt, w.n_steps, w.theta, N, w.seed, sl7.OUT_STATS, opts, stats=st)
 torch.cuda.synchronize()
