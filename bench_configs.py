@@ -269,12 +269,12 @@ def main():
                         "terminal": {k: s[k] for k in ("mean", "var", "skew", "exkurt", "strong_err")},
                         "quantiles_1_50_99": s["quantiles"], "clocks": clk.summary()}
                 if flags == -3:
-                    # fused CDC_PRED kernel: issue-bound; 228 thread-instructions per path-step measured by ncu
+                    # fused CDC_PRED kernel: issue-bound; 254 thread-instructions per path-step measured by ncu
                     # (smsp__inst_executed x 32 / path-steps, profiles/r01_cdc_pred_fused_ncu.md, libm normals)
-                    ach = rate * 228.0
+                    ach = rate * 254.0
                     line["roofline"] = {"bound": "alu", "pipe": "issue", "achieved": ach / 1e12,
                                         "peak": issue_peak / 1e12, "unit": "T thread-instr/s", "frac": ach / issue_peak,
-                                        "algorithmic": "228 instructions per path-step (ncu count of this kernel)"}
+                                        "algorithmic": "254 instructions per path-step (ncu count of this kernel on cfg2 OU)"}
                 if colloc == sl7.COLLOC_ANN and prec in (sl7.PREC_BF16, sl7.PREC_TF32):
                     trans = sum(w.dims[1:-1])
                     ach = trans * rate / 1e12
