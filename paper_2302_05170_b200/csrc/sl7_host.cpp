@@ -637,11 +637,17 @@ sl7_status run(sl7_ctx c, RunParams& p, const sl7_run_opts* o, float* d_out, dou
     }
     e = cdc_init_scratch(c->d_cdc, o->stream);
     if (e) return cuda_fail(c, (cudaError_t)e, "cdc scratch init");
+    // the fused CDC_PRED kernel (m = 5, 7) keeps every path's state in registers through all steps: no
+    // state buffer in STATS mode
+    const bool pred_fused = o->scheme == SL7_SCHEME_CDC_PRED && (c->m == 5 || c->m == 7) &&
+                            p.n_steps <= kCdcFusedMaxSteps;
     std::vector<float*> rows;
     if (p.out_mode == kFull) {
       for (int i = 0; i <= p.n_steps; ++i) rows.push_back(d_out + (size_t)i * p.n_paths);
     } else if (p.out_mode == kTerminal) {
       rows.push_back(d_out);
+    } else if (pred_fused) {
+      rows.push_back(nullptr);
     } else {
       if (c->state_cap < p.n_paths) {
         if (c->d_state) cudaFree(c->d_state);
@@ -656,8 +662,10 @@ sl7_status run(sl7_ctx c, RunParams& p, const sl7_run_opts* o, float* d_out, dou
     CdcLevels lv;
     for (int k = 0; k < kMaxM; ++k) lv.p[k] = (k < c->m) ? 0.5 * std::erfc(-c->x[k] / std::sqrt(2.0)) : 0.0;
     if (o->scheme == SL7_SCHEME_CDC_PRED) {
+      if (c->cdc_hz.size() != (size_t)p.n_steps)
+        return fail(c, SL7_ESTATE, "CDC_PRED horizons not prepared for this call (internal)");
       void* tabs = nullptr;
-      if ((c->m == 5 || c->m == 7) && p.n_steps <= kCdcFusedMaxSteps) {   // fused all-steps kernel
+      if (pred_fused) {   // fused all-steps kernel
         if (c->cdc_tab_cap < p.n_steps) {
           if (c->d_cdc_tabs) cudaFree(c->d_cdc_tabs);
           c->d_cdc_tabs = nullptr;
@@ -848,6 +856,31 @@ sl7_status sl7_load_weights(sl7_ctx c, const void* blob, size_t nbytes) {
   return SL7_OK;
 }
 
+// SL7_SCHEME_CDC_PRED: the predictor's constants at each horizon t_i = i dt (reading R-26), folded by the
+// same code as the run's own (prepare with dt -> t_i); step 0 needs none (every path at Y0).  Every entry
+// point that can run the scheme (sl7_simulate, sl7_simulate_host, sl7_simulate_host_async) calls this after
+// its own prepare(), so run() always sees the horizons of the current call.  No-op for other schemes.
+static sl7_status prepare_cdc_horizons(sl7_ctx c, double Y0, double dt, int32_t n_steps, const double* theta,
+                                int32_t n_theta, uint64_t n_paths, uint64_t seed, sl7_out out_mode,
+                                const sl7_run_opts* opts, bool has_out, bool has_stats) {
+  if (opts->scheme != SL7_SCHEME_CDC_PRED) return SL7_OK;
+  c->cdc_hz.assign((size_t)n_steps, CdcHorizon{});
+  for (int32_t i = 1; i < n_steps; ++i) {
+    RunParams q;
+    sl7_status s = prepare(c, Y0, dt * (double)i, n_steps, theta, n_theta, n_paths, seed, out_mode, opts, q, has_out,
+                           has_stats);
+    if (s != SL7_OK) return s;
+    CdcHorizon& h = c->cdc_hz[(size_t)i];
+    std::memcpy(h.l1b, q.l1b, sizeof h.l1b);
+    std::memcpy(h.osc, q.out_scale, sizeof h.osc);
+    std::memcpy(h.osh, q.out_shift, sizeof h.osh);
+    std::memcpy(h.c, q.c, sizeof h.c);
+    h.ou_a = q.ou_a;
+    h.ou_b = q.ou_b;
+  }
+  return SL7_OK;
+}
+
 sl7_status sl7_simulate(sl7_ctx c, double Y0, double dt, int32_t n_steps, const double* theta, int32_t n_theta,
                         uint64_t n_paths, uint64_t seed, sl7_out out_mode, const sl7_run_opts* opts, float* d_out,
                         double* d_stats) {
@@ -855,24 +888,9 @@ sl7_status sl7_simulate(sl7_ctx c, double Y0, double dt, int32_t n_steps, const 
   sl7_status s = prepare(c, Y0, dt, n_steps, theta, n_theta, n_paths, seed, out_mode, opts, p, d_out != nullptr,
                          d_stats != nullptr);
   if (s != SL7_OK) return s;
-  if (opts->scheme == SL7_SCHEME_CDC_PRED) {
-    // the predictor's constants at each horizon t_i = i dt (reading R-26), folded by the same code as the
-    // run's own (prepare with dt -> t_i); step 0 needs none (every path at Y0)
-    c->cdc_hz.assign((size_t)n_steps, CdcHorizon{});
-    for (int32_t i = 1; i < n_steps; ++i) {
-      RunParams q;
-      s = prepare(c, Y0, dt * (double)i, n_steps, theta, n_theta, n_paths, seed, out_mode, opts, q, d_out != nullptr,
-                  d_stats != nullptr);
-      if (s != SL7_OK) return s;
-      CdcHorizon& h = c->cdc_hz[(size_t)i];
-      std::memcpy(h.l1b, q.l1b, sizeof h.l1b);
-      std::memcpy(h.osc, q.out_scale, sizeof h.osc);
-      std::memcpy(h.osh, q.out_shift, sizeof h.osh);
-      std::memcpy(h.c, q.c, sizeof h.c);
-      h.ou_a = q.ou_a;
-      h.ou_b = q.ou_b;
-    }
-  }
+  s = prepare_cdc_horizons(c, Y0, dt, n_steps, theta, n_theta, n_paths, seed, out_mode, opts, d_out != nullptr,
+                           d_stats != nullptr);
+  if (s != SL7_OK) return s;
   DeviceGuard g(c->device);
   if (!g.ok) return fail(c, SL7_ECUDA, "cudaSetDevice(%d)", c->device);
   return run(c, p, opts, out_mode == SL7_OUT_STATS ? nullptr : d_out, d_stats);
@@ -1050,6 +1068,9 @@ sl7_status sl7_simulate_host(sl7_ctx c, double Y0, double dt, int32_t n_steps, c
   sl7_status s = prepare(c, Y0, dt, n_steps, theta, n_theta, n_paths, seed, out_mode, opts, p, h_out != nullptr,
                          h_stats != nullptr);
   if (s != SL7_OK) return s;
+  s = prepare_cdc_horizons(c, Y0, dt, n_steps, theta, n_theta, n_paths, seed, out_mode, opts, h_out != nullptr,
+                           h_stats != nullptr);
+  if (s != SL7_OK) return s;
   DeviceGuard g(c->device);
   if (!g.ok) return fail(c, SL7_ECUDA, "cudaSetDevice(%d)", c->device);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(opts->stream);
@@ -1107,6 +1128,9 @@ sl7_status sl7_simulate_host_async(sl7_ctx c, double Y0, double dt, int32_t n_st
   RunParams p;
   sl7_status s = prepare(c, Y0, dt, n_steps, theta, n_theta, n_paths, seed, out_mode, opts, p, h_out != nullptr,
                          h_stats != nullptr);
+  if (s != SL7_OK) return s;
+  s = prepare_cdc_horizons(c, Y0, dt, n_steps, theta, n_theta, n_paths, seed, out_mode, opts, h_out != nullptr,
+                           h_stats != nullptr);
   if (s != SL7_OK) return s;
   DeviceGuard g(c->device);
   if (!g.ok) return fail(c, SL7_ECUDA, "cudaSetDevice(%d)", c->device);

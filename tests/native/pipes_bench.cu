@@ -37,6 +37,88 @@ __device__ __forceinline__ float op(float x) {
   return r;
 }
 
+// Packed fp32 (sm_100a FFMA2: fma.rn.f32x2, two fp32 FMAs per lane per instruction).  B = 0: all three
+// operands packed registers; B = 1: the multiplier is a scalar register broadcast to both halves.
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+template <int B>
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long x, float s) {
+  unsigned long long r;
+  if constexpr (B == 0) {
+    const unsigned long long m = pk2(0.999f, 0.998f), c = pk2(1e-4f, 2e-4f);
+    asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(x), "l"(m), "l"(c));
+  } else {
+    const unsigned long long m = pk2(s, s), c = pk2(1e-4f, 2e-4f);
+    asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(x), "l"(m), "l"(c));
+  }
+  return r;
+}
+
+// OP 10 / 11: FFMA2 (packed / broadcast), CH independent chains of packed pairs: 2 thread-FMAs per op.
+template <int OP>
+__global__ void pipe2_kernel(float* out, long long* cycles, float s) {
+  unsigned long long v[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) v[c] = pk2(0.5f + 0.01f * (threadIdx.x + c), 0.25f + 0.01f * c);
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) v[c] = ffma2<OP - 10>(v[c], s);
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  float acc = 0.f;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) acc += __uint_as_float((uint32_t)v[c]) + __uint_as_float((uint32_t)(v[c] >> 32));
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+  if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+}
+
+// Mix: per iteration NM MUFU.EX2 chains and NF FFMA2 chains (independent): measures whether the MUFU and
+// the packed FMA pipe overlap (co-issue limit) -- the budget of a softplus epilogue that puts the log1p
+// polynomial on FFMA2 next to the MUFU ex2.
+template <int NM, int NF>
+__global__ void mix_kernel(float* out, long long* cycles, float s) {
+  float m[NM > 0 ? NM : 1];
+  unsigned long long f[NF > 0 ? NF : 1];
+#pragma unroll
+  for (int c = 0; c < NM; ++c) m[c] = 0.5f + 0.01f * (threadIdx.x + c);
+#pragma unroll
+  for (int c = 0; c < NF; ++c) f[c] = pk2(0.5f + 0.01f * c, 0.25f);
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+    for (int c = 0; c < NM; ++c) m[c] = op<0>(m[c]);
+#pragma unroll
+    for (int c = 0; c < NF; ++c) f[c] = ffma2<1>(f[c], s);
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  float acc = 0.f;
+#pragma unroll
+  for (int c = 0; c < NM; ++c) acc += m[c];
+#pragma unroll
+  for (int c = 0; c < NF; ++c) acc += __uint_as_float((uint32_t)f[c]);
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+  if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+}
+
+// HBM: store-only (16-byte st.global.v4, grid-stride, one wave of 148 x 4 CTAs) and copy (v4 load + v4 store)
+__global__ void store_kernel(float4* dst, size_t n4, float v) {
+  const float4 q = make_float4(v, v, v, v);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = q;
+}
+__global__ void copy_kernel(float4* dst, const float4* src, size_t n4) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
 template <int OP>
 __global__ void pipe_kernel(float* out, long long* cycles) {
   float v[CH];
@@ -71,6 +153,73 @@ void run(const char* name, int sms, int threads, float* d_out, long long* d_cyc)
   printf("{\"op\": \"%s\", \"threads_per_sm\": %d, \"thread_ops_per_clk_per_sm\": %.2f}\n", name, threads, ops / avg);
 }
 
+template <int OP>
+void run2(const char* name, int sms, int threads, float* d_out, long long* d_cyc) {
+  pipe2_kernel<OP><<<sms, threads>>>(d_out, d_cyc, 0.999f);
+  pipe2_kernel<OP><<<sms, threads>>>(d_out, d_cyc, 0.999f);
+  cudaDeviceSynchronize();
+  long long h[1024];
+  cudaMemcpy(h, d_cyc, sizeof(long long) * sms, cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < sms; ++i) avg += (double)h[i];
+  avg /= sms;
+  const double instr = (double)threads * ITERS * CH;
+  printf("{\"op\": \"%s\", \"threads_per_sm\": %d, \"thread_instr_per_clk_per_sm\": %.2f, "
+         "\"fp32_fma_per_clk_per_sm\": %.2f}\n", name, threads, instr / avg, 2 * instr / avg);
+}
+
+template <int NM, int NF>
+void runmix(int sms, int threads, float* d_out, long long* d_cyc) {
+  mix_kernel<NM, NF><<<sms, threads>>>(d_out, d_cyc, 0.999f);
+  mix_kernel<NM, NF><<<sms, threads>>>(d_out, d_cyc, 0.999f);
+  cudaDeviceSynchronize();
+  long long h[1024];
+  cudaMemcpy(h, d_cyc, sizeof(long long) * sms, cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < sms; ++i) avg += (double)h[i];
+  avg /= sms;
+  const double it = (double)threads * ITERS;
+  printf("{\"op\": \"mix MUFU.EX2 x %d + FFMA2 x %d\", \"threads_per_sm\": %d, \"mufu_per_clk_per_sm\": %.2f, "
+         "\"ffma2_instr_per_clk_per_sm\": %.2f, \"clk_per_thread_iter_x128\": %.3f}\n",
+         NM, NF, threads, NM * it / avg, NF * it / avg, avg / it * 128.0);
+}
+
+void run_hbm(int sms) {
+  const size_t bytes = (size_t)8 << 30;   // 8 GiB >> 126 MB L2
+  float4 *a = nullptr, *b = nullptr;
+  if (cudaMalloc(&a, bytes) != cudaSuccess || cudaMalloc(&b, bytes) != cudaSuccess) {
+    printf("{\"hbm\": \"alloc failed\"}\n");
+    return;
+  }
+  const size_t n4 = bytes / 16;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int cta_per_sm : {2, 4, 8}) {
+    const int grid = sms * cta_per_sm;
+    float best_st = 1e30f, best_cp = 1e30f;
+    for (int r = 0; r < 6; ++r) {
+      cudaEventRecord(e0);
+      store_kernel<<<grid, 256>>>(a, n4, 1.0f + r);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (r && ms < best_st) best_st = ms;
+      cudaEventRecord(e0);
+      copy_kernel<<<grid, 256>>>(b, a, n4);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (r && ms < best_cp) best_cp = ms;
+    }
+    printf("{\"hbm\": \"v4 grid-stride, %d CTAs x 256 thr\", \"bytes\": %zu, \"store_only_GBps\": %.1f, "
+           "\"copy_rw_GBps\": %.1f}\n", grid, bytes, bytes / (best_st * 1e6), 2.0 * bytes / (best_cp * 1e6));
+  }
+  cudaFree(a);
+  cudaFree(b);
+}
+
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -79,6 +228,15 @@ int main() {
   cudaMalloc(&d_out, sizeof(float) * sms * 1024);
   cudaMalloc(&d_cyc, sizeof(long long) * sms);
   for (int threads : {512, 1024}) {
+    run2<10>("FFMA2 (fma.rn.f32x2, packed operands)", sms, threads, d_out, d_cyc);
+    run2<11>("FFMA2 (fma.rn.f32x2, scalar broadcast multiplier)", sms, threads, d_out, d_cyc);
+    runmix<1, 0>(sms, threads, d_out, d_cyc);
+    runmix<1, 2>(sms, threads, d_out, d_cyc);
+    runmix<1, 4>(sms, threads, d_out, d_cyc);
+    runmix<1, 6>(sms, threads, d_out, d_cyc);
+    runmix<1, 8>(sms, threads, d_out, d_cyc);
+    runmix<2, 8>(sms, threads, d_out, d_cyc);
+    runmix<0, 8>(sms, threads, d_out, d_cyc);
     run<0>("MUFU.EX2 (ex2.approx.f32)", sms, threads, d_out, d_cyc);
     run<1>("MUFU.RCP (rcp.approx.f32)", sms, threads, d_out, d_cyc);
     run<2>("MUFU.LG2 (lg2.approx.f32)", sms, threads, d_out, d_cyc);
@@ -90,5 +248,6 @@ int main() {
     run<8>("tanh.approx.bf16x2 (2 results/instr)", sms, threads, d_out, d_cyc);
     run<9>("LOP3 (ALU)", sms, threads, d_out, d_cyc);
   }
+  run_hbm(sms);
   return 0;
 }

@@ -144,3 +144,26 @@ def test_cdc_pred_fused_edge_sizes(gpu_lib, mode):
         got = out.double().cpu().numpy().reshape(-1, n_paths)
         ref = Y if mode == "full" else Y[-1:]
         np.testing.assert_allclose(got, ref, rtol=2e-5, atol=2e-5)
+
+
+@pytest.mark.parametrize("entry", ["host", "host_async"])
+def test_cdc_pred_host_entry_points_equal_simulate(gpu_lib, entry):
+    # sl7_simulate_host / _async build the per-step predictor horizons themselves: on a fresh
+    # context, and after an earlier call with other (Y0, dt, n_steps) -- stale horizons would change the paths
+    import torch
+    sl7 = gpu_lib
+    ctx, code, th, spec = _setup(sl7, "cfg2_ou_ann", 7, "ann", None, None, None, 16)
+    n = 5_003
+    o = sl7.make_opts(colloc=code, scheme=sl7.SCHEME_CDC_PRED)
+    ref_ctx, _, _, _ = _setup(sl7, "cfg2_ou_ann", 7, "ann", None, None, None, 16)
+    ref, _ = ref_ctx.simulate(spec.y0, spec.dt, 16, th, n, 5, sl7.OUT_FULL, o)
+    ref_short, _ = ref_ctx.simulate(0.4, 0.05, 6, th, n, 5, sl7.OUT_FULL, o)
+    torch.cuda.synchronize()
+    for y0, dt, ns, want in ((spec.y0, spec.dt, 16, ref), (0.4, 0.05, 6, ref_short), (spec.y0, spec.dt, 16, ref)):
+        h = np.empty(sl7.out_elems(ns, n, sl7.OUT_FULL), dtype=np.float32)
+        if entry == "host":
+            ctx.simulate_host(y0, dt, ns, th, n, 5, sl7.OUT_FULL, o, h_out=h)
+        else:
+            ctx.simulate_host_async(y0, dt, ns, th, n, 5, sl7.OUT_FULL, o, h_out=h)
+            ctx.sync()
+        assert np.array_equal(h, want.cpu().numpy())
