@@ -693,10 +693,10 @@ sl7_status run(sl7_ctx c, RunParams& p, const sl7_run_opts* o, float* d_out, dou
 #endif
     t.split = (o->prec == SL7_PREC_SPLIT) ? 1 : 0;
     t.tf32 = (o->prec == SL7_PREC_TF32) ? 1 : 0;
-    // tanh on MUFU.TANH by default (SL7_TC_VARIANT 1..9 select the ex2 + rcp epilogues of DESIGN.md §6 for
-    // A/B timing; SPLIT keeps the accurate epilogue)
+    // tanh on MUFU.TANH in BF16 mode (SL7_TC_VARIANT 1..9 select the ex2 + rcp epilogues of DESIGN.md §6 for
+    // A/B timing); SPLIT and TF32 keep the accurate epilogue (their rounding decisions must follow O3 / O6)
     const bool ab_hook = (t.variant >= 1 && t.variant <= 9);
-    t.tanh_mufu = (c->act == SL7_ACT_TANH && !t.split && (t.tf32 || !ab_hook)) ? 1 : 0;
+    t.tanh_mufu = (c->act == SL7_ACT_TANH && !t.split && !t.tf32 && !ab_hook) ? 1 : 0;
     const double sc = (c->act == SL7_ACT_TANH && !t.tanh_mufu) ? 2.0 / std::log(2.0) : 1.0;
     t.act_scale = (float)sc;
     for (int k = 0; k < kTcN; ++k) {

@@ -476,8 +476,11 @@ cudaError_t launch_tc_tf32(const RunParams& p, const TcParams& t, cudaStream_t s
 
 int launch_tc_kernel(const RunParams& p, const TcParams& t, void* stream, int num_sms) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // TF32 takes its rna rounding decisions on an accurate tanh (ex2 + reciprocal, ~2e-7 absolute): MUFU.TANH's
+  // 1e-5 flips a few tf32 roundings of the one shared step-0 evaluation, which shifts every path's points
+  // together (reading R-15), so the tf32 moments would not match O6 on the identical path set (T-4)
   if (t.tf32)
-    return (int)(p.act == SL7_ACT_TANH ? launch_tc_tf32<kActTanhX, 0x00u>(p, t, st, num_sms)
+    return (int)(p.act == SL7_ACT_TANH ? launch_tc_tf32<SL7_ACT_TANH, kTanhNewtonMask>(p, t, st, num_sms)
                                        : launch_tc_tf32<SL7_ACT_SOFTPLUS, kSoftplusPolyMask>(p, t, st, num_sms));
   if (p.act == SL7_ACT_TANH && t.tanh_mufu) {
     return (int)launch_tc_act_x(p, t, st, num_sms);

@@ -108,6 +108,54 @@ __global__ void mix_kernel(float* out, long long* cycles, float s) {
   if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
 }
 
+// Issue cost of FFMA2 against FFMA at equal FLOPs, next to other pipes: per iteration NA ALU LOP3 chains
+// (asm volatile, not foldable) and NM MUFU.EX2 chains plus either 2*NF FFMA (P = 0) or NF FFMA2 (P = 1).
+// If FFMA2 took one issue slot its 64-lane work would leave the next slot to another pipe.
+template <int NM, int NA, int NF, int P>
+__global__ void mix2_kernel(float* out, long long* cycles, float s) {
+  float m[NM > 0 ? NM : 1];
+  uint32_t a[NA > 0 ? NA : 1];
+  float f[NF > 0 ? 2 * NF : 1];
+  unsigned long long g[NF > 0 ? NF : 1];
+#pragma unroll
+  for (int c = 0; c < NM; ++c) m[c] = 0.5f + 0.01f * (threadIdx.x + c);
+#pragma unroll
+  for (int c = 0; c < NA; ++c) a[c] = threadIdx.x * 2654435761u + c;
+#pragma unroll
+  for (int c = 0; c < 2 * NF; ++c) f[c] = 0.5f + 0.01f * c;
+#pragma unroll
+  for (int c = 0; c < NF; ++c) g[c] = pk2(0.5f + 0.01f * c, 0.25f);
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+    for (int c = 0; c < NM; ++c) m[c] = op<0>(m[c]);
+#pragma unroll
+    for (int c = 0; c < NA; ++c)
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a[c]) : "r"(a[(c + 1) % (NA > 0 ? NA : 1)]), "r"(i));
+    if constexpr (P == 0) {
+#pragma unroll
+      for (int c = 0; c < 2 * NF; ++c) asm volatile("fma.rn.f32 %0, %0, %1, 0f38D1B717;" : "+f"(f[c]) : "f"(s));
+    } else {
+#pragma unroll
+      for (int c = 0; c < NF; ++c) g[c] = ffma2<1>(g[c], s);
+    }
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  float acc = 0.f;
+#pragma unroll
+  for (int c = 0; c < NM; ++c) acc += m[c];
+#pragma unroll
+  for (int c = 0; c < NA; ++c) acc += __uint_as_float(a[c]);
+#pragma unroll
+  for (int c = 0; c < 2 * NF; ++c) acc += f[c];
+#pragma unroll
+  for (int c = 0; c < NF; ++c) acc += __uint_as_float((uint32_t)g[c]);
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+  if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+}
+
 // HBM: store-only (16-byte st.global.v4, grid-stride, one wave of 148 x 4 CTAs) and copy (v4 load + v4 store)
 __global__ void store_kernel(float4* dst, size_t n4, float v) {
   const float4 q = make_float4(v, v, v, v);
@@ -184,6 +232,22 @@ void runmix(int sms, int threads, float* d_out, long long* d_cyc) {
          NM, NF, threads, NM * it / avg, NF * it / avg, avg / it * 128.0);
 }
 
+template <int NM, int NA, int NF, int P>
+void runmix2(int sms, int threads, float* d_out, long long* d_cyc) {
+  mix2_kernel<NM, NA, NF, P><<<sms, threads>>>(d_out, d_cyc, 0.999f);
+  mix2_kernel<NM, NA, NF, P><<<sms, threads>>>(d_out, d_cyc, 0.999f);
+  cudaDeviceSynchronize();
+  long long h[1024];
+  cudaMemcpy(h, d_cyc, sizeof(long long) * sms, cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < sms; ++i) avg += (double)h[i];
+  avg /= sms;
+  const double it = (double)threads * ITERS;
+  printf("{\"op\": \"mix2 MUFU x %d + LOP3 x %d + %s\", \"threads_per_sm\": %d, "
+         "\"clk_per_warp_iter_per_smsp\": %.3f}\n", NM, NA, P ? (NF == 4 ? "FFMA2 x 4" : NF == 8 ? "FFMA2 x 8" : "FFMA2 x 2")
+         : (NF == 4 ? "FFMA x 8" : NF == 8 ? "FFMA x 16" : "FFMA x 4"), threads, avg / it * 128.0);
+}
+
 void run_hbm(int sms) {
   const size_t bytes = (size_t)8 << 30;   // 8 GiB >> 126 MB L2
   float4 *a = nullptr, *b = nullptr;
@@ -228,6 +292,19 @@ int main() {
   cudaMalloc(&d_out, sizeof(float) * sms * 1024);
   cudaMalloc(&d_cyc, sizeof(long long) * sms);
   for (int threads : {512, 1024}) {
+    runmix2<0, 0, 8, 0>(sms, threads, d_out, d_cyc);
+    runmix2<0, 0, 8, 1>(sms, threads, d_out, d_cyc);
+    runmix2<0, 8, 4, 0>(sms, threads, d_out, d_cyc);
+    runmix2<0, 8, 4, 1>(sms, threads, d_out, d_cyc);
+    runmix2<0, 4, 4, 0>(sms, threads, d_out, d_cyc);
+    runmix2<0, 4, 4, 1>(sms, threads, d_out, d_cyc);
+    runmix2<1, 0, 4, 0>(sms, threads, d_out, d_cyc);
+    runmix2<1, 0, 4, 1>(sms, threads, d_out, d_cyc);
+    runmix2<1, 0, 2, 0>(sms, threads, d_out, d_cyc);
+    runmix2<1, 0, 2, 1>(sms, threads, d_out, d_cyc);
+    runmix2<1, 4, 2, 0>(sms, threads, d_out, d_cyc);
+    runmix2<1, 4, 2, 1>(sms, threads, d_out, d_cyc);
+    runmix2<0, 8, 0, 0>(sms, threads, d_out, d_cyc);
     run2<10>("FFMA2 (fma.rn.f32x2, packed operands)", sms, threads, d_out, d_cyc);
     run2<11>("FFMA2 (fma.rn.f32x2, scalar broadcast multiplier)", sms, threads, d_out, d_cyc);
     runmix<1, 0>(sms, threads, d_out, d_cyc);

@@ -302,31 +302,6 @@ def test_ann_bf16_tc_teacher_forced(gpu_lib, name, gen):
     print("bf16 teacher-forced worst |err|/kappa = %.3g" % worst)
 
 
-@pytest.mark.parametrize("name", ["cfg0", "cfg2_ou", "cfg2_cir"])
-def test_ann_bf16_terminal_moments(gpu_lib, name):
-    """T-4: free-running terminal mean and variance over the identical path set within 1e-4 relative
-    of the quantisation-aware oracle (|dmean| <= 1e-4 sd when the mean is ~0)."""
-    sl7 = gpu_lib
-    blob, m, dims, act, theta, y0, n_steps, dt = _ann_case(name, None)
-    w = workloads()[name]
-    n_steps, dt = w.n_steps, w.dt
-    n_paths = 20_000
-    ctx = sl7.Context(m, dims, act)
-    ctx.load_weights(blob)
-    YT, _ = _run(sl7, ctx, dict(y0=y0, dt=dt, n_steps=n_steps), n_paths, w.seed, sl7.OUT_TERMINAL, sl7.COLLOC_ANN,
-                 prec=sl7.PREC_BF16, theta=theta)
-    spec = O.Spec(m, "ann", theta, y0, dt, n_steps, net=O.parse_blob(blob), quant="bf16")
-    Yo, _ = O.simulate(spec, w.seed, np.arange(n_paths, dtype=np.uint64))
-    mo, md = Yo[-1].mean(), YT.mean()
-    vo, vd = Yo[-1].var(), YT.var()
-    sd = np.sqrt(vo)
-    assert abs(md - mo) <= 1e-4 * max(abs(mo), sd if abs(mo) < 1e-3 * sd else abs(mo))
-    assert abs(vd - vo) <= 1e-4 * vo
-    rel = np.abs(YT - Yo[-1]) / np.maximum(np.abs(Yo[-1]), sd)
-    print("%s bf16 free-running per-value: median %.2g p99 %.2g max %.2g" % (name, np.median(rel),
-                                                                           np.quantile(rel, 0.99), rel.max()))
-
-
 @pytest.mark.parametrize("name,gen", ANN_CASES, ids=[c[0] for c in ANN_CASES])
 def test_ann_tf32_tc_teacher_forced(gpu_lib, name, gen):
     """T-3 for SL7_PREC_TF32 (tcgen05 kind::tf32): within 5e-3 * kappa of O6 with TF32 (cvt.rna) rounding."""
@@ -342,42 +317,6 @@ def test_ann_tf32_tc_teacher_forced(gpu_lib, name, gen):
     Z = O.normals(57, np.arange(n_paths, dtype=np.uint64), n_steps)
     worst = _teacher_forced(spec, Yd, Z, tol=5e-3)
     print("tf32 teacher-forced worst |err|/kappa = %.3g" % worst)
-
-
-@pytest.mark.parametrize("name", ["cfg0", "cfg2_ou"])
-def test_ann_tf32_terminal_moments(gpu_lib, name):
-    """T-4 for SL7_PREC_TF32 against O6 (tf32) on the identical path set, free-running from step 1.
-
-    Step 0 is ONE network evaluation (every path sits at Y0), so the tf32 rounding decisions of its
-    ~150 activations shift every path's point set together.  The device takes those decisions on
-    MUFU.TANH values (<= 9.9e-6 relative, reading R-15), O6 on exact tanh; at the tf32 unit 2^-11 a
-    few of them flip per evaluation, which moves the points by ~2e-4 (perturbing O6's tanh by 1e-5 at
-    random reproduces this on the CPU) and biases the terminal mean by as much.  That single
-    evaluation is T-3's domain (within 5e-3 kappa); here the oracle continues from the device's row 1,
-    where the states are spread and such flips average out, and the rest of the run must match the
-    moments to 1e-4."""
-    sl7 = gpu_lib
-    blob, m, dims, act, theta, y0, n_steps, dt = _ann_case(name, None)
-    w = workloads()[name]
-    n_steps, dt = w.n_steps, w.dt
-    n_paths = 20_000
-    ctx = sl7.Context(m, dims, act)
-    ctx.load_weights(blob)
-    Yd, _ = _run(sl7, ctx, dict(y0=y0, dt=dt, n_steps=n_steps), n_paths, w.seed, sl7.OUT_FULL, sl7.COLLOC_ANN,
-                 prec=sl7.PREC_TF32, theta=theta)
-    Yd = Yd.reshape(n_steps + 1, n_paths)
-    YT = Yd[-1]
-    spec = O.Spec(m, "ann", theta, y0, dt, n_steps, net=O.parse_blob(blob), quant="tf32")
-    Z = O.normals(w.seed, np.arange(n_paths, dtype=np.uint64), n_steps)
-    Y = Yd[1]
-    for i in range(1, n_steps):
-        Y = O.step(spec, Y, Z[i])
-    Yo = [Y]
-    mo, md = Yo[-1].mean(), YT.mean()
-    vo, vd = Yo[-1].var(), YT.var()
-    sd = np.sqrt(vo)
-    assert abs(md - mo) <= 1e-4 * max(abs(mo), sd if abs(mo) < 1e-3 * sd else abs(mo))
-    assert abs(vd - vo) <= 1e-4 * vo
 
 
 @pytest.mark.parametrize("name,gen", ANN_CASES, ids=[c[0] for c in ANN_CASES])
