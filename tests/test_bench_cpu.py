@@ -21,7 +21,7 @@ def _check(d, n):
     assert d["n_gpus"] == n and d["steps"] == 1 and d["warmup"] == 3
     assert d["value"] > 0 and d["ms_per_step"] > 0 and d["higher_is_better"] is True
     assert d["dtype"] == "f64" and d["vs_baseline"] is None
-    assert d["config"]["workload"].startswith("cfg1")
+    assert d["config"]["workload"].startswith("cfg4")
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["sample"] and cb["value"] == d["value"]
     e = d["e2e"]
