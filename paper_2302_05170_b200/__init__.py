@@ -16,7 +16,8 @@ import ctypes
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libsl7.so")
+# SL7_LIB: an experiment build (python -m paper_2302_05170_b200.build --ab -> libsl7_ab.so) for A/B timings
+LIB_PATH = os.environ.get("SL7_LIB") or os.path.join(PKG, "libsl7.so")
 
 OK, EINVAL, ESTATE, EFORMAT, ENOMEM, ECUDA, ENONFINITE, EUNSUPPORTED = range(8)
 ACT_TANH, ACT_SOFTPLUS = 0, 1

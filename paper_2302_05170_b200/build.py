@@ -27,23 +27,27 @@ def _stale() -> bool:
     return any(os.path.exists(d) and os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src, obj):
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v",
+def _compile(src, obj, extra=()):
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v", *extra,
            "-I", os.path.join(ROOT, "include"), "-c", "-o", obj, src]
     r = subprocess.run(cmd, capture_output=True, text=True)
     return cmd, r
 
 
-def build(force: bool = False, verbose: bool = True) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = True, ab: bool = False) -> str:
+    """ab=True: the experiment build libsl7_ab.so (-DSL7_AB_HOOKS: SL7_TC_VARIANT selects the epilogue
+    variants of DESIGN.md §6; load it with SL7_LIB=...); never used by the tests, smoke() or bench.py."""
+    lib = LIB if not ab else os.path.join(PKG, "libsl7_ab.so")
+    extra = ("-DSL7_AB_HOOKS",) if ab else ()
+    if not ab and not force and not _stale():
         return LIB
     from concurrent.futures import ThreadPoolExecutor
     srcs = [os.path.join(CSRC, f) for f in SOURCES if os.path.exists(os.path.join(CSRC, f))]
-    objdir = os.path.join(PKG, "build")
+    objdir = os.path.join(PKG, "build" if not ab else "build_ab")
     os.makedirs(objdir, exist_ok=True)
     objs = [os.path.join(objdir, os.path.basename(s) + ".o") for s in srcs]
     with ThreadPoolExecutor(len(srcs)) as ex:
-        results = list(ex.map(lambda so: _compile(*so), zip(srcs, objs)))
+        results = list(ex.map(lambda so: _compile(*so, extra), zip(srcs, objs)))
     log = os.path.join(PKG, "build_ptxas.log")
     with open(log, "w") as f:
         for cmd, r in results:
@@ -54,14 +58,14 @@ def build(force: bool = False, verbose: bool = True) -> str:
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("nvcc failed (see %s)" % log)
-    link = [NVCC, *ARCH, "-shared", "--cudart", "static", "-o", LIB + ".tmp", *objs]
+    link = [NVCC, *ARCH, "-shared", "--cudart", "static", "-o", lib + ".tmp", *objs]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc link failed")
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv))
+    print(build(force="--force" in sys.argv, ab="--ab" in sys.argv))

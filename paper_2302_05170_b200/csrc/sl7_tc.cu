@@ -95,10 +95,70 @@ __device__ __forceinline__ bool use_newton(int c) {
   return (NMASK >> (c & 7)) & 1u;
 }
 
+// ---- paired softplus (kActSoftplusPair): two units per FFMA2 (fma.rn.f32x2, sm_100a).  FFMA2 has the
+// FFMA FLOP rate at half the instructions and co-issues with MUFU better than FFMA (profiles/r02_pipes.md:
+// 1 MUFU + 2 FFMA2 per warp-iteration 8.2 clk, 1 MUFU + 4 FFMA 10.1 clk; the MUFU bound is 8), so a pair
+// whose log1p runs as a polynomial costs 1 MUFU per unit and ~9 FMA-pipe cycles, a pair on MUFU lg2 2 MUFU.
+// NMASK bit (pair index % 8) selects the polynomial pairs.
+constexpr int kActSoftplusPair = 4;
+
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void up2(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t fma2s(uint64_t a, float b, float c) { return fma2(a, pk2(b, b), pk2(c, c)); }
+
+// softplus of a pair.  POLY: log1p(e), e = 2^(-|u| log2 e) in (0, 1], as e q(e) with q the degree-7
+// minimax polynomial of log1p(e)/e on [0, 1] (absolute error 2.5e-8 in exact arithmetic, 1.6e-7 after fp32
+// Horner rounding, mean -1.4e-8 over e^-|u|, u ~ N(0, 2)); the last Horner step adds max(u, 0):
+//   h = e q(e) + max(u, 0)   (8 FFMA2 per pair).
+// Otherwise: h = ln 2 lg2(1 + e) + max(u, 0) with MUFU lg2 (FADD2 / FFMA2 for the pair).
+template <bool POLY, bool DEG7 = false>
+__device__ __forceinline__ void softplus_pair(float u0, float u1, float& h0, float& h1) {
+  const float e0 = ex2_approx(fabsf(u0) * -1.4426950408889634f);
+  const float e1 = ex2_approx(fabsf(u1) * -1.4426950408889634f);
+  const uint64_t mx = pk2(fmaxf(u0, 0.0f), fmaxf(u1, 0.0f));
+  const uint64_t E = pk2(e0, e1);
+  uint64_t r;
+  if constexpr (POLY && DEG7) {
+    // degree-6 q (total degree 7): minimax error 1.8e-7, 3.4e-7 after fp32 rounding, mean -3.3e-8
+    uint64_t q = fma2s(E, 1.081165298819542e-02f, -5.5391568690538406e-02f);
+    q = fma2(q, E, pk2(1.351390779018402e-01f, 1.351390779018402e-01f));
+    q = fma2(q, E, pk2(-2.263084203004837e-01f, -2.263084203004837e-01f));
+    q = fma2(q, E, pk2(3.284189999103546e-01f, 3.284189999103546e-01f));
+    q = fma2(q, E, pk2(-4.995054006576538e-01f, -4.995054006576538e-01f));
+    q = fma2(q, E, pk2(9.99983012676239e-01f, 9.99983012676239e-01f));
+    r = fma2(q, E, mx);
+  } else if constexpr (POLY) {
+    uint64_t q = fma2s(E, -6.678603123873472e-03f, 3.697235882282257e-02f);
+    q = fma2(q, E, pk2(-9.672726690769196e-02f, -9.672726690769196e-02f));
+    q = fma2(q, E, pk2(1.6879309713840485e-01f, 1.6879309713840485e-01f));
+    q = fma2(q, E, pk2(-2.412412464618683e-01f, -2.412412464618683e-01f));
+    q = fma2(q, E, pk2(3.3191972970962524e-01f, 3.3191972970962524e-01f));
+    q = fma2(q, E, pk2(-4.998879134654999e-01f, -4.998879134654999e-01f));
+    q = fma2(q, E, pk2(9.999969601631165e-01f, 9.999969601631165e-01f));
+    r = fma2(q, E, mx);
+  } else {
+    float a0, a1;
+    up2(fma2(E, pk2(1.0f, 1.0f), pk2(1.0f, 1.0f)), a0, a1);   // 1 + e
+    r = fma2(pk2(lg2_approx(a0), lg2_approx(a1)), pk2(0.69314718055994531f, 0.69314718055994531f), mx);
+  }
+  up2(r, h0, h1);
+}
+
 // Pack two activations as NP bf16 parts: part 0 = bf16(h); NP = 3 (SL7_PREC_SPLIT) adds the rounded
 // residuals, so h = h0 + h1 + h2 to ~2^-24 relative (the split-precision A operand).
-template <int NP>
-__device__ __forceinline__ void split_pack(float a, float b, uint32_t (&pk)[NP][16], int k) {
+template <int NP, int NW>
+__device__ __forceinline__ void split_pack(float a, float b, uint32_t (&pk)[NP][NW], int k) {
   uint32_t w = tc::pack_bf16x2(a, b);
   pk[0][k] = w;
 #pragma unroll
@@ -112,21 +172,35 @@ __device__ __forceinline__ void split_pack(float a, float b, uint32_t (&pk)[NP][
 
 // FOLD: the hidden bias rides in the MMA (K columns H, H+1, H+2 of A hold 1.0, the weight tile holds
 // the bias split into three bf16 terms), so u = acc * scale.  Otherwise u = acc * scale + bias_scaled.
-template <int ACT, int H, unsigned NMASK, bool FOLD, int NP>
-__device__ __forceinline__ void act_pack_32(const uint32_t (&v)[32], int col0, float scale, const float* bs,
-                                            uint32_t (&pk)[NP][16]) {
+template <int ACT, int H, unsigned NMASK, bool FOLD, int NP, int NC = 32>
+__device__ __forceinline__ void act_pack_32(const uint32_t (&v)[NC], int col0, float scale, const float* bs,
+                                            uint32_t (&pk)[NP][NC / 2]) {
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
+  for (int k = 0; k < NC / 2; ++k) {
     float h[2];
+    const int c0 = col0 + 2 * k;
+    if (ACT == kActSoftplusPair && c0 + 1 < H) {
+      // softplus: the host folds no scale (act_scale = 1), so u is the accumulator (+ bias)
+      const float u0 = FOLD ? __uint_as_float(v[2 * k]) : __uint_as_float(v[2 * k]) + bs[c0];
+      const float u1 = FOLD ? __uint_as_float(v[2 * k + 1]) : __uint_as_float(v[2 * k + 1]) + bs[c0 + 1];
+      if ((NMASK >> ((c0 >> 1) & 7)) & 1u) softplus_pair<true, (NMASK & 0x100u) != 0>(u0, u1, h[0], h[1]);
+      else softplus_pair<false>(u0, u1, h[0], h[1]);
+    } else {
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int c = col0 + 2 * k + q;
-      if (c < H) {
-        const float acc = __uint_as_float(v[2 * k + q]);
-        const float u = FOLD ? (ACT == kActTanhX ? acc : acc * scale) : fmaf(acc, scale, bs[c]);
-        h[q] = tc_act_u<ACT>(u, use_newton<ACT, NMASK>(c));
-      } else {
-        h[q] = (FOLD && c < H + 3) ? 1.0f : 0.0f;
+      for (int q = 0; q < 2; ++q) {
+        const int c = c0 + q;
+        if (c < H) {
+          const float acc = __uint_as_float(v[2 * k + q]);
+          if constexpr (ACT == kActSoftplusPair) {
+            const float u = FOLD ? acc : acc + bs[c];
+            h[q] = tc_act_u<SL7_ACT_SOFTPLUS>(u, false);
+          } else {
+            const float u = FOLD ? (ACT == kActTanhX ? acc : acc * scale) : fmaf(acc, scale, bs[c]);
+            h[q] = tc_act_u<ACT>(u, use_newton<ACT, NMASK>(c));
+          }
+        } else {
+          h[q] = (FOLD && c < H + 3) ? 1.0f : 0.0f;
+        }
       }
     }
     split_pack<NP>(h[0], h[1], pk, k);
@@ -193,6 +267,9 @@ __device__ __forceinline__ void issue_layer(uint32_t acc_t, uint32_t a_t, uint32
 template <int NG, int H, int MR, bool RT_M, int ACT, unsigned NMASK, int NP = 1, bool SKIPMMA = false, bool TF32 = false>
 __global__ void __launch_bounds__(NG * kGroupThreads, 1)
     ann_tc_step_kernel(const __grid_constant__ RunParams p, const __grid_constant__ TcParams t) {
+  // epilogue in quarters of 16 columns (paired softplus, NMASK bit 9); the A columns of a quarter that is
+  // not stored keep the layer-1 values (all such columns are zero padding: the same on every layer)
+  constexpr bool QUARTERS = (ACT == kActSoftplusPair) && (NMASK & 0x200u) && !TF32;
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint64_t mbar[NG];   // per group: MMA completion (tcgen05.commit)
   __shared__ uint32_t tmem_base_sh;
@@ -282,11 +359,20 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
 #pragma unroll
           for (int k = 0; k < 16; ++k) {
             float h[2];
+            const int c0 = 32 * half + 2 * k;
+            if (ACT == kActSoftplusPair && c0 + 1 < H) {
+              const float u0 = fmaf(Y, t.l1w[c0], t.l1b[c0]), u1 = fmaf(Y, t.l1w[c0 + 1], t.l1b[c0 + 1]);
+              if ((NMASK >> ((c0 >> 1) & 7)) & 1u) softplus_pair<true, (NMASK & 0x100u) != 0>(u0, u1, h[0], h[1]);
+              else softplus_pair<false>(u0, u1, h[0], h[1]);
+            } else {
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              const int c = 32 * half + 2 * k + q;
-              h[q] = (c < H) ? tc_act_u<ACT>(fmaf(Y, t.l1w[c], t.l1b[c]), use_newton<ACT, NMASK>(c))
-                             : ((FOLD && c < H + 3) ? 1.0f : 0.0f);
+              for (int q = 0; q < 2; ++q) {
+                const int c = c0 + q;
+                constexpr int A1 = (ACT == kActSoftplusPair) ? SL7_ACT_SOFTPLUS : ACT;
+                h[q] = (c < H) ? tc_act_u<A1>(fmaf(Y, t.l1w[c], t.l1b[c]),
+                                              ACT != kActSoftplusPair && use_newton<ACT, NMASK>(c))
+                               : ((FOLD && c < H + 3) ? 1.0f : 0.0f);
+              }
             }
             split_pack<NP>(h[0], h[1], pk, k);
           }
@@ -325,6 +411,23 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
         phase ^= 1u;
         tc::fence_after();
         if (!last) {
+          if constexpr (QUARTERS) {
+            // 16 columns at a time (fewer live registers: more pairs of the epilogue in flight); the
+            // quarters past the last unit (and its 3 bias columns) are not loaded
+#pragma unroll
+            for (int qt = 0; qt < 4; ++qt) {
+              if (16 * qt < (FOLD ? H + 3 : H)) {
+                uint32_t v[16];
+                tc::tmem_ld_32x32b_x16(acc_t + lane_off + 16u * qt, v);
+                tc::wait_ld();
+                uint32_t pk[NP][8];
+                act_pack_32<ACT, H, NMASK, FOLD, NP, 16>(v, 16 * qt, t.act_scale, t.bias[l], pk);
+#pragma unroll
+                for (int part = 0; part < NP; ++part)
+                  tc::tmem_st_32x32b_x8(a_t + 32u * part + lane_off + 8u * qt, pk[part]);
+              }
+            }
+          } else {
 #pragma unroll
           for (int half = 0; half < 2; ++half) {
             uint32_t v[32];
@@ -341,6 +444,7 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
               for (int part = 0; part < NP; ++part)
                 tc::tmem_st_32x32b_x16(a_t + 32u * part + lane_off + 16u * half, pk[part]);
             }
+          }
           }
           tc::wait_st();
         } else {
@@ -418,6 +522,46 @@ constexpr int kTcGroupsSplit = 3;
 constexpr int kTcGroupsSoftplus = 5;
 
 template <int ACT>
+cudaError_t launch_tc_act(const RunParams& p, const TcParams& t, cudaStream_t st, int num_sms);
+
+// softplus, BF16: paired epilogue; polynomial log1p on the pairs of kSoftplusPairMask (bit = pair index % 8)
+constexpr unsigned kSoftplusPairMask = 0x15Fu;
+
+template <unsigned PM>
+cudaError_t launch_sp_pair(const RunParams& p, const TcParams& t, cudaStream_t st, int num_sms) {
+  constexpr int NG = kTcGroupsSoftplus;
+  if (p.width == 50 && p.m == 5) return launch_tc_t<NG, 50, 5, false, kActSoftplusPair, PM>(p, t, st, num_sms);
+  if (p.width == 50 && p.m == 7) return launch_tc_t<NG, 50, 7, false, kActSoftplusPair, PM>(p, t, st, num_sms);
+  return launch_tc_t<NG, 64, kMaxM, true, kActSoftplusPair, PM>(p, t, st, num_sms);
+}
+
+cudaError_t launch_softplus_bf16(const RunParams& p, const TcParams& t, cudaStream_t st, int num_sms) {
+#ifdef SL7_AB_HOOKS
+  switch (t.variant) {   // A/B hook (SL7_TC_VARIANT): share of polynomial pairs, or the r01 epilogue
+    case 20: return launch_sp_pair<0x00u>(p, t, st, num_sms);
+    case 21: return launch_sp_pair<0x55u>(p, t, st, num_sms);
+    case 22: return launch_sp_pair<0x77u>(p, t, st, num_sms);
+    case 23: return launch_sp_pair<0x7Fu>(p, t, st, num_sms);
+    case 24: return launch_sp_pair<0xFFu>(p, t, st, num_sms);
+    case 25: return launch_tc_act<SL7_ACT_SOFTPLUS>(p, t, st, num_sms);
+    case 26: return launch_sp_pair<0x177u>(p, t, st, num_sms);
+    case 27: return launch_sp_pair<0x17Fu>(p, t, st, num_sms);
+    case 28: return launch_sp_pair<0x1FFu>(p, t, st, num_sms);
+    case 29: return launch_sp_pair<0x15Fu>(p, t, st, num_sms);
+    case 30: return launch_sp_pair<0x13Fu>(p, t, st, num_sms);
+    case 31: return launch_sp_pair<0x1DFu>(p, t, st, num_sms);
+    case 32: return launch_sp_pair<0x15Bu>(p, t, st, num_sms);
+    case 33: return launch_sp_pair<0x1F7u>(p, t, st, num_sms);
+    case 34: return launch_sp_pair<0x35Fu>(p, t, st, num_sms);
+    case 35: return launch_sp_pair<0x377u>(p, t, st, num_sms);
+    case 36: return launch_sp_pair<0x3FFu>(p, t, st, num_sms);
+    default: break;
+  }
+#endif
+  return launch_sp_pair<kSoftplusPairMask>(p, t, st, num_sms);
+}
+
+template <int ACT>
 cudaError_t launch_tc_act(const RunParams& p, const TcParams& t, cudaStream_t st, int num_sms) {
   constexpr int NG = (ACT == SL7_ACT_SOFTPLUS) ? kTcGroupsSoftplus : kTcGroups;
   constexpr unsigned NM = (ACT == SL7_ACT_TANH) ? kTanhNewtonMask : kSoftplusPolyMask;
@@ -485,6 +629,7 @@ int launch_tc_kernel(const RunParams& p, const TcParams& t, void* stream, int nu
   if (p.act == SL7_ACT_TANH && t.tanh_mufu) {
     return (int)launch_tc_act_x(p, t, st, num_sms);
   }
+  if (p.act == SL7_ACT_SOFTPLUS && !t.split) return (int)launch_softplus_bf16(p, t, st, num_sms);
   return (int)(p.act == SL7_ACT_TANH ? launch_tc_act<SL7_ACT_TANH>(p, t, st, num_sms)
                                      : launch_tc_act<SL7_ACT_SOFTPLUS>(p, t, st, num_sms));
 }
