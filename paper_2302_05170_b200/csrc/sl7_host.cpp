@@ -46,7 +46,7 @@ struct sl7_ctx_s {
   int width = 0;           // hidden width used by the FP32 kernel (50 or 64 padded)
   float* d_wf32 = nullptr;
   void* d_wtc = nullptr;   // bf16 SWIZZLE_128B operand image for the tcgen05 kernel
-  void* d_wtc_split = nullptr;   // the same with W split into three bf16 parts (SL7_PREC_SPLIT)
+  void* d_wtc_split = nullptr;   // W 2^s split into two fp16 parts per layer (SL7_PREC_SPLIT)
   void* d_wtc_tf32 = nullptr;    // tf32 operand image (SL7_PREC_TF32)
   TcParams tcp;            // biases + image pointer for the tcgen05 kernel
   int num_sms = 148;
@@ -259,6 +259,26 @@ uint16_t f32_to_bf16_rne(float f) {
   return (uint16_t)(u >> 16);
 }
 
+// fp16 (binary16) round-to-nearest-even of a finite |v| < 65504, and its value (SL7_PREC_SPLIT operands)
+uint16_t f32_to_f16_rne(float f) {
+  uint32_t x;
+  std::memcpy(&x, &f, 4);
+  const uint16_t sign = (uint16_t)((x >> 16) & 0x8000u);
+  const uint32_t ax = x & 0x7FFFFFFFu;
+  if (ax >= 0x38800000u) {                 // |f| >= 2^-14: normal binary16
+    uint32_t r = ax - 0x38000000u;         // exponent rebias 127 -> 15
+    r += 0xFFFu + ((r >> 13) & 1u);        // round the 23-bit mantissa to 10 bits, ties to even
+    return (uint16_t)(sign | (r >> 13));
+  }
+  // subnormal binary16: multiples of 2^-24 (the scaling by 2^24 is exact; nearbyint rounds ties to even)
+  return (uint16_t)(sign | (uint16_t)std::nearbyint(std::fabs((double)f) * 16777216.0));
+}
+float f16_value(uint16_t h) {
+  const int e = (h >> 10) & 0x1F, m = h & 0x3FF;
+  const double v = e ? std::ldexp(1024.0 + m, e - 25) : std::ldexp((double)m, -24);
+  return (float)((h & 0x8000u) ? -v : v);
+}
+
 // bf16 operand image of the MMA layers (layout: TcParams in sl7_internal.h) + fp32 biases.
 sl7_status build_tc_image(sl7_ctx c) {
   const int L = (int)c->dims.size() - 2;
@@ -269,37 +289,64 @@ sl7_status build_tc_image(sl7_ctx c) {
     std::memcpy(&f, &u, 4);
     return f;
   };
-  // np = 1: W rounded to bf16 (SL7_PREC_BF16).  np = 3: W = W0 + W1 + W2 split into bf16 parts
-  // (SL7_PREC_SPLIT); part p of hidden tile l at (np (l-1) + p) * 8 KB, output part p after them.
+  // np = 1: W rounded to bf16 (SL7_PREC_BF16).  np = 2 (SL7_PREC_SPLIT): W 2^s_l = W0 + W1 split into two
+  // fp16 parts (W0 = fp16(W 2^s), W1 = fp16(W 2^s - W0): 22 significant bits), s_l a per-layer power of two
+  // that puts max |W|, |b| of the layer at <= 2^14, so W1 stays out of the binary16 subnormals for all but
+  // the layer's smallest weights; part p of hidden tile l at (np (l-1) + p) * 8 KB, output part p after them.
+  auto layer_exp = [&](int l) {
+    const int fi = c->dims[l], fo = c->dims[l + 1];
+    double mx = 0.0;
+    for (int i = 0; i < fi * fo; ++i) mx = std::max(mx, (double)std::fabs(c->W[l][(size_t)i]));
+    for (int n = 0; n < fo; ++n) mx = std::max(mx, (double)std::fabs(c->b[l][n]));
+    if (!(mx > 0.0)) return 0;
+    int e;
+    std::frexp(mx, &e);                     // mx in [2^(e-1), 2^e)
+    return std::max(-60, std::min(60, 14 - e));
+  };
   auto build = [&](int np) {
     std::vector<uint16_t> img((size_t)np * (nL * kTcTileBytes + kTcOutBytes) / 2, 0);
-    auto put = [&](size_t tile_off_bytes, int n, int k, float v) {
+    auto put = [&](size_t tile_off_bytes, int n, int k, uint16_t v) {
       const size_t byte =
           tile_off_bytes + (size_t)n * 128 + (size_t)((((k * 2) >> 4) ^ (n & 7)) << 4) + (size_t)((k * 2) & 15);
-      img[byte / 2] = f32_to_bf16_rne(v);
+      img[byte / 2] = v;
     };
     for (int l = 1; l <= L; ++l) {   // blob layer l: hidden l -> hidden l+1 (l < L) or -> output (l == L)
       const int fi = c->dims[l], fo = c->dims[l + 1];
       const size_t part_bytes = (l < L) ? kTcTileBytes : kTcOutBytes;
       const size_t base = (l < L) ? (size_t)np * (l - 1) * kTcTileBytes : (size_t)np * nL * kTcTileBytes;
+      const int se = (np == 2) ? layer_exp(l) : 0;
+      c->tcp.split_exp[l - 1] = se;
       for (int n = 0; n < fo; ++n)
         for (int k = 0; k < fi; ++k) {
-          float r = c->W[l][(size_t)n * fi + k];
-          for (int pt = 0; pt < np; ++pt) {
-            const float q = bf(r);
-            put(base + pt * part_bytes, n, k, q);
-            r -= q;
+          const float w = c->W[l][(size_t)n * fi + k];
+          if (np == 1) {
+            put(base, n, k, f32_to_bf16_rne(w));
+          } else {
+            const float ws = std::ldexp(w, se);            // exact (power of two)
+            const uint16_t h0 = f32_to_f16_rne(ws);
+            put(base, n, k, h0);
+            put(base + part_bytes, n, k, f32_to_f16_rne(ws - f16_value(h0)));
           }
         }
       if (c->width == 50) {
         // the width-50 kernel (FOLD) feeds A = 1.0 in K columns 50..52 (part 0 only): the bias enters
-        // the fp32 accumulation as three bf16 terms whose sum reproduces the fp32 bias (hi + mid + lo)
+        // the fp32 accumulation as three terms whose sum reproduces the fp32 bias (hi + mid + lo)
         for (int n = 0; n < fo; ++n) {
-          const float b = c->b[l][n];
-          const float hi = bf(b), mid = bf(b - hi), lo = bf(b - hi - mid);
-          put(base, n, 50, hi);
-          put(base, n, 51, mid);
-          put(base, n, 52, lo);
+          if (np == 1) {
+            const float b = c->b[l][n];
+            const float hi = bf(b), mid = bf(b - hi), lo = bf(b - hi - mid);
+            put(base, n, 50, f32_to_bf16_rne(hi));
+            put(base, n, 51, f32_to_bf16_rne(mid));
+            put(base, n, 52, f32_to_bf16_rne(lo));
+          } else {
+            const float b = std::ldexp(c->b[l][n], se);
+            const uint16_t hi = f32_to_f16_rne(b);
+            const uint16_t mid = f32_to_f16_rne(b - f16_value(hi));
+            const uint16_t lo = f32_to_f16_rne(b - f16_value(hi) - f16_value(mid));
+            put(base, n, 50, hi);
+            put(base, n, 51, mid);
+            put(base, n, 52, lo);
+          }
         }
       }
     }
@@ -312,7 +359,7 @@ sl7_status build_tc_image(sl7_ctx c) {
       else c->tcp.bout[n] = c->b[l][n];
     }
   c->tcp.n_mma_hidden = nL;
-  for (int np : {1, 3}) {
+  for (int np : {1, 2}) {
     const std::vector<uint16_t> img = build(np);
     void*& d = (np == 1) ? c->d_wtc : c->d_wtc_split;
     if (d) cudaFree(d);
@@ -705,6 +752,9 @@ sl7_status run(sl7_ctx c, RunParams& p, const sl7_run_opts* o, float* d_out, dou
     }
     for (int l = 0; l < t.n_mma_hidden; ++l)
       for (int k = 0; k < kTcN; ++k) t.bias[l][k] = (float)((double)c->tcp.bias[l][k] * sc);
+    // the SPLIT image holds W 2^s_l: its accumulators are scaled back by 2^-s_l (exact) in the epilogue
+    for (int l = 0; l < t.n_mma_hidden; ++l) t.lscale[l] = (float)std::ldexp(sc, t.split ? -c->tcp.split_exp[l] : 0);
+    t.oscale = (float)std::ldexp(1.0, t.split ? -c->tcp.split_exp[t.n_mma_hidden] : 0);
     e = launch_tc_kernel(p, t, o->stream, c->num_sms);
   } else {
     e = launch_step_kernel(p, (int)o->prec, o->stream, c->num_sms);

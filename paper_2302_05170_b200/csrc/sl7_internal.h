@@ -105,8 +105,13 @@ struct TcParams {
   float l1w[kTcN], l1b[kTcN];         // layer 1 folded and scaled by act_scale
   float bias[kMaxHidden - 1][kTcN];   // hidden biases scaled by act_scale
   float bout[kTcNOut];
+  // accumulator scale of each hidden MMA layer (act_scale, times 2^-s_l for SL7_PREC_SPLIT whose weight
+  // image is W 2^s_l) and of the output layer (1, or 2^-s_out)
+  float lscale[kMaxHidden - 1];
+  float oscale;
+  int split_exp[kMaxHidden];   // SL7_PREC_SPLIT: s_l of the MMA layers (hidden 0..L-2, then the output)
   const void* wimg;
-  const void* wimg_split;   // SL7_PREC_SPLIT: per tile the three bf16 parts W = W0 + W1 + W2 in turn
+  const void* wimg_split;   // SL7_PREC_SPLIT: per tile the two fp16 parts of W 2^s = W0 + W1 in turn
   const void* wimg_tf32;    // SL7_PREC_TF32: tf32 (cvt.rna) tiles, two SWIZZLE_128B K-blocks [N][128 B] each
   int n_mma_hidden;   // L - 1
   int variant;        // activation variant (experiment hook, SL7_TC_VARIANT)

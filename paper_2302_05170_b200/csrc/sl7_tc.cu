@@ -155,18 +155,86 @@ __device__ __forceinline__ void softplus_pair(float u0, float u1, float& h0, flo
   up2(r, h0, h1);
 }
 
-// Pack two activations as NP bf16 parts: part 0 = bf16(h); NP = 3 (SL7_PREC_SPLIT) adds the rounded
-// residuals, so h = h0 + h1 + h2 to ~2^-24 relative (the split-precision A operand).
+// ---- accurate tanh of a pair (kActTanhPair; SPLIT and TF32): u = z 2 log2(e) (the scale is folded into
+// the accumulator scale), tanh|z| = 2 r - 1 with r = 1 / (1 + e), e = 2^-|u| in (0, 1]: absolute error
+// ~1.2e-7 (the same form as the MUFU ex2 + rcp epilogue).  NEWTON: r by a quadratic seed on [1, 2]
+// (1.7%) and two Newton steps (8e-8) in FFMA2 (8 FFMA2 per pair, 1 MUFU per unit); otherwise MUFU rcp.
+constexpr int kActTanhPair = 5;
+constexpr int kActSoftplusPairS = 6;   // softplus pairs with a scaled accumulator (SPLIT: 2^-s)
+
+template <bool NEWTON>
+__device__ __forceinline__ void tanh_pair(float u0, float u1, float& h0, float& h1) {
+  const uint64_t E = pk2(ex2_approx(-fabsf(u0)), ex2_approx(-fabsf(u1)));
+  uint64_t R;
+  if constexpr (NEWTON) {
+    const uint64_t NS = fma2(E, pk2(-1.0f, -1.0f), pk2(-1.0f, -1.0f));        // -(1 + e)
+    R = fma2(fma2s(NS, 0.30153724f, 1.39582404f), NS, pk2(2.08733358f, 2.08733358f));
+    R = fma2(R, fma2(NS, R, pk2(1.0f, 1.0f)), R);
+    R = fma2(R, fma2(NS, R, pk2(1.0f, 1.0f)), R);
+  } else {
+    float s0, s1;
+    up2(fma2(E, pk2(1.0f, 1.0f), pk2(1.0f, 1.0f)), s0, s1);
+    R = pk2(rcp_approx(s0), rcp_approx(s1));
+  }
+  float t0, t1;
+  up2(fma2(R, pk2(2.0f, 2.0f), pk2(-1.0f, -1.0f)), t0, t1);
+  h0 = copysignf(t0, u0);
+  h1 = copysignf(t1, u1);
+}
+
+__host__ __device__ constexpr bool is_pair_act(int act) {
+  return act == kActSoftplusPair || act == kActTanhPair || act == kActSoftplusPairS;
+}
+__host__ __device__ constexpr int base_act(int act) {
+  return act == kActTanhPair ? SL7_ACT_TANH : (is_pair_act(act) ? SL7_ACT_SOFTPLUS : act);
+}
+
+// one pair of units (c0, c0 + 1); NMASK bit (pair index % 8): polynomial log1p / Newton reciprocal.
+// Softplus NMASK bit 8: the degree-7 log1p (BF16 only; the fp32-class modes keep degree 8).
+template <int ACT, unsigned NMASK>
+__device__ __forceinline__ void act_pair(float u0, float u1, int c0, float& h0, float& h1) {
+  const bool alt = (NMASK >> ((c0 >> 1) & 7)) & 1u;
+  if constexpr (ACT == kActTanhPair) {
+    if (alt) tanh_pair<true>(u0, u1, h0, h1);
+    else tanh_pair<false>(u0, u1, h0, h1);
+  } else {
+    if (alt) softplus_pair<true, (NMASK & 0x100u) != 0>(u0, u1, h0, h1);
+    else softplus_pair<false>(u0, u1, h0, h1);
+  }
+}
+
+// the pre-activation of a pair unit: BF16 softplus takes the accumulator as is (the host folds no scale);
+// the others multiply by the layer's accumulator scale (FOLD) or add the scaled bias
+template <int ACT, bool FOLD>
+__device__ __forceinline__ float pair_u(float acc, float scale, const float* bs, int c) {
+  if constexpr (ACT == kActSoftplusPair) return FOLD ? acc : acc + bs[c];
+  else return FOLD ? acc * scale : fmaf(acc, scale, bs[c]);
+}
+
+// Pack two activations: NP = 1: bf16(h) (SL7_PREC_BF16).  NP = 2 (SL7_PREC_SPLIT): two fp16 parts,
+// h0 = fp16(h), h1 = fp16(h - h0): h = h0 + h1 to 2^-22 relative (absolute 2^-25 where h1 falls into the
+// binary16 subnormals), the fp32-class A operand of the three-product split MMA.
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ void unpack_f16x2(uint32_t w, float& lo, float& hi) {
+  asm("{\n\t.reg .f16 a, b;\n\tmov.b32 {a, b}, %2;\n\tcvt.f32.f16 %0, a;\n\tcvt.f32.f16 %1, b;\n\t}"
+      : "=f"(lo), "=f"(hi) : "r"(w));
+}
+
 template <int NP, int NW>
 __device__ __forceinline__ void split_pack(float a, float b, uint32_t (&pk)[NP][NW], int k) {
-  uint32_t w = tc::pack_bf16x2(a, b);
-  pk[0][k] = w;
-#pragma unroll
-  for (int part = 1; part < NP; ++part) {
-    a -= __uint_as_float(w << 16);
-    b -= __uint_as_float(w & 0xFFFF0000u);
-    w = tc::pack_bf16x2(a, b);
-    pk[part][k] = w;
+  static_assert(NP == 1 || NP == 2, "bf16 (1) or fp16 two-part (2)");
+  if constexpr (NP == 1) {
+    pk[0][k] = tc::pack_bf16x2(a, b);
+  } else {
+    const uint32_t w = pack_f16x2(a, b);
+    float a0, b0;
+    unpack_f16x2(w, a0, b0);
+    pk[0][k] = w;
+    pk[1][k] = pack_f16x2(a - a0, b - b0);
   }
 }
 
@@ -179,21 +247,17 @@ __device__ __forceinline__ void act_pack_32(const uint32_t (&v)[NC], int col0, f
   for (int k = 0; k < NC / 2; ++k) {
     float h[2];
     const int c0 = col0 + 2 * k;
-    if (ACT == kActSoftplusPair && c0 + 1 < H) {
-      // softplus: the host folds no scale (act_scale = 1), so u is the accumulator (+ bias)
-      const float u0 = FOLD ? __uint_as_float(v[2 * k]) : __uint_as_float(v[2 * k]) + bs[c0];
-      const float u1 = FOLD ? __uint_as_float(v[2 * k + 1]) : __uint_as_float(v[2 * k + 1]) + bs[c0 + 1];
-      if ((NMASK >> ((c0 >> 1) & 7)) & 1u) softplus_pair<true, (NMASK & 0x100u) != 0>(u0, u1, h[0], h[1]);
-      else softplus_pair<false>(u0, u1, h[0], h[1]);
+    if (is_pair_act(ACT) && c0 + 1 < H) {
+      act_pair<ACT, NMASK>(pair_u<ACT, FOLD>(__uint_as_float(v[2 * k]), scale, bs, c0),
+                           pair_u<ACT, FOLD>(__uint_as_float(v[2 * k + 1]), scale, bs, c0 + 1), c0, h[0], h[1]);
     } else {
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const int c = c0 + q;
         if (c < H) {
           const float acc = __uint_as_float(v[2 * k + q]);
-          if constexpr (ACT == kActSoftplusPair) {
-            const float u = FOLD ? acc : acc + bs[c];
-            h[q] = tc_act_u<SL7_ACT_SOFTPLUS>(u, false);
+          if constexpr (is_pair_act(ACT)) {
+            h[q] = tc_act_u<base_act(ACT)>(pair_u<ACT, FOLD>(acc, scale, bs, c), true);
           } else {
             const float u = FOLD ? (ACT == kActTanhX ? acc : acc * scale) : fmaf(acc, scale, bs[c]);
             h[q] = tc_act_u<ACT>(u, use_newton<ACT, NMASK>(c));
@@ -219,17 +283,31 @@ template <int ACT, int H, unsigned NMASK, bool FOLD>
 __device__ __forceinline__ void act_tf32_32(const uint32_t (&v)[32], int col0, float scale, const float* bs,
                                             uint32_t (&w)[32]) {
 #pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    const int c = col0 + k;
-    float h;
-    if (c < H) {
-      const float acc = __uint_as_float(v[k]);
-      const float u = FOLD ? (ACT == kActTanhX ? acc : acc * scale) : fmaf(acc, scale, bs[c]);
-      h = tc_act_u<ACT>(u, use_newton<ACT, NMASK>(c));
+  for (int k = 0; k < 32; k += 2) {
+    const int c0 = col0 + k;
+    float h[2];
+    if (is_pair_act(ACT) && c0 + 1 < H) {
+      act_pair<ACT, NMASK>(pair_u<ACT, FOLD>(__uint_as_float(v[k]), scale, bs, c0),
+                           pair_u<ACT, FOLD>(__uint_as_float(v[k + 1]), scale, bs, c0 + 1), c0, h[0], h[1]);
     } else {
-      h = (FOLD && c < H + 3) ? 1.0f : 0.0f;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int c = c0 + q;
+        if (c < H) {
+          const float acc = __uint_as_float(v[k + q]);
+          if constexpr (is_pair_act(ACT)) {
+            h[q] = tc_act_u<base_act(ACT)>(pair_u<ACT, FOLD>(acc, scale, bs, c), true);
+          } else {
+            const float u = FOLD ? (ACT == kActTanhX ? acc : acc * scale) : fmaf(acc, scale, bs[c]);
+            h[q] = tc_act_u<ACT>(u, use_newton<ACT, NMASK>(c));
+          }
+        } else {
+          h[q] = (FOLD && c < H + 3) ? 1.0f : 0.0f;
+        }
+      }
     }
-    w[k] = tf32_rna(h);
+    w[k] = tf32_rna(h[0]);
+    w[k + 1] = tf32_rna(h[1]);
   }
 }
 
@@ -246,14 +324,14 @@ __device__ __forceinline__ void issue_layer_tf32(uint32_t acc_t, uint32_t a_t, u
 }
 
 // MMA issue for one layer: sum over (A part, B part) pairs of [128 x 64] x [64 x N] with K = 4 x 16.
-// NP = 1: bf16 x bf16.  NP = 3: the six pairs whose products are >= 2^-16 of the leading one
-// (hh, hm, mh, hl, lh, mm): fp32-class products from bf16 tensor cores.
+// NP = 1: bf16 x bf16.  NP = 2 (fp16 parts): h0 W0 + h0 W1 + h1 W0 -- the dropped h1 W1 is 2^-22 of the
+// leading product, so the layer is fp32-class from three f16 tensor-core products.
 template <int NP>
 __device__ __forceinline__ void issue_layer(uint32_t acc_t, uint32_t a_t, uint32_t b_base, uint32_t b_part_bytes,
                                             uint32_t idesc) {
-  constexpr int NPAIR = (NP == 1) ? 1 : 6;
-  constexpr int PA[6] = {0, 0, 1, 0, 2, 1};
-  constexpr int PB[6] = {0, 1, 0, 2, 0, 1};
+  constexpr int NPAIR = (NP == 1) ? 1 : 3;
+  constexpr int PA[3] = {0, 0, 1};
+  constexpr int PB[3] = {0, 1, 0};
 #pragma unroll
   for (int pr = 0; pr < NPAIR; ++pr) {
     const uint64_t bdesc = tc::smem_desc_sw128(b_base + (uint32_t)PB[pr] * b_part_bytes);
@@ -280,7 +358,7 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
   const int wq = warp & 3;                 // warp within the group -> TMEM lanes [32 wq, 32 wq + 32)
   const int tid_g = threadIdx.x & (kGroupThreads - 1);
   static_assert(!TF32 || NP == 1, "TF32 has one operand part");
-  constexpr uint32_t kCols = kAccCol + 64u + (TF32 ? 64u : 32u * NP);   // acc fp32 [0,64) + A (NP bf16 parts | tf32)
+  constexpr uint32_t kCols = kAccCol + 64u + (TF32 ? 64u : 32u * NP);   // acc fp32 [0,64) + A (NP 16-bit parts | tf32)
   constexpr uint32_t kTileB = TF32 ? 2u * kTcTileBytes : (uint32_t)kTcTileBytes;   // bytes per weight tile part
   constexpr uint32_t kOutB = TF32 ? 2u * kTcOutBytes : (uint32_t)kTcOutBytes;
   constexpr uint32_t kTmemCols = NG * kCols <= 256 ? 256u : 512u;
@@ -320,8 +398,10 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
   const uint32_t gcol = tbase + (uint32_t)g * kCols;
   const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
   const uint32_t acc_t = gcol + kAccCol, a_t = gcol + kACol;
-  constexpr uint32_t idesc_h = TF32 ? tc::idesc_tf32_f32(128, kTcN) : tc::idesc_bf16_f32(128, kTcN);
-  constexpr uint32_t idesc_o = TF32 ? tc::idesc_tf32_f32(128, kTcNOut) : tc::idesc_bf16_f32(128, kTcNOut);
+  constexpr uint32_t idesc_h = TF32 ? tc::idesc_tf32_f32(128, kTcN)
+                                    : (NP == 2 ? tc::idesc_f16_f32(128, kTcN) : tc::idesc_bf16_f32(128, kTcN));
+  constexpr uint32_t idesc_o = TF32 ? tc::idesc_tf32_f32(128, kTcNOut)
+                                    : (NP == 2 ? tc::idesc_f16_f32(128, kTcNOut) : tc::idesc_bf16_f32(128, kTcNOut));
   uint64_t* bar = &mbar[g];
   uint32_t phase = 0;
 
@@ -345,37 +425,32 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
       // ---- layer 1 (fp32, rank 1 in Y) -> A operand in TMEM, two 32-unit halves
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
+        float h[32];
+#pragma unroll
+        for (int k = 0; k < 32; k += 2) {
+          const int c0 = 32 * half + k;
+          if (is_pair_act(ACT) && c0 + 1 < H) {
+            act_pair<ACT, NMASK>(fmaf(Y, t.l1w[c0], t.l1b[c0]), fmaf(Y, t.l1w[c0 + 1], t.l1b[c0 + 1]), c0, h[k],
+                                 h[k + 1]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int c = c0 + q;
+              h[k + q] = (c < H) ? tc_act_u<base_act(ACT)>(fmaf(Y, t.l1w[c], t.l1b[c]),
+                                                           is_pair_act(ACT) || use_newton<ACT, NMASK>(c))
+                                 : ((FOLD && c < H + 3) ? 1.0f : 0.0f);
+            }
+          }
+        }
         if constexpr (TF32) {
           uint32_t w[32];
 #pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            const int c = 32 * half + k;
-            w[k] = tf32_rna((c < H) ? tc_act_u<ACT>(fmaf(Y, t.l1w[c], t.l1b[c]), use_newton<ACT, NMASK>(c))
-                                    : ((FOLD && c < H + 3) ? 1.0f : 0.0f));
-          }
+          for (int k = 0; k < 32; ++k) w[k] = tf32_rna(h[k]);
           tc::tmem_st_32x32b_x32(a_t + lane_off + 32u * half, w);
         } else {
           uint32_t pk[NP][16];
 #pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            float h[2];
-            const int c0 = 32 * half + 2 * k;
-            if (ACT == kActSoftplusPair && c0 + 1 < H) {
-              const float u0 = fmaf(Y, t.l1w[c0], t.l1b[c0]), u1 = fmaf(Y, t.l1w[c0 + 1], t.l1b[c0 + 1]);
-              if ((NMASK >> ((c0 >> 1) & 7)) & 1u) softplus_pair<true, (NMASK & 0x100u) != 0>(u0, u1, h[0], h[1]);
-              else softplus_pair<false>(u0, u1, h[0], h[1]);
-            } else {
-#pragma unroll
-              for (int q = 0; q < 2; ++q) {
-                const int c = c0 + q;
-                constexpr int A1 = (ACT == kActSoftplusPair) ? SL7_ACT_SOFTPLUS : ACT;
-                h[q] = (c < H) ? tc_act_u<A1>(fmaf(Y, t.l1w[c], t.l1b[c]),
-                                              ACT != kActSoftplusPair && use_newton<ACT, NMASK>(c))
-                               : ((FOLD && c < H + 3) ? 1.0f : 0.0f);
-              }
-            }
-            split_pack<NP>(h[0], h[1], pk, k);
-          }
+          for (int k = 0; k < 16; ++k) split_pack<NP>(h[2 * k], h[2 * k + 1], pk, k);
 #pragma unroll
           for (int part = 0; part < NP; ++part)
             tc::tmem_st_32x32b_x16(a_t + 32u * part + lane_off + 16u * half, pk[part]);
@@ -421,7 +496,7 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
                 tc::tmem_ld_32x32b_x16(acc_t + lane_off + 16u * qt, v);
                 tc::wait_ld();
                 uint32_t pk[NP][8];
-                act_pack_32<ACT, H, NMASK, FOLD, NP, 16>(v, 16 * qt, t.act_scale, t.bias[l], pk);
+                act_pack_32<ACT, H, NMASK, FOLD, NP, 16>(v, 16 * qt, t.lscale[l], t.bias[l], pk);
 #pragma unroll
                 for (int part = 0; part < NP; ++part)
                   tc::tmem_st_32x32b_x8(a_t + 32u * part + lane_off + 8u * qt, pk[part]);
@@ -435,11 +510,11 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
             tc::wait_ld();
             if constexpr (TF32) {
               uint32_t w[32];
-              act_tf32_32<ACT, H, NMASK, FOLD>(v, 32 * half, t.act_scale, t.bias[l], w);
+              act_tf32_32<ACT, H, NMASK, FOLD>(v, 32 * half, t.lscale[l], t.bias[l], w);
               tc::tmem_st_32x32b_x32(a_t + lane_off + 32u * half, w);
             } else {
               uint32_t pk[NP][16];
-              act_pack_32<ACT, H, NMASK, FOLD, NP>(v, 32 * half, t.act_scale, t.bias[l], pk);
+              act_pack_32<ACT, H, NMASK, FOLD, NP>(v, 32 * half, t.lscale[l], t.bias[l], pk);
 #pragma unroll
               for (int part = 0; part < NP; ++part)
                 tc::tmem_st_32x32b_x16(a_t + 32u * part + lane_off + 16u * half, pk[part]);
@@ -452,9 +527,10 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
           tc::tmem_ld_32x32b_x16(acc_t + lane_off, v);
           tc::wait_ld();
 #pragma unroll
-          for (int j = 0; j < MR; ++j)
-            y[j] = fmaf(p.res_y, Y, fmaf(FOLD ? __uint_as_float(v[j]) : __uint_as_float(v[j]) + t.bout[j],
-                                         p.out_scale[j], p.out_shift[j]));
+          for (int j = 0; j < MR; ++j) {
+            const float acc = (NP == 2) ? __uint_as_float(v[j]) * t.oscale : __uint_as_float(v[j]);
+            y[j] = fmaf(p.res_y, Y, fmaf(FOLD ? acc : acc + t.bout[j], p.out_scale[j], p.out_shift[j]));
+          }
         }
       }
       // ---- steps 5-6: Y_{i+1} = g_m(X_hat)
@@ -515,8 +591,8 @@ constexpr int kTcGroups = 4;
 constexpr unsigned kTanhNewtonMask = 0x55u;
 constexpr unsigned kSoftplusPolyMask = 0x55u;
 
-// SL7_PREC_SPLIT: three bf16 parts per operand (TMEM 64 + 3 x 32 = 160 columns per group -> 3 groups).
-constexpr int kTcGroupsSplit = 3;
+// SL7_PREC_SPLIT: two fp16 parts per operand (TMEM 64 + 2 x 32 = 128 columns per group -> 4 groups).
+constexpr int kTcGroupsSplit = 4;
 
 // softplus (2 MUFU ops per unit on half of the units): 5 groups per SM, as for tanh (cfg2: 1.03e10 vs 9.4e9)
 constexpr int kTcGroupsSoftplus = 5;
@@ -555,22 +631,51 @@ cudaError_t launch_softplus_bf16(const RunParams& p, const TcParams& t, cudaStre
     case 34: return launch_sp_pair<0x35Fu>(p, t, st, num_sms);
     case 35: return launch_sp_pair<0x377u>(p, t, st, num_sms);
     case 36: return launch_sp_pair<0x3FFu>(p, t, st, num_sms);
+    case 37: return launch_tc_t<kTcGroupsSoftplus, 50, 7, false, kActSoftplusPair, 0x15Fu, 1, true>(p, t, st, num_sms);
+    case 38: return launch_tc_t<4, 50, 7, false, kActSoftplusPair, 0x15Fu>(p, t, st, num_sms);
     default: break;
   }
 #endif
   return launch_sp_pair<kSoftplusPairMask>(p, t, st, num_sms);
 }
 
+// SL7_PREC_SPLIT / TF32: accurate activations in FFMA2 pairs; NMASK bit (pair % 8) = Newton reciprocal
+// (tanh) / polynomial log1p (softplus, degree 8) on that pair, the others on MUFU
+constexpr unsigned kSplitTanhMask = 0x77u;
+constexpr unsigned kSplitSoftplusMask = 0x7Fu;
+
+template <int NG, int PACT, unsigned PM, int NP, bool TF32>
+cudaError_t launch_pairs(const RunParams& p, const TcParams& t, cudaStream_t st, int num_sms) {
+  if (p.width == 50 && p.m == 5) return launch_tc_t<NG, 50, 5, false, PACT, PM, NP, false, TF32>(p, t, st, num_sms);
+  if (p.width == 50 && p.m == 7) return launch_tc_t<NG, 50, 7, false, PACT, PM, NP, false, TF32>(p, t, st, num_sms);
+  return launch_tc_t<NG, 64, kMaxM, true, PACT, PM, NP, false, TF32>(p, t, st, num_sms);
+}
+
+template <int NG, int NP, bool TF32>
+cudaError_t launch_accurate(const RunParams& p, const TcParams& t, cudaStream_t st, int num_sms) {
+  const bool tanh = (p.act == SL7_ACT_TANH);
+#ifdef SL7_AB_HOOKS
+  switch (t.variant) {   // A/B hook: share of Newton / polynomial pairs
+    case 40: return tanh ? launch_pairs<NG, kActTanhPair, 0x55u, NP, TF32>(p, t, st, num_sms)
+                         : launch_pairs<NG, kActSoftplusPairS, 0x55u, NP, TF32>(p, t, st, num_sms);
+    case 41: return tanh ? launch_pairs<NG, kActTanhPair, 0x7Fu, NP, TF32>(p, t, st, num_sms)
+                         : launch_pairs<NG, kActSoftplusPairS, 0x7Fu, NP, TF32>(p, t, st, num_sms);
+    case 42: return tanh ? launch_pairs<NG, kActTanhPair, 0xFFu, NP, TF32>(p, t, st, num_sms)
+                         : launch_pairs<NG, kActSoftplusPairS, 0xFFu, NP, TF32>(p, t, st, num_sms);
+    case 43: return tanh ? launch_pairs<NG, kActTanhPair, 0x5Fu, NP, TF32>(p, t, st, num_sms)
+                         : launch_pairs<NG, kActSoftplusPairS, 0x5Fu, NP, TF32>(p, t, st, num_sms);
+    default: break;
+  }
+#endif
+  return tanh ? launch_pairs<NG, kActTanhPair, kSplitTanhMask, NP, TF32>(p, t, st, num_sms)
+              : launch_pairs<NG, kActSoftplusPairS, kSplitSoftplusMask, NP, TF32>(p, t, st, num_sms);
+}
+
 template <int ACT>
 cudaError_t launch_tc_act(const RunParams& p, const TcParams& t, cudaStream_t st, int num_sms) {
   constexpr int NG = (ACT == SL7_ACT_SOFTPLUS) ? kTcGroupsSoftplus : kTcGroups;
   constexpr unsigned NM = (ACT == SL7_ACT_TANH) ? kTanhNewtonMask : kSoftplusPolyMask;
-  if (t.split) {
-    constexpr int NS = kTcGroupsSplit;
-    if (p.width == 50 && p.m == 5) return launch_tc_t<NS, 50, 5, false, ACT, NM, 3>(p, t, st, num_sms);
-    if (p.width == 50 && p.m == 7) return launch_tc_t<NS, 50, 7, false, ACT, NM, 3>(p, t, st, num_sms);
-    return launch_tc_t<NS, 64, kMaxM, true, ACT, NM, 3>(p, t, st, num_sms);
-  }
+  if (t.split) return launch_accurate<kTcGroupsSplit, 2, false>(p, t, st, num_sms);
   if (p.width == 50 && p.m == 5) return launch_tc_t<NG, 50, 5, false, ACT, NM>(p, t, st, num_sms);
   if (p.width == 50 && p.m == 7) {
     switch (t.variant) {   // A/B hook (SL7_TC_VARIANT): fraction of units with the FMA-pipe transcendental
@@ -594,12 +699,7 @@ constexpr int kTcGroupsTanhX = 5;
 cudaError_t launch_tc_act_x(const RunParams& p, const TcParams& t, cudaStream_t st, int num_sms) {
   constexpr int NG = kTcGroupsTanhX;
   constexpr unsigned NM = 0x00u;
-  if (t.split) {
-    constexpr int NS = kTcGroupsSplit;
-    if (p.width == 50 && p.m == 5) return launch_tc_t<NS, 50, 5, false, kActTanhX, NM, 3>(p, t, st, num_sms);
-    if (p.width == 50 && p.m == 7) return launch_tc_t<NS, 50, 7, false, kActTanhX, NM, 3>(p, t, st, num_sms);
-    return launch_tc_t<NS, 64, kMaxM, true, kActTanhX, NM, 3>(p, t, st, num_sms);
-  }
+  // (SPLIT never takes MUFU.TANH: the host clears tanh_mufu for it)
   if (p.width == 50 && p.m == 5) return launch_tc_t<NG, 50, 5, false, kActTanhX, NM>(p, t, st, num_sms);
   if (p.width == 50 && p.m == 7) return launch_tc_t<NG, 50, 7, false, kActTanhX, NM>(p, t, st, num_sms);
   return launch_tc_t<NG, 64, kMaxM, true, kActTanhX, NM>(p, t, st, num_sms);
@@ -610,22 +710,13 @@ cudaError_t launch_tc_act_x(const RunParams& p, const TcParams& t, cudaStream_t 
 // SL7_PREC_TF32: TMEM 64 + 64 columns per group -> 4 groups (512 columns)
 constexpr int kTcGroupsTf32 = 4;
 
-template <int ACT, unsigned NM>
-cudaError_t launch_tc_tf32(const RunParams& p, const TcParams& t, cudaStream_t st, int num_sms) {
-  constexpr int NG = kTcGroupsTf32;
-  if (p.width == 50 && p.m == 5) return launch_tc_t<NG, 50, 5, false, ACT, NM, 1, false, true>(p, t, st, num_sms);
-  if (p.width == 50 && p.m == 7) return launch_tc_t<NG, 50, 7, false, ACT, NM, 1, false, true>(p, t, st, num_sms);
-  return launch_tc_t<NG, 64, kMaxM, true, ACT, NM, 1, false, true>(p, t, st, num_sms);
-}
 
 int launch_tc_kernel(const RunParams& p, const TcParams& t, void* stream, int num_sms) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   // TF32 takes its rna rounding decisions on an accurate tanh (ex2 + reciprocal, ~2e-7 absolute): MUFU.TANH's
   // 1e-5 flips a few tf32 roundings of the one shared step-0 evaluation, which shifts every path's points
   // together (reading R-15), so the tf32 moments would not match O6 on the identical path set (T-4)
-  if (t.tf32)
-    return (int)(p.act == SL7_ACT_TANH ? launch_tc_tf32<SL7_ACT_TANH, kTanhNewtonMask>(p, t, st, num_sms)
-                                       : launch_tc_tf32<SL7_ACT_SOFTPLUS, kSoftplusPolyMask>(p, t, st, num_sms));
+  if (t.tf32) return (int)launch_accurate<kTcGroupsTf32, 1, true>(p, t, st, num_sms);
   if (p.act == SL7_ACT_TANH && t.tanh_mufu) {
     return (int)launch_tc_act_x(p, t, st, num_sms);
   }
