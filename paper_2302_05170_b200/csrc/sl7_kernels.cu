@@ -9,6 +9,9 @@
 // FULL-mode store of step i by a warp is one contiguous 128-byte segment of row i.
 #include <cuda_runtime.h>
 
+#include <cstdint>
+#include <cstdlib>
+
 #include "sl7_device.cuh"
 
 namespace sl7 {
@@ -132,6 +135,148 @@ __global__ void __launch_bounds__(256) exact_special_kernel(const __grid_constan
     }
     if (p.out_mode == kTerminal) p.out[q] = Y;
     if (p.has_stats) stat_add(acc, p, Y, REF_ON ? ref_final(rs, p) : 0.0, hist);
+  }
+  if (p.has_stats) stat_flush(acc, p, hist, red);
+}
+
+// FULL-output form for the HBM-store-bound cfg3 (§8(a7)): each thread carries FOUR consecutive paths
+// through all steps and writes each step's row segment as one 16-byte store (st.global.cs.v4: the 52 GB
+// path tensor is written once and never re-read by the kernel, so it is marked evict-first).  A warp's
+// store is 512 contiguous bytes of row i.  The arithmetic of two paths at a time runs in FFMA2
+// (fma.rn.f32x2): the fast Box-Muller of box_muller_fast and the closed-form Horner of special_step,
+// operation for operation (bit-identical results, fewer issue slots).  Needs n_paths % 4 == 0 and a
+// 16-byte aligned output (the launcher falls back to exact_special_kernel otherwise).
+namespace {
+__device__ __forceinline__ uint64_t f2pk(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2up(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2c(float c) { return f2pk(c, c); }
+// (2 (r >> 9) + 1) 2^-24 exactly: the float 1 + (r >> 9) 2^-23, minus (1 - 2^-24)
+__device__ __forceinline__ float unit_bits(uint32_t r) { return __uint_as_float(0x3F800000u | (r >> 9)); }
+
+// box_muller_fast for two (ra, rb) word pairs at once (paths p and q); returns W = -Z (the sign is folded
+// into the Horner coefficients of the caller): Wa = rad cos(a), Wb = rad sin(a)
+__device__ __forceinline__ void box_muller_fast_x2(uint32_t rap, uint32_t rbp, uint32_t raq, uint32_t rbq,
+                                                   uint64_t& Wa, uint64_t& Wb) {
+  const uint64_t UA = f2fma(f2pk(unit_bits(rap), unit_bits(raq)), f2c(1.0f), f2c(-0.99999994039535522f));
+  const uint64_t UB = f2fma(f2pk(unit_bits(rbp), unit_bits(rbq)), f2c(1.0f), f2c(-0.99999994039535522f));
+  const uint64_t V = f2fma(UA, f2c(-1.0f), f2c(1.0f));
+  uint64_t P = f2fma(V, f2c(0.2f), f2c(0.25f));
+  P = f2fma(P, V, f2c(0.33333333f));
+  P = f2fma(P, V, f2c(0.5f));
+  P = f2fma(P, V, f2c(1.0f));
+  const uint64_t SER = f2fma(f2fma(V, f2c(2.0f), f2c(0.0f)), P, f2c(0.0f));
+  float uap, uaq, vp, vq, sp, sq;
+  f2up(UA, uap, uaq);
+  const uint64_t LG = f2fma(f2pk(lg2_fast(uap), lg2_fast(uaq)), f2c(-1.3862943611198906f), f2c(0.0f));
+  float lp, lq;
+  f2up(V, vp, vq);
+  f2up(SER, sp, sq);
+  f2up(LG, lp, lq);
+  float rp, rq;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(rp) : "f"((vp < 0.0625f) ? sp : lp));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(rq) : "f"((vq < 0.0625f) ? sq : lq));
+  float ap, aq;
+  f2up(f2fma(f2fma(UB, f2c(1.0f), f2c(-0.5f)), f2c(6.2831853071795865f), f2c(0.0f)), ap, aq);
+  float snp, snq, csp, csq;
+  asm("sin.approx.f32 %0, %1;" : "=f"(snp) : "f"(ap));
+  asm("cos.approx.f32 %0, %1;" : "=f"(csp) : "f"(ap));
+  asm("sin.approx.f32 %0, %1;" : "=f"(snq) : "f"(aq));
+  asm("cos.approx.f32 %0, %1;" : "=f"(csq) : "f"(aq));
+  const uint64_t RAD = f2pk(rp, rq);
+  Wa = f2fma(RAD, f2pk(csp, csq), f2c(0.0f));
+  Wb = f2fma(RAD, f2pk(snp, snq), f2c(0.0f));
+}
+}  // namespace
+
+template <int MR, int COLLOC, bool FAST, bool REF_ON, bool CS, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) exact_full4_kernel(const __grid_constant__ RunParams p) {
+  static_assert(COLLOC == kExactGbm && FAST, "FFMA2 full-output kernel: GBM closed form, fast normals");
+  extern __shared__ uint32_t hist[];
+  __shared__ double red[8];
+  hist_init(p, hist);
+  __syncthreads();
+  StatAcc acc;
+  // Horner in W = -Z: q'_j = (-1)^(MR-1-j) q_j gives qz' = (-1)^(MR-1) qz, rounding for rounding
+  uint64_t QC[MR];
+#pragma unroll
+  for (int j = 0; j < MR; ++j) QC[j] = f2c(((MR - 1 - j) & 1) ? -p.q[j] : p.q[j]);
+  constexpr float kSign = ((MR - 1) & 1) ? -1.0f : 1.0f;
+  const uint64_t n4 = p.n_paths >> 2, stride = (uint64_t)gridDim.x * blockDim.x;
+  const int nb = (p.n_steps + 3) >> 2;
+  for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n4; g += stride) {
+    const uint64_t gp = p.path_offset + 4 * g;
+    uint64_t Y01 = f2c(p.y0), Y23 = f2c(p.y0);
+    float4* o = reinterpret_cast<float4*>(p.out) + g;
+    auto put = [&](float4* a) {
+      float4 v;
+      f2up(Y01, v.x, v.y);
+      f2up(Y23, v.z, v.w);
+      if constexpr (CS) __stcs(a, v);
+      else *a = v;
+    };
+    put(o);
+    RefState rs[4];
+    if (REF_ON)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) ref_init(rs[u], p);
+    for (int b = 0; b < nb; ++b) {
+      uint4 r[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) r[u] = philox_path_block_rk(p.rk0, p.rk1, gp + u, (uint32_t)b);
+      // W[k][pair]: step k of the block for paths (0,1) and (2,3)
+      uint64_t W[4][2];
+      box_muller_fast_x2(r[0].x, r[0].y, r[1].x, r[1].y, W[0][0], W[1][0]);
+      box_muller_fast_x2(r[2].x, r[2].y, r[3].x, r[3].y, W[0][1], W[1][1]);
+      box_muller_fast_x2(r[0].z, r[0].w, r[1].z, r[1].w, W[2][0], W[3][0]);
+      box_muller_fast_x2(r[2].z, r[2].w, r[3].z, r[3].w, W[2][1], W[3][1]);
+      const int ns = (p.n_steps - 4 * b < 4) ? p.n_steps - 4 * b : 4;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (k < ns) {
+          uint64_t q01 = QC[MR - 1], q23 = QC[MR - 1];
+#pragma unroll
+          for (int j = MR - 2; j >= 0; --j) {
+            q01 = f2fma(q01, W[k][0], QC[j]);
+            q23 = f2fma(q23, W[k][1], QC[j]);
+          }
+          Y01 = f2fma(Y01, q01, f2c(0.0f));
+          Y23 = f2fma(Y23, q23, f2c(0.0f));
+          if constexpr (kSign < 0.0f) {
+            Y01 = f2fma(Y01, f2c(-1.0f), f2c(0.0f));
+            Y23 = f2fma(Y23, f2c(-1.0f), f2c(0.0f));
+          }
+          if (REF_ON) {
+            float w0, w1, w2, w3;
+            f2up(W[k][0], w0, w1);
+            f2up(W[k][1], w2, w3);
+            ref_step(rs[0], p, -w0);
+            ref_step(rs[1], p, -w1);
+            ref_step(rs[2], p, -w2);
+            ref_step(rs[3], p, -w3);
+          }
+          o += n4;
+          put(o);
+        }
+      }
+    }
+    if (p.has_stats) {
+      float y[4];
+      f2up(Y01, y[0], y[1]);
+      f2up(Y23, y[2], y[3]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) stat_add(acc, p, y[u], REF_ON ? ref_final(rs[u], p) : 0.0, hist);
+    }
   }
   if (p.has_stats) stat_flush(acc, p, hist, red);
 }
@@ -330,8 +475,37 @@ cudaError_t launch_exact_special_r(const RunParams& p, cudaStream_t st, int num_
   return launch_persistent(exact_special_kernel<7, COLLOC, FAST, REF_ON>, 256, smem, p, st, num_sms);
 }
 
+template <int COLLOC, bool FAST, bool REF_ON, bool CS, int MINB = 1>
+cudaError_t launch_exact_full4_r(const RunParams& p, cudaStream_t st, int num_sms, size_t smem) {
+  if (p.m != 5 && p.m != 7)
+    return launch_persistent(exact_full4_kernel<8, COLLOC, FAST, REF_ON, CS, MINB>, 256, smem, p, st, num_sms, 1024);
+  if (p.m == 5)
+    return launch_persistent(exact_full4_kernel<5, COLLOC, FAST, REF_ON, CS, MINB>, 256, smem, p, st, num_sms, 1024);
+  return launch_persistent(exact_full4_kernel<7, COLLOC, FAST, REF_ON, CS, MINB>, 256, smem, p, st, num_sms, 1024);
+}
+
 template <int COLLOC, bool FAST>
 cudaError_t launch_exact_special(const RunParams& p, cudaStream_t st, int num_sms, size_t smem) {
+  const bool v4 = COLLOC == kExactGbm && FAST && p.out_mode == kFull && (p.n_paths & 3) == 0 &&
+                  (reinterpret_cast<uintptr_t>(p.out) & 15) == 0;
+  int variant = 0;
+#ifdef SL7_AB_HOOKS
+  if (const char* v = std::getenv("SL7_TC_VARIANT")) variant = std::atoi(v);   // 50: one path per thread
+#endif
+  if constexpr (COLLOC == kExactGbm && FAST) {
+    if (v4 && variant != 50) {
+      const bool ref = p.ref != kRefNone && p.has_stats;
+      if (variant == 51) return ref ? launch_exact_full4_r<COLLOC, FAST, true, false>(p, st, num_sms, smem)
+                                    : launch_exact_full4_r<COLLOC, FAST, false, false>(p, st, num_sms, smem);
+      if (variant == 52) return ref ? launch_exact_full4_r<COLLOC, FAST, true, true, 4>(p, st, num_sms, smem)
+                                    : launch_exact_full4_r<COLLOC, FAST, false, true, 4>(p, st, num_sms, smem);
+      if (variant == 53) return ref ? launch_exact_full4_r<COLLOC, FAST, true, true, 3>(p, st, num_sms, smem)
+                                    : launch_exact_full4_r<COLLOC, FAST, false, true, 3>(p, st, num_sms, smem);
+      // 4 CTAs of 256 per SM (<= 64 registers): 9.0e11 vs 8.8e11 path-steps/s at 3 (cfg3, B200)
+      return ref ? launch_exact_full4_r<COLLOC, FAST, true, true, 4>(p, st, num_sms, smem)
+                 : launch_exact_full4_r<COLLOC, FAST, false, true, 4>(p, st, num_sms, smem);
+    }
+  }
   return (p.ref != kRefNone && p.has_stats) ? launch_exact_special_r<COLLOC, FAST, true>(p, st, num_sms, smem)
                                             : launch_exact_special_r<COLLOC, FAST, false>(p, st, num_sms, smem);
 }
