@@ -222,6 +222,87 @@ __device__ __forceinline__ float activate(float z) {
 }
 
 // ------------------------------------------------------------------------------------------------
+// Packed fp32 pairs (sm_100a FFMA2, fma.rn.f32x2): two units / two paths per instruction.  FFMA2 has the
+// FFMA FLOP rate at half the instructions and co-issues with MUFU better than FFMA (profiles/r02_pipes.md).
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void up2(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t fma2s(uint64_t a, float b, float c) { return fma2(a, pk2(b, b), pk2(c, c)); }
+
+// softplus of a pair.  POLY: log1p(e), e = 2^(-|u| log2 e) in (0, 1], as e q(e) with q the degree-7
+// minimax polynomial of log1p(e)/e on [0, 1] (absolute error 2.5e-8 in exact arithmetic, 1.6e-7 after fp32
+// Horner rounding, mean -1.4e-8 over e^-|u|, u ~ N(0, 2)); the last Horner step adds max(u, 0):
+//   h = e q(e) + max(u, 0)   (8 FFMA2 per pair).
+// Otherwise: h = ln 2 lg2(1 + e) + max(u, 0) with MUFU lg2 (FADD2 / FFMA2 for the pair).
+template <bool POLY, bool DEG7 = false>
+__device__ __forceinline__ void softplus_pair(float u0, float u1, float& h0, float& h1) {
+  const float e0 = ex2_approx(fabsf(u0) * -1.4426950408889634f);
+  const float e1 = ex2_approx(fabsf(u1) * -1.4426950408889634f);
+  const uint64_t mx = pk2(fmaxf(u0, 0.0f), fmaxf(u1, 0.0f));
+  const uint64_t E = pk2(e0, e1);
+  uint64_t r;
+  if constexpr (POLY && DEG7) {
+    // degree-6 q (total degree 7): minimax error 1.8e-7, 3.4e-7 after fp32 rounding, mean -3.3e-8
+    uint64_t q = fma2s(E, 1.081165298819542e-02f, -5.5391568690538406e-02f);
+    q = fma2(q, E, pk2(1.351390779018402e-01f, 1.351390779018402e-01f));
+    q = fma2(q, E, pk2(-2.263084203004837e-01f, -2.263084203004837e-01f));
+    q = fma2(q, E, pk2(3.284189999103546e-01f, 3.284189999103546e-01f));
+    q = fma2(q, E, pk2(-4.995054006576538e-01f, -4.995054006576538e-01f));
+    q = fma2(q, E, pk2(9.99983012676239e-01f, 9.99983012676239e-01f));
+    r = fma2(q, E, mx);
+  } else if constexpr (POLY) {
+    uint64_t q = fma2s(E, -6.678603123873472e-03f, 3.697235882282257e-02f);
+    q = fma2(q, E, pk2(-9.672726690769196e-02f, -9.672726690769196e-02f));
+    q = fma2(q, E, pk2(1.6879309713840485e-01f, 1.6879309713840485e-01f));
+    q = fma2(q, E, pk2(-2.412412464618683e-01f, -2.412412464618683e-01f));
+    q = fma2(q, E, pk2(3.3191972970962524e-01f, 3.3191972970962524e-01f));
+    q = fma2(q, E, pk2(-4.998879134654999e-01f, -4.998879134654999e-01f));
+    q = fma2(q, E, pk2(9.999969601631165e-01f, 9.999969601631165e-01f));
+    r = fma2(q, E, mx);
+  } else {
+    float a0, a1;
+    up2(fma2(E, pk2(1.0f, 1.0f), pk2(1.0f, 1.0f)), a0, a1);   // 1 + e
+    r = fma2(pk2(lg2_approx(a0), lg2_approx(a1)), pk2(0.69314718055994531f, 0.69314718055994531f), mx);
+  }
+  up2(r, h0, h1);
+}
+
+// ---- accurate tanh of a pair (kActTanhPair; SPLIT and TF32): u = z 2 log2(e) (the scale is folded into
+// the accumulator scale), tanh|z| = 2 r - 1 with r = 1 / (1 + e), e = 2^-|u| in (0, 1]: absolute error
+// ~1.2e-7 (the same form as the MUFU ex2 + rcp epilogue).  NEWTON: r by a quadratic seed on [1, 2]
+// (1.7%) and two Newton steps (8e-8) in FFMA2 (8 FFMA2 per pair, 1 MUFU per unit); otherwise MUFU rcp.
+template <bool NEWTON>
+__device__ __forceinline__ void tanh_pair(float u0, float u1, float& h0, float& h1) {
+  const uint64_t E = pk2(ex2_approx(-fabsf(u0)), ex2_approx(-fabsf(u1)));
+  uint64_t R;
+  if constexpr (NEWTON) {
+    const uint64_t NS = fma2(E, pk2(-1.0f, -1.0f), pk2(-1.0f, -1.0f));        // -(1 + e)
+    R = fma2(fma2s(NS, 0.30153724f, 1.39582404f), NS, pk2(2.08733358f, 2.08733358f));
+    R = fma2(R, fma2(NS, R, pk2(1.0f, 1.0f)), R);
+    R = fma2(R, fma2(NS, R, pk2(1.0f, 1.0f)), R);
+  } else {
+    float s0, s1;
+    up2(fma2(E, pk2(1.0f, 1.0f), pk2(1.0f, 1.0f)), s0, s1);
+    R = pk2(rcp_approx(s0), rcp_approx(s1));
+  }
+  float t0, t1;
+  up2(fma2(R, pk2(2.0f, 2.0f), pk2(-1.0f, -1.0f)), t0, t1);
+  h0 = copysignf(t0, u0);
+  h1 = copysignf(t1, u1);
+}
+
+// ------------------------------------------------------------------------------------------------
 // a7.  Fused statistics of the terminal values.
 // ------------------------------------------------------------------------------------------------
 struct StatAcc {

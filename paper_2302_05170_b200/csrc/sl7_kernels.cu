@@ -408,6 +408,128 @@ __global__ void __launch_bounds__(128) ann_f32_step_kernel(const __grid_constant
   if (p.has_stats) stat_flush(acc, p, hist, red);
 }
 
+// Packed form of the ANN-FP32 kernel: two paths per thread held as fp32 pairs, every weight (a scalar from
+// the shared-memory float4 broadcast) feeds ONE FFMA2 (fma.rn.f32x2 with the weight broadcast to both
+// halves) for the two paths -- the FFMA work is unchanged, the instruction count of the contractions
+// halves (the r01 kernel was issue-bound at ~8000 instructions per path-step, 5350 of them FFMA).
+// Activations of the two paths in pairs on MUFU (ex2 + rcp / ex2 + lg2: the FMA pipe is the bound here).
+template <int ACT>
+__device__ __forceinline__ uint64_t act_f32_pair(uint64_t U) {
+  float u0, u1, h0, h1;
+  up2(U, u0, u1);
+  if constexpr (ACT == SL7_ACT_TANH) {
+    // tanh z = (1 - e) / (1 + e) with e = 2^-2|z|log2(e): the pair form of act_tanh (argument scaled here)
+    tanh_pair<false>(u0 * 2.8853900817779268f, u1 * 2.8853900817779268f, h0, h1);
+  } else {
+    softplus_pair<false>(u0, u1, h0, h1);
+  }
+  return pk2(h0, h1);
+}
+
+template <int H, int HS, int MR, int ACT, int MINB = 1>
+__global__ void __launch_bounds__(128, MINB) ann_f32x2_step_kernel(const __grid_constant__ RunParams p) {
+  extern __shared__ float4 smem4[];
+  float* sw = reinterpret_cast<float*>(smem4);
+  __shared__ double red[8];
+  const int L = p.n_hidden;
+  const size_t nw = f32_weight_floats(H, HS, L, MR);
+  uint64_t* gs = reinterpret_cast<uint64_t*>(sw + ((nw + 3) & ~size_t(3)));   // [H][blockDim] pair scratch
+  uint32_t* hist = reinterpret_cast<uint32_t*>(gs + (size_t)H * blockDim.x);
+  for (size_t k = threadIdx.x; k < nw; k += blockDim.x) sw[k] = p.wdev[k];
+  hist_init(p, hist);
+  __syncthreads();
+  const float* wout = sw + (size_t)(L - 1) * f32_layer_floats(H, HS);
+  const float* bout = wout + MR * HS;
+  StatAcc acc;
+  const uint64_t tile = 2ull * blockDim.x;
+  const uint64_t stride = (uint64_t)gridDim.x * tile;
+  for (uint64_t base = (uint64_t)blockIdx.x * tile; base < p.n_paths; base += stride) {
+    uint64_t q[2], gp[2];
+    bool ok[2];
+    float z[2][4];
+    RefState rs[2];
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp) {
+      q[pp] = base + (uint64_t)pp * blockDim.x + threadIdx.x;
+      ok[pp] = q[pp] < p.n_paths;
+      gp[pp] = p.path_offset + (ok[pp] ? q[pp] : 0);
+      if (ok[pp] && p.out_mode == kFull) p.out[q[pp]] = p.y0;
+      ref_init(rs[pp], p);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) z[pp][r] = 0.f;
+    }
+    uint64_t Y = pk2(p.y0, p.y0);
+    for (int i = 0; i < p.n_steps; ++i) {
+      float Z[2];
+#pragma unroll
+      for (int pp = 0; pp < 2; ++pp) {
+        if ((i & 3) == 0) normals4(p.key0, p.key1, gp[pp], (uint32_t)(i >> 2), z[pp][0], z[pp][1], z[pp][2], z[pp][3]);
+        Z[pp] = z[pp][0];
+        z[pp][0] = z[pp][1]; z[pp][1] = z[pp][2]; z[pp][2] = z[pp][3];
+      }
+      uint64_t h[H];
+#pragma unroll
+      for (int k = 0; k < H; ++k) h[k] = act_f32_pair<ACT>(fma2(Y, pk2(p.l1w[k], p.l1w[k]), pk2(p.l1b[k], p.l1b[k])));
+      for (int l = 0; l < L - 1; ++l) {
+        const float* W = sw + (size_t)l * f32_layer_floats(H, HS);
+        const float* b = W + H * HS;
+#pragma unroll 2
+        for (int j = 0; j < H; ++j) {
+          const float4* row = reinterpret_cast<const float4*>(W + j * HS);
+          uint64_t a0 = pk2(b[j], b[j]), a1 = pk2(0.f, 0.f);
+#pragma unroll
+          for (int kk = 0; kk < HS / 4; ++kk) {
+            const float4 wv = row[kk];
+            if (4 * kk + 0 < H) a0 = fma2(h[4 * kk + 0], pk2(wv.x, wv.x), a0);
+            if (4 * kk + 1 < H) a1 = fma2(h[4 * kk + 1], pk2(wv.y, wv.y), a1);
+            if (4 * kk + 2 < H) a0 = fma2(h[4 * kk + 2], pk2(wv.z, wv.z), a0);
+            if (4 * kk + 3 < H) a1 = fma2(h[4 * kk + 3], pk2(wv.w, wv.w), a1);
+          }
+          gs[(size_t)j * blockDim.x + threadIdx.x] = act_f32_pair<ACT>(fma2(a0, pk2(1.f, 1.f), a1));
+        }
+#pragma unroll
+        for (int k = 0; k < H; ++k) h[k] = gs[(size_t)k * blockDim.x + threadIdx.x];
+      }
+      float y[2][MR];
+#pragma unroll
+      for (int j = 0; j < MR; ++j) {
+        const float4* row = reinterpret_cast<const float4*>(wout + j * HS);
+        uint64_t a0 = pk2(bout[j], bout[j]), a1 = pk2(0.f, 0.f);
+#pragma unroll
+        for (int kk = 0; kk < HS / 4; ++kk) {
+          const float4 wv = row[kk];
+          if (4 * kk + 0 < H) a0 = fma2(h[4 * kk + 0], pk2(wv.x, wv.x), a0);
+          if (4 * kk + 1 < H) a1 = fma2(h[4 * kk + 1], pk2(wv.y, wv.y), a1);
+          if (4 * kk + 2 < H) a0 = fma2(h[4 * kk + 2], pk2(wv.z, wv.z), a0);
+          if (4 * kk + 3 < H) a1 = fma2(h[4 * kk + 3], pk2(wv.w, wv.w), a1);
+        }
+        float s0, s1, y0, y1;
+        up2(fma2(a0, pk2(1.f, 1.f), a1), s0, s1);
+        up2(Y, y0, y1);
+        y[0][j] = fmaf(p.res_y, y0, fmaf(s0, p.out_scale[j], p.out_shift[j]));
+        y[1][j] = fmaf(p.res_y, y1, fmaf(s1, p.out_scale[j], p.out_shift[j]));
+      }
+      float yn[2];
+#pragma unroll
+      for (int pp = 0; pp < 2; ++pp) {
+        yn[pp] = gm_eval<MR, false>(p, Z[pp], y[pp]);
+        ref_step(rs[pp], p, Z[pp]);
+        if (ok[pp] && p.out_mode == kFull) p.out[(uint64_t)(i + 1) * p.n_paths + q[pp]] = yn[pp];
+      }
+      Y = pk2(yn[0], yn[1]);
+    }
+    float yT[2];
+    up2(Y, yT[0], yT[1]);
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp) {
+      if (!ok[pp]) continue;
+      if (p.out_mode == kTerminal) p.out[q[pp]] = yT[pp];
+      if (p.has_stats) stat_add(acc, p, yT[pp], ref_final(rs[pp], p), hist);
+    }
+  }
+  if (p.has_stats) stat_flush(acc, p, hist, red);
+}
+
 // ------------------------------------------------------------------------------------------------
 // RNG verification kernels (same device functions as the step kernels).
 // ------------------------------------------------------------------------------------------------
@@ -536,8 +658,31 @@ cudaError_t launch_ann_f32_t(const RunParams& p, cudaStream_t st, int num_sms) {
   return launch_persistent(ann_f32_step_kernel<H, HS, MR, RT, ACT, PP>, 128, smem, p, st, num_sms, 128 * PP);
 }
 
+template <int H, int HS, int MR, int ACT, int MINB = 1>
+cudaError_t launch_ann_f32x2_t(const RunParams& p, cudaStream_t st, int num_sms) {
+  const size_t nw = f32_weight_floats(H, HS, p.n_hidden, MR);
+  const size_t smem = (((nw + 3) & ~size_t(3)) + (size_t)H * 2 * 128) * sizeof(float) + hist_bytes(p);
+  return launch_persistent(ann_f32x2_step_kernel<H, HS, MR, ACT, MINB>, 128, smem, p, st, num_sms, 256);
+}
+
 template <int ACT>
 cudaError_t launch_ann_f32(const RunParams& p, cudaStream_t st, int num_sms) {
+  int variant = 0;
+#ifdef SL7_AB_HOOKS
+  if (const char* v = std::getenv("SL7_TC_VARIANT")) variant = std::atoi(v);   // 60: the r01 FFMA kernel
+#endif
+  if (variant == 61) {
+    if (p.width == 50 && p.m == 5) return launch_ann_f32x2_t<50, 52, 5, ACT, 3>(p, st, num_sms);
+    if (p.width == 50 && p.m == 7) return launch_ann_f32x2_t<50, 52, 7, ACT, 3>(p, st, num_sms);
+  }
+  if (variant == 62) {
+    if (p.width == 50 && p.m == 5) return launch_ann_f32x2_t<50, 52, 5, ACT, 4>(p, st, num_sms);
+    if (p.width == 50 && p.m == 7) return launch_ann_f32x2_t<50, 52, 7, ACT, 4>(p, st, num_sms);
+  }
+  if (variant != 60) {
+    if (p.width == 50 && p.m == 5) return launch_ann_f32x2_t<50, 52, 5, ACT>(p, st, num_sms);
+    if (p.width == 50 && p.m == 7) return launch_ann_f32x2_t<50, 52, 7, ACT>(p, st, num_sms);
+  }
   if (p.width == 50 && p.m == 5) return launch_ann_f32_t<50, 52, 5, false, ACT, 2>(p, st, num_sms);
   if (p.width == 50 && p.m == 7) return launch_ann_f32_t<50, 52, 7, false, ACT, 2>(p, st, num_sms);
   if (p.width == 64) return launch_ann_f32_t<64, 64, kMaxM, true, ACT, 1>(p, st, num_sms);
