@@ -8,9 +8,9 @@
 //
 // F is evaluated in float64 as its Poisson mixture F(x) = sum_k w_k P(d/2 + k, x/2),
 // w_k = e^{-mu} mu^k / k!, mu = lam/2, P the regularised lower incomplete gamma: P is computed once at
-// the Poisson mode (series for y < a + 1, Lentz continued fraction otherwise) and carried to the other
-// k by the exact recurrences P(a+1, y) = P(a, y) - G(a), G(a) = y^a e^{-y} / Gamma(a+1) (forward) and
-// P(a, y) = P(a+1, y) + G(a) (backward), the weights by w_{k+1} = w_k mu / (k+1); the density comes
+// the Poisson mode (series for y < a + 1, otherwise Legendre's continued fraction for Q by the Wallis
+// recurrences of its convergents) and carried to the other k by the exact recurrences
+// P(a+1, y) = P(a, y) - G(a), G(a) = y^a e^{-y} / Gamma(a+1) (forward) and P(a, y) = P(a+1, y) + G(a) (backward), the weights by w_{k+1} = w_k mu / (k+1); the density comes
 // from the same terms.  The quantile is a bracketed Newton iteration from the Patnaik (scaled central
 // chi-square) + Wilson-Hilferty starting point, which takes the normal quantile x_j directly.
 // The work is float64 special-function evaluation (~4 Newton steps x ~2 (sqrt(mu) + ...) terms x m nodes
@@ -49,20 +49,25 @@ __device__ double gamma_p(double a, double y, double lg_a1) {
     }
     return exp(lpre) * sum;
   }
-  // Q(a, y) = e^{-y} y^a / Gamma(a) * CF  (modified Lentz)
-  const double tiny = 1e-300;
-  double b = y + 1.0 - a, cc = 1.0 / tiny, dd = 1.0 / b, h = dd;
-  for (int i = 1; i < 2000; ++i) {
-    const double an = -i * (i - a);
-    b += 2.0;
-    dd = fma(an, dd, b);
-    if (fabs(dd) < tiny) dd = tiny;
-    cc = b + an / cc;
-    if (fabs(cc) < tiny) cc = tiny;
-    dd = 1.0 / dd;
-    const double del = dd * cc;
-    h *= del;
-    if (fabs(del - 1.0) < 1e-16) break;
+  // Q(a, y) = e^{-y} y^a / Gamma(a) / K with Legendre's continued fraction
+  //   K = b_0 + a_1/(b_1 + a_2/(b_2 + ...)),  b_n = y + 2n + 1 - a,  a_n = -n (n - a),
+  // evaluated by the fundamental (Wallis) recurrences of its convergents P_n / R_n:
+  //   P_n = b_n P_{n-1} + a_n P_{n-2},  R_n = b_n R_{n-1} + a_n R_{n-2}  (P_{-1} = 1, R_{-1} = 0, R_0 = 1),
+  // rescaled whenever the numerators grow large; 1/K = R_n / P_n.
+  double pm = 1.0, p0 = y + 1.0 - a, rm = 0.0, r0 = 1.0;
+  double h = r0 / p0;
+  for (int n = 1; n < 2000; ++n) {
+    const double an = -(double)n * ((double)n - a), bn = y + 2.0 * n + 1.0 - a;
+    const double p1 = fma(bn, p0, an * pm), r1 = fma(bn, r0, an * rm);
+    pm = p0; p0 = p1; rm = r0; r0 = r1;
+    if (fabs(p0) > 1e150) {
+      const double sc = 1.0 / fabs(p0);
+      pm *= sc; p0 *= sc; rm *= sc; r0 *= sc;
+    }
+    const double hn = r0 / p0;
+    const bool done = fabs(hn - h) <= 1e-16 * fabs(hn);
+    h = hn;
+    if (done) break;
   }
   return 1.0 - exp(lpre + log(a)) * h;
 }

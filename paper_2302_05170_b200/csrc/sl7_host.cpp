@@ -117,51 +117,27 @@ struct DeviceGuard {
   }
 };
 
-// ---- Golub-Welsch: eigenvalues of symmetric tridiagonal (d, e) by implicit QL with shifts ----
-void tridiag_ql_eigenvalues(std::vector<double>& d, std::vector<double> e) {
-  const int n = (int)d.size();
-  // e[i] couples d[i] and d[i+1]; e[n-1] = 0
-  e.push_back(0.0);
-  for (int l = 0; l < n; ++l) {
-    for (int iter = 0; iter < 200; ++iter) {
-      int mm;
-      for (mm = l; mm < n - 1; ++mm) {
-        const double dd = std::fabs(d[mm]) + std::fabs(d[mm + 1]);
-        if (std::fabs(e[mm]) <= 1e-17 * dd) break;
-      }
-      if (mm == l) break;
-      double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
-      double r = std::hypot(g, 1.0);
-      g = d[mm] - d[l] + e[l] / (g + (g >= 0 ? std::fabs(r) : -std::fabs(r)));
-      double s = 1.0, c = 1.0, p = 0.0;
-      int i;
-      for (i = mm - 1; i >= l; --i) {
-        double f = s * e[i];
-        const double bb = c * e[i];
-        r = std::hypot(f, g);
-        e[i + 1] = r;
-        if (r == 0.0) {
-          d[i + 1] -= p;
-          e[mm] = 0.0;
-          break;
-        }
-        s = f / r;
-        c = g / r;
-        g = d[i + 1] - p;
-        r = (d[i] - g) * s + 2.0 * c * bb;
-        p = s * r;
-        d[i + 1] = g + p;
-        g = c * r - bb;
-      }
-      if (r == 0.0 && i >= l) continue;
-      d[l] -= p;
-      e[l] = g;
-      e[mm] = 0.0;
-    }
+// ---- Gauss-Hermite nodes (the x_j are the roots of the probabilists' He_m) ----
+// The three-term recurrence He_0 = 1, He_1 = x, He_{k+1} = x He_k - k He_{k-1} is the sequence of leading
+// principal minors det(x I - J_k) of the Jacobi matrix J (zero diagonal, off-diagonal sqrt(k)), hence a
+// Sturm sequence: the number of sign changes of He_0(x), ..., He_m(x) is the number of roots below x.  Each
+// root is isolated by bisection on that count (the ratios q_k = He_k / He_{k-1} keep it overflow-free) and
+// then polished by Newton on He_m with He_m' = m He_{m-1}.  All roots lie in |x| < sqrt(4m + 2).
+
+// number of roots of He_m below x: m minus the sign changes of the Sturm sequence (counted on its ratios)
+int hermite_roots_below(int m, double x) {
+  int changes = 0;
+  double q = x;                       // He_1 / He_0
+  for (int k = 1;; ++k) {
+    if (q == 0.0) q = -1e-300;        // a zero minor: the sign the sequence has just right of x
+    if (q < 0.0) ++changes;
+    if (k == m) break;
+    q = x - (double)k / q;            // He_{k+1} / He_k
   }
+  return m - changes;
 }
 
-// He_m(x) and He_{m-1}(x) by the recurrence He_{k+1} = x He_k - k He_{k-1}.
+// He_m(x) and He_{m-1}(x) by the recurrence
 void hermite_pair(int m, double x, double& hm, double& hm1) {
   double a = 1.0, b = x;  // He_0, He_1
   if (m == 0) { hm = 1.0; hm1 = 0.0; return; }
@@ -175,21 +151,25 @@ void hermite_pair(int m, double x, double& hm, double& hm1) {
 }
 
 void gh_grid(int m, double* x, double* w) {
-  std::vector<double> d(m, 0.0), e;
-  for (int k = 1; k < m; ++k) e.push_back(std::sqrt((double)k));
-  tridiag_ql_eigenvalues(d, e);
-  std::sort(d.begin(), d.end());
+  std::vector<double> r(m);
+  const double bound = std::sqrt(4.0 * m + 2.0);
   for (int j = 0; j < m; ++j) {
-    double xj = d[j];
-    for (int it = 0; it < 3; ++it) {  // Newton polish: He_m' = m He_{m-1}
+    // the (j+1)-th smallest root lies in [lo, hi): roots_below(lo) <= j < roots_below(hi)
+    double lo = -bound, hi = bound;
+    for (int it = 0; it < 200 && hi - lo > 1e-15 * (1.0 + std::fabs(lo)); ++it) {
+      const double mid = 0.5 * (lo + hi);
+      if (hermite_roots_below(m, mid) > j) hi = mid; else lo = mid;
+    }
+    double xj = 0.5 * (lo + hi);
+    for (int it = 0; it < 3; ++it) {  // Newton polish
       double hm, hm1;
       hermite_pair(m, xj, hm, hm1);
       if (hm1 == 0.0) break;
       xj -= hm / (m * hm1);
     }
-    d[j] = xj;
+    r[j] = xj;
   }
-  for (int j = 0; j < m; ++j) x[j] = 0.5 * (d[j] - d[m - 1 - j]);  // exact symmetry
+  for (int j = 0; j < m; ++j) x[j] = 0.5 * (r[j] - r[m - 1 - j]);  // exact symmetry
   for (int j = 0; j < m; ++j) {
     double p = 1.0;
     for (int k = 0; k < m; ++k)
