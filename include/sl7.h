@@ -112,7 +112,9 @@ typedef enum { SL7_REF_NONE = 0, SL7_REF_GBM = 1, SL7_REF_OU = 2 } sl7_ref;
  * z_k(t_i) = H(Y0, t_i = i dt, theta)_k ("only requires the ANNs to compute a small number of marginal
  * collocation points"; reading R-26 of DESIGN.md); t_0 has every path at Y0 (nearest row).
  * The table is then the same for every path set, so there are no selection passes and no exchange:
- * shard it like SL7_SCHEME_7L with path_offset.  The network must be fitted for horizons up to T. */
+ * shard it like SL7_SCHEME_7L with path_offset.  The network must be fitted for horizons up to T: with a
+ * blob that carries its fitted domain (flags bit 2), a call whose horizons dt..(n_steps-1) dt or whose Y0
+ * leave that box fails with SL7_EINVAL instead of extrapolating. */
 typedef enum { SL7_SCHEME_7L = 0, SL7_SCHEME_CDC = 1, SL7_SCHEME_CDC_PRED = 2 } sl7_scheme;
 
 typedef struct {
@@ -161,7 +163,8 @@ typedef struct {
  *               d_in = 2 + n_theta (input order (Y, dt, theta...)), 1 <= L <= SL7_MAX_HIDDEN,
  *               h_l <= SL7_MAX_WIDTH, last entry == m.
  * act         : hidden activation.
- * Host setup done here (once): Gauss-Hermite nodes (own Golub-Welsch QL in double), barycentric
+ * Host setup done here (once): Gauss-Hermite nodes (Sturm-sequence bisection on the He_k recurrence +
+ * Newton, in double), barycentric
  * weights, fp32 hi/lo node split.  Errors: SL7_EINVAL (m, layer_dims), SL7_ECUDA (device). */
 sl7_status sl7_create(int32_t m, const int32_t* layer_dims, int32_t n_dims, sl7_act act,
                       int32_t device, sl7_ctx* out);
@@ -169,8 +172,10 @@ sl7_status sl7_create(int32_t m, const int32_t* layer_dims, int32_t n_dims, sl7_
 /* Load the trained network (Algorithm I step 1 output) from a blob; copied, so the
  * caller may free it on return.  Little-endian "SL7W" container:
  *   char magic[4] = "SL7W"; u32 version = 1; u32 n_dims; u32 dims[n_dims]; u32 act; u32 flags
- *   (bit0 has_norm, bit1 residual; other bits rejected); then per layer l: f32 W[out][in] (row-major),
- *   f32 b[out]; if has_norm: f32 in_shift[d_in], in_scale[d_in], out_shift[m], out_scale[m]
+ *   (bit0 has_norm, bit1 residual, bit2 has_domain; other bits rejected); then per layer l:
+ *   f32 W[out][in] (row-major), f32 b[out]; if has_norm: f32 in_shift[d_in], in_scale[d_in],
+ *   out_shift[m], out_scale[m]; if has_domain: f32 dom_lo[d_in], dom_hi[d_in], the box of raw features
+ *   (Y, dt, theta...) the network was fitted on
  *   (network sees (f - in_shift)/in_scale; prediction is out * out_scale + out_shift, or out without
  *   has_norm).  residual (reading R-11 in DESIGN.md): y_j = Y + sqrt(dt) * prediction_j, so the
  *   network carries only the step's spread and bf16 / tf32 rounding no longer scales with |Y|.

@@ -41,26 +41,41 @@ def _sample(rng, n, ranges, log_cols=()):
     return np.stack(cols, axis=1)
 
 
+# Raw-feature box each network is fitted on, (lo, hi) per column, and the columns sampled log-uniformly.
+# The box is stored in the blob (flags bit 2) so that the library can refuse to read the predictor outside
+# it (CDC_PRED horizons, include/sl7.h).  CIR: dt up to 4 = configs[4]'s T, so that the 7L-CDC predictor
+# (reading R-26) can be read at every horizon t_i < T of configs 2 and 4.
+RANGES = {
+    "gbm": ([(0.2, 5.0), (1 / 64, 1.0)], (0, 1)),
+    # SPEC.md:180 default OU training ranges; features (Y, dt, Ybar, lam, sigma)
+    "ou": ([(-2, 2), (0.05, 2.0), (-1, 1), (0.1, 2.0), (0.1, 1.0)], ()),
+    # features (Y, dt, kappa, Ybar, sigma)
+    "cir": ([(0.002, 0.5), (0.05, 4.0), (0.5, 2.0), (0.05, 0.2), (0.15, 0.45)], (0, 1)),
+}
+
+
 def make_dataset(kind, m, n, seed):
     rng = np.random.default_rng(seed)
     x = O.gauss_hermite_nodes(m)
+    ranges, log_cols = RANGES[kind]
+    F = _sample(rng, n, ranges, log_cols=log_cols)
     if kind == "gbm":
         mu, sigma = 0.05, 0.2
-        F = _sample(rng, n, [(0.2, 5.0), (1 / 64, 1.0)], log_cols=(0, 1))
         Yl = np.stack([O.gbm_collocation(F[i:i + 1, 0], F[i, 1], mu, sigma, x)[0] for i in range(n)], 0)
         return F, Yl
     if kind == "ou":
-        # SPEC.md:180 default OU training ranges; features (Y, dt, Ybar, lam, sigma)
-        F = _sample(rng, n, [(-2, 2), (0.05, 2.0), (-1, 1), (0.1, 2.0), (0.1, 1.0)])
         Yl = np.stack([O.ou_collocation(F[i:i + 1, 0], F[i, 1], F[i, 2], F[i, 3], F[i, 4], x)[0]
                        for i in range(n)], 0)
         return F, Yl
     if kind == "cir":
-        # features (Y, dt, kappa, Ybar, sigma)
-        F = _sample(rng, n, [(0.002, 0.5), (0.05, 0.5), (0.5, 2.0), (0.05, 0.2), (0.15, 0.45)], log_cols=(0,))
         Yl = O.cir_collocation(F[:, 0], F[:, 1], F[:, 2], F[:, 3], F[:, 4], x)
         return F, Yl
     raise ValueError(kind)
+
+
+def domain_of(kind):
+    ranges, _ = RANGES[kind]
+    return (np.array([lo for lo, _ in ranges], dtype=np.float64), np.array([hi for _, hi in ranges], dtype=np.float64))
 
 
 def fit(kind, m, act, hidden, seconds, seed=WEIGHT_SEED, n=200_000, device="cpu", residual=True):
@@ -116,7 +131,7 @@ def fit(kind, m, act, hidden, seconds, seed=WEIGHT_SEED, n=200_000, device="cpu"
     b = [l.bias.detach().double().cpu().numpy().astype(np.float32).astype(np.float64) for l in lins]
     f32 = lambda a: np.asarray(a).astype(np.float32).astype(np.float64)
     p = MlpParams(tuple(dims), act, W, b, f32(in_shift), f32(in_scale), f32(out_shift), f32(out_scale),
-                  residual=residual)
+                  residual=residual, domain=domain_of(kind))
     # report fit quality with the oracle's own forward pass on the held-out rows
     blob = pack_blob(p)
     onet = O.parse_blob(blob)
@@ -143,13 +158,29 @@ def main():
     ap.add_argument("--device", default="cpu", help="torch device for the optimiser (labels are the oracle's)")
     ap.add_argument("--absolute", action="store_true", help="absolute-output blobs (no residual form)")
     ap.add_argument("--out-dir", default=GOLDEN)
+    ap.add_argument("--stamp-domain", action="store_true",
+                    help="re-pack the existing blobs with their recipe's feature box (flags bit 2), weights unchanged")
     a = ap.parse_args()
     man_path = os.path.join(a.out_dir, "weights_manifest.json")
     manifest = json.load(open(man_path)) if os.path.exists(man_path) else {}
     for name, (kind, m, act, hidden) in NETS.items():
         if a.only and a.only != name:
             continue
-        n = 60_000 if kind == "cir" else 200_000
+        if a.stamp_domain:
+            path = os.path.join(a.out_dir, name)
+            net = O.parse_blob(open(path, "rb").read())
+            p = MlpParams(net.dims, net.act, net.W, net.b, *net.norm, residual=net.residual, domain=domain_of(kind))
+            blob = pack_blob(p)
+            assert O.parse_blob(blob).W[0].tobytes() == net.W[0].tobytes()
+            open(path, "wb").write(blob)
+            e = manifest[name]
+            e["sha256"] = hashlib.sha256(blob).hexdigest()
+            e["domain"] = [list(map(float, d)) for d in domain_of(kind)]
+            e["script"] += " ; python -m oracle.fit_weights --stamp-domain --only %s" % name
+            print(name, "stamped", e["domain"], flush=True)
+            json.dump(manifest, open(man_path, "w"), indent=1, sort_keys=True)
+            continue
+        n = 120_000 if kind == "cir" else 200_000
         blob, q = fit(kind, m, act, hidden, a.seconds, n=n, device=a.device, residual=not a.absolute)
         with open(os.path.join(a.out_dir, name), "wb") as f:
             f.write(blob)
@@ -157,6 +188,7 @@ def main():
                           "hidden": hidden, "sha256": hashlib.sha256(blob).hexdigest(),
                           "fit_seconds": a.seconds, "seed": WEIGHT_SEED, "quality": q, "device": a.device,
                           "residual": not a.absolute,
+                          "domain": [list(map(float, d)) for d in domain_of(kind)],
                           "script": "python -m oracle.fit_weights --seconds %g --device %s%s" % (
                               a.seconds, a.device, " --absolute" if a.absolute else "")}
         print(name, q, flush=True)

@@ -284,6 +284,10 @@ def parse_blob(blob: bytes) -> Mlp:
             arrs.append(np.frombuffer(blob, dtype="<f4", count=n, offset=off).astype(np.float64))
             off += 4 * n
         norm = tuple(arrs)
+    if flags & 4:   # fitted feature box (lo[d_in], hi[d_in]): metadata, not used by the arithmetic
+        off += 8 * dims[0]
+    if flags & ~7:
+        raise ValueError("flags")
     if off != len(blob):
         raise ValueError("size")
     return Mlp(dims, act, W, b, norm, residual=bool(flags & 2))

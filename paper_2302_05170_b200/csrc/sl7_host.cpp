@@ -42,6 +42,7 @@ struct sl7_ctx_s {
   bool has_norm = false;
   bool residual = false;          // blob flags bit 1: H_j = Y + sqrt(dt) (out_j out_scale_j + out_shift_j)
   std::vector<float> in_shift, in_scale, out_shift, out_scale;
+  std::vector<float> dom_lo, dom_hi;   // blob flags bit 2: the feature box the network was fitted on
   // device images
   int width = 0;           // hidden width used by the FP32 kernel (50 or 64 padded)
   float* d_wf32 = nullptr;
@@ -846,9 +847,9 @@ sl7_status sl7_load_weights(sl7_ctx c, const void* blob, size_t nbytes) {
     std::memcpy(b.back().data(), p + off, 4 * fo);
     off += 4 * fo;
   }
-  if (flags & ~3u) return fail(c, SL7_EFORMAT, "flags (bit0 has_norm, bit1 residual)");
+  if (flags & ~7u) return fail(c, SL7_EFORMAT, "flags (bit0 has_norm, bit1 residual, bit2 has_domain)");
   const bool has_norm = flags & 1u;
-  std::vector<float> ish, isc, osh, osc;
+  std::vector<float> ish, isc, osh, osc, dlo, dhi;
   if (has_norm) {
     const size_t d_in = c->dims[0], m = c->m;
     if (!need(4 * (2 * d_in + 2 * m))) return fail(c, SL7_EFORMAT, "size (normalisation)");
@@ -864,6 +865,17 @@ sl7_status sl7_load_weights(sl7_ctx c, const void* blob, size_t nbytes) {
     for (float s : isc)
       if (!(s != 0.0f) || !std::isfinite(s)) return fail(c, SL7_EFORMAT, "in_scale");
   }
+  if (flags & 4u) {
+    const size_t d_in = c->dims[0];
+    if (!need(8 * d_in)) return fail(c, SL7_EFORMAT, "size (domain)");
+    dlo.resize(d_in);
+    dhi.resize(d_in);
+    std::memcpy(dlo.data(), p + off, 4 * d_in);
+    std::memcpy(dhi.data(), p + off + 4 * d_in, 4 * d_in);
+    off += 8 * d_in;
+    for (size_t k = 0; k < d_in; ++k)
+      if (!(dlo[k] <= dhi[k])) return fail(c, SL7_EFORMAT, "domain[%zu]: lo > hi or not a number", k);
+  }
   if (off != nbytes) return fail(c, SL7_EFORMAT, "size (%zu bytes, expected %zu)", nbytes, off);
   for (auto& v : W)
     for (float x : v)
@@ -876,6 +888,8 @@ sl7_status sl7_load_weights(sl7_ctx c, const void* blob, size_t nbytes) {
   c->in_scale = isc;
   c->out_shift = osh;
   c->out_scale = osc;
+  c->dom_lo = dlo;
+  c->dom_hi = dhi;
   DeviceGuard g(c->device);
   if (!g.ok) return fail(c, SL7_ECUDA, "cudaSetDevice(%d)", c->device);
   sl7_status s = build_f32_image(c);
@@ -894,6 +908,16 @@ static sl7_status prepare_cdc_horizons(sl7_ctx c, double Y0, double dt, int32_t 
                                 int32_t n_theta, uint64_t n_paths, uint64_t seed, sl7_out out_mode,
                                 const sl7_run_opts* opts, bool has_out, bool has_stats) {
   if (opts->scheme != SL7_SCHEME_CDC_PRED) return SL7_OK;
+  if (opts->colloc == SL7_COLLOC_ANN && !c->dom_hi.empty()) {
+    // the predictor is read at (Y0, t_i) for t_i up to (n_steps - 1) dt: outside the fitted box it extrapolates
+    const double t_max = dt * (double)(n_steps - 1), tol = 1e-6;
+    if (n_steps > 1 && (t_max > (double)c->dom_hi[1] * (1.0 + tol) || dt < (double)c->dom_lo[1] * (1.0 - tol)))
+      return fail(c, SL7_EINVAL, "CDC_PRED horizons [%g, %g] leave the network's fitted dt range [%g, %g]", dt, t_max,
+                  (double)c->dom_lo[1], (double)c->dom_hi[1]);
+    if (Y0 < (double)c->dom_lo[0] || Y0 > (double)c->dom_hi[0])
+      return fail(c, SL7_EINVAL, "CDC_PRED: Y0 = %g outside the network's fitted range [%g, %g]", Y0,
+                  (double)c->dom_lo[0], (double)c->dom_hi[0]);
+  }
   c->cdc_hz.assign((size_t)n_steps, CdcHorizon{});
   for (int32_t i = 1; i < n_steps; ++i) {
     RunParams q;

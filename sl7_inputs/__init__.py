@@ -88,6 +88,7 @@ class MlpParams:
     out_shift: np.ndarray | None = None
     out_scale: np.ndarray | None = None
     residual: bool = False          # blob flags bit 1 (include/sl7.h, 'Weights blob')
+    domain: tuple | None = None     # blob flags bit 2: (lo[d_in], hi[d_in]) of the raw features fitted on
 
     @property
     def has_norm(self) -> bool:
@@ -126,12 +127,16 @@ def pack_blob(p: MlpParams) -> bytes:
     out += BLOB_MAGIC
     out += struct.pack("<II", BLOB_VERSION, len(p.dims))
     out += struct.pack("<%dI" % len(p.dims), *p.dims)
-    out += struct.pack("<II", p.act, (1 if p.has_norm else 0) | (2 if p.residual else 0))
+    out += struct.pack("<II", p.act, (1 if p.has_norm else 0) | (2 if p.residual else 0)
+                       | (4 if p.domain is not None else 0))
     for W, b in zip(p.W, p.b):
         out += np.asarray(W, dtype="<f4").tobytes()
         out += np.asarray(b, dtype="<f4").tobytes()
     if p.has_norm:
         for a in (p.in_shift, p.in_scale, p.out_shift, p.out_scale):
+            out += np.asarray(a, dtype="<f4").tobytes()
+    if p.domain is not None:
+        for a in p.domain:
             out += np.asarray(a, dtype="<f4").tobytes()
     return bytes(out)
 
