@@ -426,7 +426,36 @@ __device__ __forceinline__ uint64_t act_f32_pair(uint64_t U) {
   return pk2(h0, h1);
 }
 
-template <int H, int HS, int MR, int ACT, int MINB = 1>
+// NJ output neurons of one hidden layer at a time for the pair of paths, two accumulator chains each (2 NJ
+// independent FFMA2 chains per thread: the r02 kernel with NJ = 2 stalled on FFMA2 latency at 2 warps per
+// scheduler); the NJ weight rows are read as float4 broadcasts, each weight feeds one FFMA2.
+template <int H, int HS, int NJ>
+__device__ __forceinline__ void f32x2_neurons(const float* W, const float* b, const uint64_t (&h)[H], int j,
+                                              uint64_t (&out)[NJ]) {
+  uint64_t a0[NJ], a1[NJ];
+#pragma unroll
+  for (int u = 0; u < NJ; ++u) {
+    a0[u] = pk2(b[j + u], b[j + u]);
+    a1[u] = pk2(0.f, 0.f);
+  }
+#pragma unroll
+  for (int kk = 0; kk < HS / 4; ++kk) {
+    float4 wv[NJ];
+#pragma unroll
+    for (int u = 0; u < NJ; ++u) wv[u] = reinterpret_cast<const float4*>(W + (j + u) * HS)[kk];
+#pragma unroll
+    for (int u = 0; u < NJ; ++u) {
+      if (4 * kk + 0 < H) a0[u] = fma2(h[4 * kk + 0], pk2(wv[u].x, wv[u].x), a0[u]);
+      if (4 * kk + 1 < H) a1[u] = fma2(h[4 * kk + 1], pk2(wv[u].y, wv[u].y), a1[u]);
+      if (4 * kk + 2 < H) a0[u] = fma2(h[4 * kk + 2], pk2(wv[u].z, wv[u].z), a0[u]);
+      if (4 * kk + 3 < H) a1[u] = fma2(h[4 * kk + 3], pk2(wv[u].w, wv[u].w), a1[u]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < NJ; ++u) out[u] = fma2(a0[u], pk2(1.f, 1.f), a1[u]);
+}
+
+template <int H, int HS, int MR, int ACT, int MINB = 1, int NJ = 0>
 __global__ void __launch_bounds__(128, MINB) ann_f32x2_step_kernel(const __grid_constant__ RunParams p) {
   extern __shared__ float4 smem4[];
   float* sw = reinterpret_cast<float*>(smem4);
@@ -473,6 +502,22 @@ __global__ void __launch_bounds__(128, MINB) ann_f32x2_step_kernel(const __grid_
       for (int l = 0; l < L - 1; ++l) {
         const float* W = sw + (size_t)l * f32_layer_floats(H, HS);
         const float* b = W + H * HS;
+        if constexpr (NJ > 0) {
+          int j = 0;
+#pragma unroll 1
+          for (; j + NJ <= H; j += NJ) {
+            uint64_t a[NJ];
+            f32x2_neurons<H, HS, NJ>(W, b, h, j, a);
+#pragma unroll
+            for (int u = 0; u < NJ; ++u) gs[(size_t)(j + u) * blockDim.x + threadIdx.x] = act_f32_pair<ACT>(a[u]);
+          }
+#pragma unroll 1
+          for (; j < H; ++j) {
+            uint64_t a[1];
+            f32x2_neurons<H, HS, 1>(W, b, h, j, a);
+            gs[(size_t)j * blockDim.x + threadIdx.x] = act_f32_pair<ACT>(a[0]);
+          }
+        } else {
 #pragma unroll 2
         for (int j = 0; j < H; ++j) {
           const float4* row = reinterpret_cast<const float4*>(W + j * HS);
@@ -486,6 +531,7 @@ __global__ void __launch_bounds__(128, MINB) ann_f32x2_step_kernel(const __grid_
             if (4 * kk + 3 < H) a1 = fma2(h[4 * kk + 3], pk2(wv.w, wv.w), a1);
           }
           gs[(size_t)j * blockDim.x + threadIdx.x] = act_f32_pair<ACT>(fma2(a0, pk2(1.f, 1.f), a1));
+        }
         }
 #pragma unroll
         for (int k = 0; k < H; ++k) h[k] = gs[(size_t)k * blockDim.x + threadIdx.x];
@@ -658,11 +704,11 @@ cudaError_t launch_ann_f32_t(const RunParams& p, cudaStream_t st, int num_sms) {
   return launch_persistent(ann_f32_step_kernel<H, HS, MR, RT, ACT, PP>, 128, smem, p, st, num_sms, 128 * PP);
 }
 
-template <int H, int HS, int MR, int ACT, int MINB = 1>
+template <int H, int HS, int MR, int ACT, int MINB = 1, int NJ = 0>
 cudaError_t launch_ann_f32x2_t(const RunParams& p, cudaStream_t st, int num_sms) {
   const size_t nw = f32_weight_floats(H, HS, p.n_hidden, MR);
   const size_t smem = (((nw + 3) & ~size_t(3)) + (size_t)H * 2 * 128) * sizeof(float) + hist_bytes(p);
-  return launch_persistent(ann_f32x2_step_kernel<H, HS, MR, ACT, MINB>, 128, smem, p, st, num_sms, 256);
+  return launch_persistent(ann_f32x2_step_kernel<H, HS, MR, ACT, MINB, NJ>, 128, smem, p, st, num_sms, 256);
 }
 
 template <int ACT>
@@ -674,6 +720,14 @@ cudaError_t launch_ann_f32(const RunParams& p, cudaStream_t st, int num_sms) {
   if (variant == 61) {
     if (p.width == 50 && p.m == 5) return launch_ann_f32x2_t<50, 52, 5, ACT, 3>(p, st, num_sms);
     if (p.width == 50 && p.m == 7) return launch_ann_f32x2_t<50, 52, 7, ACT, 3>(p, st, num_sms);
+  }
+  if (variant >= 63 && variant <= 66) {   // NJ neurons per iteration (2 chains each), MINB
+    if (p.width == 50 && p.m == 7) {
+      if (variant == 63) return launch_ann_f32x2_t<50, 52, 7, ACT, 1, 4>(p, st, num_sms);
+      if (variant == 64) return launch_ann_f32x2_t<50, 52, 7, ACT, 2, 4>(p, st, num_sms);
+      if (variant == 65) return launch_ann_f32x2_t<50, 52, 7, ACT, 1, 3>(p, st, num_sms);
+      return launch_ann_f32x2_t<50, 52, 7, ACT, 1, 2>(p, st, num_sms);
+    }
   }
   if (variant == 62) {
     if (p.width == 50 && p.m == 5) return launch_ann_f32x2_t<50, 52, 5, ACT, 4>(p, st, num_sms);

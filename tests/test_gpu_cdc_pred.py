@@ -106,24 +106,61 @@ def test_cdc_pred_stats_match_full(gpu_lib):
     np.testing.assert_allclose(s[2:6], v[2:6], rtol=1e-12, atol=1e-9)
 
 
-def test_cdc_pred_cir_full_size_moments(gpu_lib):
-    # cfg2's CIR at its full 1e8 paths: finite and near the analytic mean (where the empirical-quantile
-    # CDC diverges, R-25); terminal moments vs the oracle on a 2e5-path prefix within MC noise
+@pytest.mark.parametrize("name", ["cfg2_cir", "cfg4"])
+def test_cdc_pred_cir_terminal_moments_identical_paths(gpu_lib, name):
+    # T-4 on the identical path set: the device's CDC_PRED run of paths 0..2e4-1 against the oracle's
+    # free run of the same paths (fp32 table; O3), terminal mean and variance within 1e-4 relative
     import torch
     sl7 = gpu_lib
-    w = workloads()["cfg2_cir"]
+    w = workloads()[name]
     ctx, code, th, spec = _setup(sl7, "cfg2_cir_ann", 7, "ann", None, None, None, w.n_steps)
+    spec = O.Spec(w.m, "ann", th, w.y0, w.dt, w.n_steps, net=spec.net)
+    n = 20_000
+    o = sl7.make_opts(colloc=code, scheme=sl7.SCHEME_CDC_PRED)
+    out, _ = ctx.simulate(w.y0, w.dt, w.n_steps, th, n, w.seed, sl7.OUT_TERMINAL, o)
+    torch.cuda.synchronize()
+    YT = out.double().cpu().numpy()
+    with np.errstate(all="ignore"):
+        Y, _ = O.simulate_cdc_pred(spec, w.seed, np.arange(n, dtype=np.uint64))
+    Yo = Y[-1]
+    assert np.all(np.isfinite(YT)) and np.all(np.isfinite(Yo))
+    print("%s CDC_PRED: dmean/mean %.2g dvar/var %.2g" % (name, abs(YT.mean() / Yo.mean() - 1),
+                                                          abs(YT.var() / Yo.var() - 1)))
+    assert abs(YT.mean() - Yo.mean()) <= 1e-4 * abs(Yo.mean())
+    assert abs(YT.var() - Yo.var()) <= 1e-4 * Yo.var()
+
+
+@pytest.mark.parametrize("name", ["cfg2_cir", "cfg4"])
+def test_cdc_pred_cir_full_size_law(gpu_lib, name):
+    # cfg2 (1e8 paths, T = 2) and cfg4's shape (1e8 paths, T = 4): every path finite (the empirical-quantile
+    # CDC diverges here, R-25) and the terminal mean within 1% of the CIR law
+    # E Y_T = Y0 e^{-kT} + Ybar (1 - e^{-kT}) -- the network is fitted for horizons up to 4 (R-26)
+    import torch
+    sl7 = gpu_lib
+    w = workloads()[name]
+    ctx, code, th, _ = _setup(sl7, "cfg2_cir_ann", 7, "ann", None, None, None, w.n_steps)
     st = torch.zeros(sl7.stats_elems(4096), dtype=torch.float64, device="cuda")
-    o = sl7.make_opts(colloc=code, scheme=sl7.SCHEME_CDC_PRED, n_bins=4096, hist_lo=0.0, hist_hi=0.6, shift=0.1)
+    o = sl7.make_opts(colloc=code, scheme=sl7.SCHEME_CDC_PRED, n_bins=4096, hist_lo=0.0, hist_hi=0.8, shift=0.1)
     ctx.simulate(w.y0, w.dt, w.n_steps, th, 100_000_000, w.seed, sl7.OUT_STATS, o, stats=st)
     torch.cuda.synchronize()
     v = st.cpu().numpy()
     assert v[0] == 100_000_000 and v[1] == 0                     # count, non-finite count
+    k, yb, _ = w.theta
+    e = np.exp(-k * w.T)
+    law = w.y0 * e + yb * (1 - e)
     mean = 0.1 + v[2] / v[0]
-    with np.errstate(all="ignore"):
-        Y, _ = O.simulate_cdc_pred(spec, w.seed, np.arange(200_000, dtype=np.uint64))
-    sd = Y[-1].std()
-    assert abs(mean - Y[-1].mean()) < 5 * sd / np.sqrt(2e5)
+    print("%s CDC_PRED mean %.6f law %.6f" % (name, mean, law))
+    assert abs(mean / law - 1) < 0.01
+
+
+def test_cdc_pred_refuses_horizons_outside_the_fit(gpu_lib):
+    # the blob's fitted box (flags bit 2): dt 0.5 x 16 steps reads the predictor at t = 7.5 > 4
+    sl7 = gpu_lib
+    w = workloads()["cfg2_cir"]
+    ctx, code, th, _ = _setup(sl7, "cfg2_cir_ann", 7, "ann", None, None, None, w.n_steps)
+    o = sl7.make_opts(colloc=code, scheme=sl7.SCHEME_CDC_PRED)
+    with pytest.raises(sl7.Sl7Error, match="fitted dt range"):
+        ctx.simulate(w.y0, 0.5, 16, th, 1024, w.seed, sl7.OUT_TERMINAL, o)
 
 
 @pytest.mark.parametrize("mode", ["full", "terminal"])

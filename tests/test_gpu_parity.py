@@ -205,7 +205,7 @@ def test_ann_requires_weights_and_supported_precision(gpu_lib):
         ctx.load_weights(load_golden_blob(w.blob)[:-4])
     bad = bytearray(load_golden_blob(w.blob))
     fo = 12 + 4 * len(w.dims) + 4                      # flags word (include/sl7.h 'Weights blob')
-    bad[fo] |= 4                                       # unknown flag bit
+    bad[fo] |= 8                                       # unknown flag bit (bits 0-2 are defined)
     with pytest.raises(sl7.Sl7Error, match="flags"):
         ctx.load_weights(bytes(bad))
 
