@@ -90,6 +90,13 @@ def main():
     Wl = workloads()
 
     def emit(d):
+        # a run with non-finite terminal values (7L-CDC with quantile marginals on CIR diverges, R-25)
+        # has no throughput: its value is withheld and the line says why
+        t = d.get("terminal") or {}
+        nnf = d.get("n_nonfinite", 0)
+        if d.get("value") is not None and (t.get("mean") is None or (nnf or 0) > 0) and "terminal" in d:
+            d = dict(d, value=None, diverged=True, rate_withheld="non-finite terminal values: no valid throughput")
+            d.pop("roofline", None)
         print(json.dumps(d), flush=True)
 
     if a.config in ("cfg3", "all"):
@@ -123,13 +130,13 @@ def main():
         del out
         torch.cuda.empty_cache()
 
-    # issue roofline of the RNG-bound kernels: thread-instructions/s = SMs x 4 schedulers x 32 lanes x clock;
-    # instructions per fine path-step with the fast normals, counted in the SASS of em_rows_kernel's
-    # unrolled OU loop body: 108 per Philox block of 4 fine steps (Philox4x32-10 ~50, two fast
-    # Box-Muller pairs with MUFU lg2/sqrt/sin/cos ~40, four Euler updates 12, loop ~6) = 27.  frac is then
-    # the issue-slot utilisation.
+    # issue roofline of the RNG-bound kernels: thread-instructions/s = SMs x 4 schedulers x 32 lanes x clock,
+    # against an ALGORITHMIC instruction budget per (fine) path-step, not the kernel's own SASS count
+    # (bench.py's budgets): EM = Philox4x32-10 / 4 normals (11) + Box-Muller (9) + the
+    # Euler update (3: drift FFMA, diffusion FFMA, the CIR truncation or the GBM product)
+    from bench import BOX_MULLER_PER_NORMAL, PHILOX_PER_NORMAL, cdc_pred_instr
     issue_peak = n_sms * 4 * 32 * sm_max * 1e6
-    em_instr = 27.0
+    em_instr = float(PHILOX_PER_NORMAL + BOX_MULLER_PER_NORMAL + 3)
 
     if a.config in ("em", "all"):
         from sl7_inputs import CIR_THETA, OU_THETA
@@ -200,6 +207,7 @@ def main():
         ctx = sl7.Context(w.m, list(w.dims), w.act, device=0)
         ctx.load_weights(load_golden_blob(w.blob))
         for label, prec, scheme, n_paths in [("ann_bf16_tcgen05", sl7.PREC_BF16, sl7.SCHEME_7L, N),
+                                             ("cdc_pred_ann_fp32_table", sl7.PREC_FP32, sl7.SCHEME_CDC_PRED, N // 10),
                                              ("cdc_ann_fp32_table", sl7.PREC_FP32, sl7.SCHEME_CDC, N // 10)]:
             opts = sl7.make_opts(prec=prec, colloc=sl7.COLLOC_ANN, stream=stream, n_bins=4096, hist_lo=0.0, hist_hi=0.6,
                                  shift=w.y0, scheme=scheme)
@@ -214,7 +222,7 @@ def main():
             line = {"config": "cfg4", "mode": label, "metric": "7L path-steps/sec (device-timed)", "value": rate,
                     "unit": UNIT, "ms_per_launch": ms, "paths": n_paths, "n_steps": w.n_steps, "m": w.m,
                     "terminal": {k: s[k] for k in ("mean", "var", "skew", "exkurt")}, "n_counted": s["n"],
-                    "quantiles_1_50_99": s["quantiles"], "clocks": clk.summary()}
+                    "n_nonfinite": s["n_nonfinite"], "quantiles_1_50_99": s["quantiles"], "clocks": clk.summary()}
             if prec == sl7.PREC_BF16:
                 trans = sum(w.dims[1:-1])
                 ach = trans * rate / 1e12
@@ -269,12 +277,13 @@ def main():
                         "terminal": {k: s[k] for k in ("mean", "var", "skew", "exkurt", "strong_err")},
                         "quantiles_1_50_99": s["quantiles"], "clocks": clk.summary()}
                 if flags == -3:
-                    # fused CDC_PRED kernel: issue-bound; 254 thread-instructions per path-step measured by ncu
-                    # (smsp__inst_executed x 32 / path-steps, profiles/r01_cdc_pred_fused_ncu.md, libm normals)
-                    ach = rate * 254.0
+                    # fused CDC_PRED kernel: issue-bound; algorithmic budget (bench.cdc_pred_instr): Philox/4 +
+                    # Box-Muller + the table basis at the state + the m x m contraction + g_m at X_hat + clamp
+                    instr = cdc_pred_instr(w.m)
+                    ach = rate * instr
                     line["roofline"] = {"bound": "alu", "pipe": "issue", "achieved": ach / 1e12,
                                         "peak": issue_peak / 1e12, "unit": "T thread-instr/s", "frac": ach / issue_peak,
-                                        "algorithmic": "254 instructions per path-step (ncu count of this kernel on cfg2 OU)"}
+                                        "algorithmic": "%d instructions per path-step (algorithmic budget)" % instr}
                 if colloc == sl7.COLLOC_ANN and prec in (sl7.PREC_BF16, sl7.PREC_TF32):
                     trans = sum(w.dims[1:-1])
                     ach = trans * rate / 1e12

@@ -733,9 +733,15 @@ cudaError_t launch_ann_f32(const RunParams& p, cudaStream_t st, int num_sms) {
     if (p.width == 50 && p.m == 5) return launch_ann_f32x2_t<50, 52, 5, ACT, 4>(p, st, num_sms);
     if (p.width == 50 && p.m == 7) return launch_ann_f32x2_t<50, 52, 7, ACT, 4>(p, st, num_sms);
   }
-  if (variant != 60) {
+  if (variant == 67) {   // the r02 first version: neurons in a rolled loop unrolled by 2 (the compiler's chains)
     if (p.width == 50 && p.m == 5) return launch_ann_f32x2_t<50, 52, 5, ACT>(p, st, num_sms);
     if (p.width == 50 && p.m == 7) return launch_ann_f32x2_t<50, 52, 7, ACT>(p, st, num_sms);
+  }
+  if (variant != 60) {
+    // two neurons per iteration with two FFMA2 chains each, written out (cfg1: 3.49e9 -> 3.79e9 path-steps/s;
+    // four neurons per iteration 3.78e9)
+    if (p.width == 50 && p.m == 5) return launch_ann_f32x2_t<50, 52, 5, ACT, 1, 2>(p, st, num_sms);
+    if (p.width == 50 && p.m == 7) return launch_ann_f32x2_t<50, 52, 7, ACT, 1, 2>(p, st, num_sms);
   }
   if (p.width == 50 && p.m == 5) return launch_ann_f32_t<50, 52, 5, false, ACT, 2>(p, st, num_sms);
   if (p.width == 50 && p.m == 7) return launch_ann_f32_t<50, 52, 7, false, ACT, 2>(p, st, num_sms);

@@ -12,7 +12,7 @@ for w in $W; do
     cfg4)  K=regex:ann_tc_step_kernel;  CMD="python profiles/ann_probe.py cfg4 bf16 20000000 1" ;;
     split) K=regex:ann_tc_step_kernel;  CMD="python profiles/ann_probe.py cfg1 split 10000000 1" ;;
     tf32)  K=regex:ann_tc_step_kernel;  CMD="python profiles/ann_probe.py cfg1 tf32 10000000 1" ;;
-    fp32)  K=regex:ann_f32_step_kernel; CMD="python profiles/ann_probe.py cfg1 fp32 4000000 1" ;;
+    fp32)  K=regex:ann_f32; CMD="python profiles/ann_probe.py cfg1 fp32 4000000 1" ;;
     cfg3)  K=regex:exact_full4_kernel;  CMD="python profiles/exact_probe.py 50000000 1" ;;
   esac
   timeout 600 $NCU -k $K -s 1 -c 1 -o $O/${T}_$w -f $CMD > $O/${T}_$w.log 2>&1
