@@ -197,9 +197,47 @@ __device__ __forceinline__ void box_muller_fast_x2(uint32_t rap, uint32_t rbp, u
   Wa = f2fma(RAD, f2pk(csp, csq), f2c(0.0f));
   Wb = f2fma(RAD, f2pk(snp, snq), f2c(0.0f));
 }
+
+// The same fast Box-Muller with fewer FMA-pipe operations (the FULL kernel is bound by the FMA pipe: Philox's
+// IMAD.WIDE and these FFMA2, profiles/r02_exact_full4x2_ncu.md), returning the normal in units of
+// s = sqrt(2 ln 2): W' = -Z / s = sqrt(-log2 u) cos(a).  The factor -2 ln 2 of ln u moves out of the radius (the
+// sqrt takes -log2 u through its operand's negation), the series branch carries 1/(2 ln 2) in its coefficients
+// (v P(v) / ln 2 with P(v) = 1 + v/2 + v^2/3 + v^3/4 + v^4/5 ~ -ln(1 - v) / v), and the reduced angle
+// 2 pi (u_b - 1/2) = 2 pi ((bits_b - 3/2) + 2^-24) is two FFMA2 from the mantissa bits (bits_b - 3/2 exact).
+// The caller scales its Horner coefficients by s^j.  Same inputs and accuracy as box_muller_fast.
+__device__ __forceinline__ void box_muller_fast_x2s(uint32_t rap, uint32_t rbp, uint32_t raq, uint32_t rbq,
+                                                    uint64_t& Wa, uint64_t& Wb) {
+  constexpr float kInvLn2 = 1.4426950408889634f;
+  const uint64_t UA = f2fma(f2pk(unit_bits(rap), unit_bits(raq)), f2c(1.0f), f2c(-0.99999994039535522f));
+  const uint64_t V = f2fma(UA, f2c(-1.0f), f2c(1.0f));
+  uint64_t P = f2fma(V, f2c(0.2f * kInvLn2), f2c(0.25f * kInvLn2));
+  P = f2fma(P, V, f2c(0.33333333f * kInvLn2));
+  P = f2fma(P, V, f2c(0.5f * kInvLn2));
+  P = f2fma(P, V, f2c(kInvLn2));
+  const uint64_t SER = f2fma(V, P, f2c(0.0f));   // -log2(u) for v < 1/16
+  float uap, uaq, vp, vq, sp, sq;
+  f2up(UA, uap, uaq);
+  f2up(V, vp, vq);
+  f2up(SER, sp, sq);
+  float rp, rq;
+  const float lp = lg2_fast(uap), lq = lg2_fast(uaq);
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(rp) : "f"((vp < 0.0625f) ? sp : -lp));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(rq) : "f"((vq < 0.0625f) ? sq : -lq));
+  const uint64_t D = f2fma(f2pk(unit_bits(rbp), unit_bits(rbq)), f2c(1.0f), f2c(-1.5f));
+  float ap, aq;
+  f2up(f2fma(D, f2c(6.2831853071795865f), f2c(6.2831853071795865f * 0x1p-24f)), ap, aq);
+  float snp, snq, csp, csq;
+  asm("sin.approx.f32 %0, %1;" : "=f"(snp) : "f"(ap));
+  asm("cos.approx.f32 %0, %1;" : "=f"(csp) : "f"(ap));
+  asm("sin.approx.f32 %0, %1;" : "=f"(snq) : "f"(aq));
+  asm("cos.approx.f32 %0, %1;" : "=f"(csq) : "f"(aq));
+  const uint64_t RAD = f2pk(rp, rq);
+  Wa = f2fma(RAD, f2pk(csp, csq), f2c(0.0f));
+  Wb = f2fma(RAD, f2pk(snp, snq), f2c(0.0f));
+}
 }  // namespace
 
-template <int MR, int COLLOC, bool FAST, bool REF_ON, bool CS, int MINB = 1>
+template <int MR, int COLLOC, bool FAST, bool REF_ON, bool CS, int MINB = 1, bool SCALED = true>
 __global__ void __launch_bounds__(256, MINB) exact_full4_kernel(const __grid_constant__ RunParams p) {
   static_assert(COLLOC == kExactGbm && FAST, "FFMA2 full-output kernel: GBM closed form, fast normals");
   extern __shared__ uint32_t hist[];
@@ -208,9 +246,16 @@ __global__ void __launch_bounds__(256, MINB) exact_full4_kernel(const __grid_con
   __syncthreads();
   StatAcc acc;
   // Horner in W = -Z: q'_j = (-1)^(MR-1-j) q_j gives qz' = (-1)^(MR-1) qz, rounding for rounding
+  // SCALED: the normals arrive as W' = W / s (box_muller_fast_x2s), so coefficient j carries s^j
+  constexpr float kS = 1.1774100225154747f;   // sqrt(2 ln 2)
   uint64_t QC[MR];
+  float sj = 1.0f;
 #pragma unroll
-  for (int j = 0; j < MR; ++j) QC[j] = f2c(((MR - 1 - j) & 1) ? -p.q[j] : p.q[j]);
+  for (int j = 0; j < MR; ++j) {
+    const float c = ((MR - 1 - j) & 1) ? -p.q[j] : p.q[j];
+    QC[j] = f2c(SCALED ? c * sj : c);
+    sj *= kS;
+  }
   constexpr float kSign = ((MR - 1) & 1) ? -1.0f : 1.0f;
   const uint64_t n4 = p.n_paths >> 2, stride = (uint64_t)gridDim.x * blockDim.x;
   const int nb = (p.n_steps + 3) >> 2;
@@ -236,10 +281,17 @@ __global__ void __launch_bounds__(256, MINB) exact_full4_kernel(const __grid_con
       for (int u = 0; u < 4; ++u) r[u] = philox_path_block_rk(p.rk0, p.rk1, gp + u, (uint32_t)b);
       // W[k][pair]: step k of the block for paths (0,1) and (2,3)
       uint64_t W[4][2];
-      box_muller_fast_x2(r[0].x, r[0].y, r[1].x, r[1].y, W[0][0], W[1][0]);
-      box_muller_fast_x2(r[2].x, r[2].y, r[3].x, r[3].y, W[0][1], W[1][1]);
-      box_muller_fast_x2(r[0].z, r[0].w, r[1].z, r[1].w, W[2][0], W[3][0]);
-      box_muller_fast_x2(r[2].z, r[2].w, r[3].z, r[3].w, W[2][1], W[3][1]);
+      if constexpr (SCALED) {
+        box_muller_fast_x2s(r[0].x, r[0].y, r[1].x, r[1].y, W[0][0], W[1][0]);
+        box_muller_fast_x2s(r[2].x, r[2].y, r[3].x, r[3].y, W[0][1], W[1][1]);
+        box_muller_fast_x2s(r[0].z, r[0].w, r[1].z, r[1].w, W[2][0], W[3][0]);
+        box_muller_fast_x2s(r[2].z, r[2].w, r[3].z, r[3].w, W[2][1], W[3][1]);
+      } else {
+        box_muller_fast_x2(r[0].x, r[0].y, r[1].x, r[1].y, W[0][0], W[1][0]);
+        box_muller_fast_x2(r[2].x, r[2].y, r[3].x, r[3].y, W[0][1], W[1][1]);
+        box_muller_fast_x2(r[0].z, r[0].w, r[1].z, r[1].w, W[2][0], W[3][0]);
+        box_muller_fast_x2(r[2].z, r[2].w, r[3].z, r[3].w, W[2][1], W[3][1]);
+      }
       const int ns = (p.n_steps - 4 * b < 4) ? p.n_steps - 4 * b : 4;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -257,13 +309,14 @@ __global__ void __launch_bounds__(256, MINB) exact_full4_kernel(const __grid_con
             Y23 = f2fma(Y23, f2c(-1.0f), f2c(0.0f));
           }
           if (REF_ON) {
+            const float zs = SCALED ? -kS : -1.0f;
             float w0, w1, w2, w3;
             f2up(W[k][0], w0, w1);
             f2up(W[k][1], w2, w3);
-            ref_step(rs[0], p, -w0);
-            ref_step(rs[1], p, -w1);
-            ref_step(rs[2], p, -w2);
-            ref_step(rs[3], p, -w3);
+            ref_step(rs[0], p, zs * w0);
+            ref_step(rs[1], p, zs * w1);
+            ref_step(rs[2], p, zs * w2);
+            ref_step(rs[3], p, zs * w3);
           }
           o += n4;
           put(o);
@@ -643,13 +696,13 @@ cudaError_t launch_exact_special_r(const RunParams& p, cudaStream_t st, int num_
   return launch_persistent(exact_special_kernel<7, COLLOC, FAST, REF_ON>, 256, smem, p, st, num_sms);
 }
 
-template <int COLLOC, bool FAST, bool REF_ON, bool CS, int MINB = 1>
+template <int COLLOC, bool FAST, bool REF_ON, bool CS, int MINB = 1, bool SC = true>
 cudaError_t launch_exact_full4_r(const RunParams& p, cudaStream_t st, int num_sms, size_t smem) {
   if (p.m != 5 && p.m != 7)
-    return launch_persistent(exact_full4_kernel<8, COLLOC, FAST, REF_ON, CS, MINB>, 256, smem, p, st, num_sms, 1024);
+    return launch_persistent(exact_full4_kernel<8, COLLOC, FAST, REF_ON, CS, MINB, SC>, 256, smem, p, st, num_sms, 1024);
   if (p.m == 5)
-    return launch_persistent(exact_full4_kernel<5, COLLOC, FAST, REF_ON, CS, MINB>, 256, smem, p, st, num_sms, 1024);
-  return launch_persistent(exact_full4_kernel<7, COLLOC, FAST, REF_ON, CS, MINB>, 256, smem, p, st, num_sms, 1024);
+    return launch_persistent(exact_full4_kernel<5, COLLOC, FAST, REF_ON, CS, MINB, SC>, 256, smem, p, st, num_sms, 1024);
+  return launch_persistent(exact_full4_kernel<7, COLLOC, FAST, REF_ON, CS, MINB, SC>, 256, smem, p, st, num_sms, 1024);
 }
 
 template <int COLLOC, bool FAST>
@@ -669,6 +722,8 @@ cudaError_t launch_exact_special(const RunParams& p, cudaStream_t st, int num_sm
                                     : launch_exact_full4_r<COLLOC, FAST, false, true, 4>(p, st, num_sms, smem);
       if (variant == 53) return ref ? launch_exact_full4_r<COLLOC, FAST, true, true, 3>(p, st, num_sms, smem)
                                     : launch_exact_full4_r<COLLOC, FAST, false, true, 3>(p, st, num_sms, smem);
+      if (variant == 54) return ref ? launch_exact_full4_r<COLLOC, FAST, true, true, 4, false>(p, st, num_sms, smem)
+                                    : launch_exact_full4_r<COLLOC, FAST, false, true, 4, false>(p, st, num_sms, smem);
       // 4 CTAs of 256 per SM (<= 64 registers): 9.0e11 vs 8.8e11 path-steps/s at 3 (cfg3, B200)
       return ref ? launch_exact_full4_r<COLLOC, FAST, true, true, 4>(p, st, num_sms, smem)
                  : launch_exact_full4_r<COLLOC, FAST, false, true, 4>(p, st, num_sms, smem);
