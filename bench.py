@@ -369,7 +369,7 @@ def main():
 
 
 # ncu --set full DRAM bytes (read + write) per launch of the headline kernel, by precision
-TRAFFIC = {"bf16": 140800}   # profiles/r02_cfg4_bf16_ncu.md (1e8-path launch; read 140.8 KB, write 0)
+TRAFFIC = {"bf16": 129024}   # profiles/r02_cfg4_pair_ncu.md (the current kernel, 2e7-path launch; read 129.0 KB, write 0)
 
 
 def ann_roofline(dims, prec, rate, sl7, peaks, n_sms, sm_max):

@@ -34,6 +34,27 @@ __device__ __forceinline__ float op(float x) {
     r = __uint_as_float(v);
   }
   if constexpr (OP == 9) r = __uint_as_float(__float_as_uint(x) ^ 0x5a5a5a5au);  // LOP3 (ALU pipe)
+  if constexpr (OP == 12) {  // ex2.approx.f16x2: one instruction, two fp16 results
+    uint32_t u = __float_as_uint(x), v;
+    asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(v) : "r"(u));
+    r = __uint_as_float(v);
+  }
+  if constexpr (OP == 13) {
+    uint32_t u = __float_as_uint(x), v;
+    asm volatile("tanh.approx.f16x2 %0, %1;" : "=r"(v) : "r"(u));
+    r = __uint_as_float(v);
+  }
+  if constexpr (OP == 14) {  // IMAD.WIDE.U32 (Philox's multiply): low word feeds the chain, high word kept live
+    uint32_t u = __float_as_uint(x);
+    unsigned long long w;
+    asm volatile("mul.wide.u32 %0, %1, %2;" : "=l"(w) : "r"(u), "r"(0xD2511F53u));
+    r = __uint_as_float((uint32_t)w ^ (uint32_t)(w >> 32));
+  }
+  if constexpr (OP == 15) {  // FFMA with all-register operands (no immediate)
+    float m = __uint_as_float(__float_as_uint(x) | 1u), c;
+    asm volatile("mov.b32 %0, 0x38d1b717;" : "=f"(c));
+    asm volatile("fma.rn.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(x), "f"(m), "f"(c));
+  }
   return r;
 }
 
@@ -324,6 +345,10 @@ int main() {
     run<7>("ex2.approx.bf16x2 (2 results/instr)", sms, threads, d_out, d_cyc);
     run<8>("tanh.approx.bf16x2 (2 results/instr)", sms, threads, d_out, d_cyc);
     run<9>("LOP3 (ALU)", sms, threads, d_out, d_cyc);
+    run<12>("ex2.approx.f16x2 (2 results/instr)", sms, threads, d_out, d_cyc);
+    run<13>("tanh.approx.f16x2 (2 results/instr)", sms, threads, d_out, d_cyc);
+    run<14>("mul.wide.u32 + LOP3 (IMAD.WIDE)", sms, threads, d_out, d_cyc);
+    run<15>("FFMA all-register operands (+ LOP3)", sms, threads, d_out, d_cyc);
   }
   run_hbm(sms);
   return 0;
