@@ -265,7 +265,18 @@ __device__ __forceinline__ void issue_layer(uint32_t acc_t, uint32_t a_t, uint32
   }
 }
 
-template <int NG, int H, int MR, bool RT_M, int ACT, unsigned NMASK, int NP = 1, bool SKIPMMA = false, bool TF32 = false>
+// AS (A operand in shared memory): thread row r of the group's [128 x 64] bf16 A tile, SWIZZLE_128B K-major
+// (the layout of the weight tiles): row r at (r / 8) 1024 + (r % 8) 128 bytes, its 16-byte chunk c (columns
+// 8c .. 8c+7) at chunk position c ^ (r % 8).  NW packed words = NW / 4 chunks starting at chunk c0.
+template <int NW>
+__device__ __forceinline__ void st_a_row(uint32_t row_base, uint32_t r7, int c0, const uint32_t (&w)[NW]) {
+#pragma unroll
+  for (int q = 0; q < NW / 4; ++q)
+    tc::st_shared_v4(row_base + ((((uint32_t)(c0 + q)) ^ r7) << 4), w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+}
+
+template <int NG, int H, int MR, bool RT_M, int ACT, unsigned NMASK, int NP = 1, bool SKIPMMA = false, bool TF32 = false,
+          bool AS = false>
 __global__ void __launch_bounds__(NG * kGroupThreads, 1)
     ann_tc_step_kernel(const __grid_constant__ RunParams p, const __grid_constant__ TcParams t) {
   // epilogue in quarters of 16 columns (paired softplus, NMASK bit 9); the A columns of a quarter that is
@@ -281,7 +292,9 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
   const int wq = warp & 3;                 // warp within the group -> TMEM lanes [32 wq, 32 wq + 32)
   const int tid_g = threadIdx.x & (kGroupThreads - 1);
   static_assert(!TF32 || NP == 1, "TF32 has one operand part");
-  constexpr uint32_t kCols = kAccCol + 64u + (TF32 ? 64u : 32u * NP);   // acc fp32 [0,64) + A (NP 16-bit parts | tf32)
+  static_assert(!AS || (NP == 1 && !TF32), "A in shared memory: the bf16 kernel");
+  // acc fp32 [0,64) + A (NP 16-bit parts | tf32) in TMEM, or the accumulator alone when A lives in shared memory
+  constexpr uint32_t kCols = AS ? 64u : kAccCol + 64u + (TF32 ? 64u : 32u * NP);
   constexpr uint32_t kTileB = TF32 ? 2u * kTcTileBytes : (uint32_t)kTcTileBytes;   // bytes per weight tile part
   constexpr uint32_t kOutB = TF32 ? 2u * kTcOutBytes : (uint32_t)kTcOutBytes;
   constexpr uint32_t kTmemCols = NG * kCols <= 256 ? 256u : 512u;
@@ -293,7 +306,9 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
   uint8_t* wsm = smem_raw + (sbase - tc::smem_u32(smem_raw));
   const int nL = t.n_mma_hidden;
   const int wbytes = NP * (nL * (int)kTileB + (int)kOutB);
-  uint32_t* hist = reinterpret_cast<uint32_t*>(wsm + wbytes);
+  constexpr int kATileBytes = 128 * 128;   // AS: [128 rows][64 bf16] per group
+  const int abytes = AS ? NG * kATileBytes : 0;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(wsm + wbytes + abytes);
   // per-thread running sums of the statistics live in shared memory ([8][threads], SoA), not in registers:
   // they change once per tile, and the 12 registers they would pin are worth more to the epilogue
   const int hist_words = (p.has_stats && p.n_bins > 0) ? ((p.n_bins + 2 + 1) & ~1) : 0;
@@ -327,6 +342,10 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
                                     : (NP == 2 ? tc::idesc_f16_f32(128, kTcNOut) : tc::idesc_bf16_f32(128, kTcNOut));
   uint64_t* bar = &mbar[g];
   uint32_t phase = 0;
+  // AS: the group's A tile (1024-aligned: the weight image is a multiple of 1024 bytes) and this thread's row
+  const uint32_t a_s = sbase + (uint32_t)wbytes + (uint32_t)g * kATileBytes;
+  const uint32_t a_row = a_s + ((uint32_t)tid_g >> 3) * 1024u + ((uint32_t)tid_g & 7u) * 128u;
+  const uint32_t a_r7 = (uint32_t)tid_g & 7u;
 
   const uint64_t n_tiles = (p.n_paths + kGroupThreads - 1) / kGroupThreads;
   for (uint64_t tile = (uint64_t)blockIdx.x * NG + g; tile < n_tiles; tile += (uint64_t)gridDim.x * NG) {
@@ -374,12 +393,17 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
           uint32_t pk[NP][16];
 #pragma unroll
           for (int k = 0; k < 16; ++k) split_pack<NP>(h[2 * k], h[2 * k + 1], pk, k);
+          if constexpr (AS) {
+            st_a_row<16>(a_row, a_r7, 4 * half, pk[0]);
+          } else {
 #pragma unroll
-          for (int part = 0; part < NP; ++part)
-            tc::tmem_st_32x32b_x16(a_t + 32u * part + lane_off + 16u * half, pk[part]);
+            for (int part = 0; part < NP; ++part)
+              tc::tmem_st_32x32b_x16(a_t + 32u * part + lane_off + 16u * half, pk[part]);
+          }
         }
       }
-      tc::wait_st();
+      if constexpr (AS) tc::fence_proxy_async_smem();
+      else tc::wait_st();
       // ---- layers 2..L+1 on the tensor cores; the Lagrange basis at Z (independent of the MLP)
       //      is computed while the first MMA runs
       float lb[MR], den = 1.0f, y[MR];
@@ -397,6 +421,13 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
           } else if (TF32) {
             if (last) issue_layer_tf32(acc_t, a_t, sbase + (uint32_t)(nL * kTileB), kTcNOut, idesc_o);
             else issue_layer_tf32(acc_t, a_t, sbase + (uint32_t)(l * kTileB), kTcN, idesc_h);
+          } else if (AS) {
+            const uint64_t adesc = tc::smem_desc_sw128(a_s);
+            const uint64_t bdesc = tc::smem_desc_sw128(sbase + (uint32_t)((last ? nL : l) * kTcTileBytes));
+            const uint32_t idesc = last ? idesc_o : idesc_h;
+#pragma unroll
+            for (int k = 0; k < kTcN / 16; ++k)
+              tc::mma_bf16_ss(acc_t, adesc + 2u * k, bdesc + 2u * k, idesc, k > 0 ? 1u : 0u);
           } else if (last) {
             issue_layer<NP>(acc_t, a_t, sbase + (uint32_t)(NP * nL * kTcTileBytes), kTcOutBytes, idesc_o);
           } else {
@@ -420,9 +451,13 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
                 tc::wait_ld();
                 uint32_t pk[NP][8];
                 act_pack_32<ACT, H, NMASK, FOLD, NP, 16>(v, 16 * qt, t.lscale[l], t.bias[l], pk);
+                if constexpr (AS) {
+                  st_a_row<8>(a_row, a_r7, 2 * qt, pk[0]);
+                } else {
 #pragma unroll
-                for (int part = 0; part < NP; ++part)
-                  tc::tmem_st_32x32b_x8(a_t + 32u * part + lane_off + 8u * qt, pk[part]);
+                  for (int part = 0; part < NP; ++part)
+                    tc::tmem_st_32x32b_x8(a_t + 32u * part + lane_off + 8u * qt, pk[part]);
+                }
               }
             }
           } else {
@@ -438,13 +473,18 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
             } else {
               uint32_t pk[NP][16];
               act_pack_32<ACT, H, NMASK, FOLD, NP>(v, 32 * half, t.lscale[l], t.bias[l], pk);
+              if constexpr (AS) {
+                st_a_row<16>(a_row, a_r7, 4 * half, pk[0]);
+              } else {
 #pragma unroll
-              for (int part = 0; part < NP; ++part)
-                tc::tmem_st_32x32b_x16(a_t + 32u * part + lane_off + 16u * half, pk[part]);
+                for (int part = 0; part < NP; ++part)
+                  tc::tmem_st_32x32b_x16(a_t + 32u * part + lane_off + 16u * half, pk[part]);
+              }
             }
           }
           }
-          tc::wait_st();
+          if constexpr (AS) tc::fence_proxy_async_smem();
+          else tc::wait_st();
         } else {
           uint32_t v[16];
           tc::tmem_ld_32x32b_x16(acc_t + lane_off, v);
@@ -491,13 +531,15 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
 
 namespace {
 
-template <int NG, int H, int MR, bool RT, int ACT, unsigned NMASK = 0u, int NP = 1, bool SKIP = false, bool TF32 = false>
+template <int NG, int H, int MR, bool RT, int ACT, unsigned NMASK = 0u, int NP = 1, bool SKIP = false, bool TF32 = false,
+          bool AS = false>
 cudaError_t launch_tc_t(const RunParams& p, const TcParams& t, cudaStream_t st, int num_sms) {
-  auto kernel = ann_tc_step_kernel<NG, H, MR, RT, ACT, NMASK, NP, SKIP, TF32>;
+  auto kernel = ann_tc_step_kernel<NG, H, MR, RT, ACT, NMASK, NP, SKIP, TF32, AS>;
   const size_t hist = (p.has_stats && p.n_bins > 0) ? sizeof(uint32_t) * (size_t)((p.n_bins + 2 + 1) & ~1) : 0;
   const size_t sst = p.has_stats ? sizeof(double) * 8 * NG * kGroupThreads : 0;
   const size_t tile_b = TF32 ? 2 * kTcTileBytes : kTcTileBytes, out_b = TF32 ? 2 * kTcOutBytes : kTcOutBytes;
-  const size_t smem = 1024 + (size_t)NP * ((size_t)t.n_mma_hidden * tile_b + out_b) + hist + sst;
+  const size_t smem = 1024 + (size_t)NP * ((size_t)t.n_mma_hidden * tile_b + out_b) + (AS ? (size_t)NG * 128 * 128 : 0) +
+                      hist + sst;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const uint64_t tiles = (p.n_paths + kGroupThreads - 1) / kGroupThreads;
@@ -556,6 +598,12 @@ cudaError_t launch_softplus_bf16(const RunParams& p, const TcParams& t, cudaStre
     case 36: return launch_sp_pair<0x3FFu>(p, t, st, num_sms);
     case 37: return launch_tc_t<kTcGroupsSoftplus, 50, 7, false, kActSoftplusPair, 0x15Fu, 1, true>(p, t, st, num_sms);
     case 38: return launch_tc_t<4, 50, 7, false, kActSoftplusPair, 0x15Fu>(p, t, st, num_sms);
+    // A operand in shared memory: 64 TMEM columns per tile, 6 / 7 tile groups per SM
+    case 39: return launch_tc_t<6, 50, 7, false, kActSoftplusPair, 0x15Fu, 1, false, false, true>(p, t, st, num_sms);
+    case 44: return launch_tc_t<7, 50, 7, false, kActSoftplusPair, 0x15Fu, 1, false, false, true>(p, t, st, num_sms);
+    case 45: return launch_tc_t<5, 50, 7, false, kActSoftplusPair, 0x15Fu, 1, false, false, true>(p, t, st, num_sms);
+    case 46: return launch_tc_t<6, 50, 7, false, kActSoftplusPair, 0x35Fu, 1, false, false, true>(p, t, st, num_sms);
+    case 47: return launch_tc_t<7, 50, 7, false, kActSoftplusPair, 0x35Fu, 1, false, false, true>(p, t, st, num_sms);
     default: break;
   }
 #endif

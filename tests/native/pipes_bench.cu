@@ -50,6 +50,22 @@ __device__ __forceinline__ float op(float x) {
     asm volatile("mul.wide.u32 %0, %1, %2;" : "=l"(w) : "r"(u), "r"(0xD2511F53u));
     r = __uint_as_float((uint32_t)w ^ (uint32_t)(w >> 32));
   }
+  if constexpr (OP == 16) {  // mul.lo.u32 by an immediate (IMAD)
+    uint32_t u = __float_as_uint(x), w;
+    asm volatile("mul.lo.u32 %0, %1, %2;" : "=r"(w) : "r"(u), "n"(0xD2511F53u));
+    r = __uint_as_float(w);
+  }
+  if constexpr (OP == 17) {  // mul.hi.u32 by an immediate (IMAD.HI)
+    uint32_t u = __float_as_uint(x), w;
+    asm volatile("mul.hi.u32 %0, %1, %2;" : "=r"(w) : "r"(u), "n"(0xD2511F53u));
+    r = __uint_as_float(w | 0x3f000000u);
+  }
+  if constexpr (OP == 18) {  // mul.wide.u32 by an immediate, both halves consumed by one LOP3-free add
+    uint32_t u = __float_as_uint(x);
+    unsigned long long w;
+    asm volatile("mul.wide.u32 %0, %1, %2;" : "=l"(w) : "r"(u), "n"(0xD2511F53u));
+    r = __uint_as_float((uint32_t)w + (uint32_t)(w >> 32));
+  }
   if constexpr (OP == 15) {  // FFMA with all-register operands (no immediate)
     float m = __uint_as_float(__float_as_uint(x) | 1u), c;
     asm volatile("mov.b32 %0, 0x38d1b717;" : "=f"(c));
@@ -349,6 +365,9 @@ int main() {
     run<13>("tanh.approx.f16x2 (2 results/instr)", sms, threads, d_out, d_cyc);
     run<14>("mul.wide.u32 + LOP3 (IMAD.WIDE)", sms, threads, d_out, d_cyc);
     run<15>("FFMA all-register operands (+ LOP3)", sms, threads, d_out, d_cyc);
+    run<16>("mul.lo.u32 imm (IMAD)", sms, threads, d_out, d_cyc);
+    run<17>("mul.hi.u32 imm (IMAD.HI) + LOP3", sms, threads, d_out, d_cyc);
+    run<18>("mul.wide.u32 imm (IMAD.WIDE) + IADD3", sms, threads, d_out, d_cyc);
   }
   run_hbm(sms);
   return 0;
