@@ -114,7 +114,10 @@ typedef enum { SL7_REF_NONE = 0, SL7_REF_GBM = 1, SL7_REF_OU = 2 } sl7_ref;
  * The table is then the same for every path set, so there are no selection passes and no exchange:
  * shard it like SL7_SCHEME_7L with path_offset.  The network must be fitted for horizons up to T: with a
  * blob that carries its fitted domain (flags bit 2), a call whose horizons dt..(n_steps-1) dt or whose Y0
- * leave that box fails with SL7_EINVAL instead of extrapolating. */
+ * leave that box fails with SL7_EINVAL instead of extrapolating.  The hull clamp truncates the tails; a
+ * CDC_PRED run with a stats vector reports how often it acted: E1 (slot 6, unused otherwise since the CDC
+ * schemes take no strong-error reference) = the number of path-steps whose state was outside
+ * [z_0, z_{m-1}] and clamped, E2 = 0 (sl7_stats then reports E1 / n as strong_err: clamped steps per path). */
 typedef enum { SL7_SCHEME_7L = 0, SL7_SCHEME_CDC = 1, SL7_SCHEME_CDC_PRED = 2 } sl7_scheme;
 
 typedef struct {

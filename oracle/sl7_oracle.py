@@ -566,6 +566,18 @@ def simulate_cdc_pred(spec: Spec, seed: int, paths) -> tuple[np.ndarray, np.ndar
     return Y, Z
 
 
+def cdc_pred_clamped(spec: Spec, Y) -> int:
+    """Number of path-steps whose state lies outside the marginal hull [z_0, z_{m-1}] of its step and is
+    clamped by cdc_pred_state (steps with repeated or unordered z use the nearest row: no clamp).  Y is the
+    (n_steps + 1, P) state array of simulate_cdc_pred; NaN states are not counted."""
+    n = 0
+    for i in range(spec.n_steps):
+        z = cdc_pred_marginals(spec, i)
+        if np.all(np.diff(z) > 0):
+            n += int(np.count_nonzero((Y[i] < z[0]) | (Y[i] > z[-1])))
+    return n
+
+
 def cdc_pred_step_error_scale(spec: Spec, i: int, Y, Z) -> np.ndarray:
     """Forward-error scale of cdc_pred_step (tolerance helper): as cdc_step_error_scale on z_i."""
     z = cdc_pred_marginals(spec, i)

@@ -196,9 +196,14 @@ def stats_summary(h_stats, opts, q_levels=()):
     st = L.sl7_stats(v.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(opts), ctypes.byref(s))
     if st not in (OK, ENONFINITE):
         _check(st)
-    return {"n": s.n, "n_nonfinite": s.n_nonfinite, "mean": s.mean, "var": s.var, "skew": s.skew,
-            "exkurt": s.exkurt, "strong_err": s.strong_err, "rms_err": s.rms_err,
-            "quantiles": [qv[i] for i in range(len(q_levels))], "status": st}
+    out = {"n": s.n, "n_nonfinite": s.n_nonfinite, "mean": s.mean, "var": s.var, "skew": s.skew,
+           "exkurt": s.exkurt, "strong_err": s.strong_err, "rms_err": s.rms_err,
+           "quantiles": [qv[i] for i in range(len(q_levels))], "status": st}
+    if opts.scheme == SCHEME_CDC_PRED:
+        # E1 of a CDC_PRED run counts the path-steps clamped to the marginal hull (include/sl7.h)
+        out["clamped_steps"] = float(v[6])
+        out["strong_err"] = out["rms_err"] = 0.0
+    return out
 
 
 def philox_u32(seed, path_offset, n_paths, block, out, stream=None):

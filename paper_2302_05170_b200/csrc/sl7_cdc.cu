@@ -449,6 +449,7 @@ __global__ void __launch_bounds__(256) cdc_step_kernel(const __grid_constant__ R
       for (int j = 0; j < MR; ++j) Cr[k][j] = sC[k][j];
   }
   StatAcc acc;
+  uint32_t ncl = 0;   // CDC_PRED: clamped path-steps of this step (stats E1)
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const int lane = threadIdx.x & 31;
   // warp-uniform trip count (the fused histogram's __match_any_sync needs every lane)
@@ -479,6 +480,7 @@ __global__ void __launch_bounds__(256) cdc_step_kernel(const __grid_constant__ R
       // Y - z_k with the marginal point carried as z + zlo (double-accurate nodes, as the GH grid's hi/lo)
       // CDC_PRED (R-26): the state clamped to the marginal hull (zlo = 0 there: the points are fp32); NaN stays
       const float Yb = !clamp_hull ? Y : (Y < sz[0]) ? sz[0] : (Y > sz[m - 1]) ? sz[m - 1] : Y;
+      ncl += (clamp_hull && (Y < sz[0] || Y > sz[m - 1])) ? 1u : 0u;
       for (int k = 0; k < MR; ++k) d[k] = (RT_M && k >= m) ? 1.0f : ((Yb - sz[k]) - szlo[k]) * ssinv;
       pre[0] = 1.0f;
 #pragma unroll
@@ -517,7 +519,13 @@ __global__ void __launch_bounds__(256) cdc_step_kernel(const __grid_constant__ R
     }
     if (next_hist) warp_hist_add(nh, nbin);   // one call site, all lanes
   }
-  if (last && p.has_stats) stat_flush(acc, p, hist, red);
+  if (last && p.has_stats) {
+    acc.e1 += (double)ncl;
+    stat_flush(acc, p, hist, red);
+  } else if (p.has_stats && clamp_hull) {
+    const double c = warp_sum((double)ncl);
+    if (lane == 0 && c != 0.0) atomicAdd(&p.stats[6], c);
+  }
   if (next_hist) {
     __syncthreads();
     for (int i = threadIdx.x; i < 256; i += blockDim.x)
@@ -538,10 +546,11 @@ struct CdcSTab {
 };
 constexpr int kCdcFusedP = 4;
 
+// nclamp: +1 when the state lies outside the marginal hull and is clamped (reported in the stats vector's E1 slot)
 template <int MR, bool FAST>
 __device__ __forceinline__ float cdc_pred_path_step(const RunParams& p, const CdcSTab<MR>& T, const float (&Cr)[MR][MR],
                                                     const float (&zr)[MR], const float (&vr)[MR], float sinv,
-                                                    float Y, float Z) {
+                                                    float Y, float Z, uint32_t& nclamp) {
   float y[MR];
   if (T.deg) {   // repeated / unordered marginal points (step 0): the nearest row, ties -> lowest k (R-20)
     int kb = 0;
@@ -555,6 +564,7 @@ __device__ __forceinline__ float cdc_pred_path_step(const RunParams& p, const Cd
     for (int j = 0; j < MR; ++j) y[j] = T.C[kb][j];
   } else {
     const float Yb = (Y < zr[0]) ? zr[0] : (Y > zr[MR - 1]) ? zr[MR - 1] : Y;   // hull clamp (R-26); NaN stays
+    nclamp += (Y < zr[0] || Y > zr[MR - 1]) ? 1u : 0u;
     float d[MR], pre[MR], lk[MR];
 #pragma unroll
     for (int k = 0; k < MR; ++k) d[k] = (Yb - zr[k]) * sinv;
@@ -607,6 +617,7 @@ __global__ void __launch_bounds__(256, 2) cdc_pred_fused_kernel(const __grid_con
   const bool full = (p.out_mode == kFull);
   const uint64_t N = p.n_paths, chunk = (uint64_t)blockDim.x * P;
   StatAcc acc;
+  uint32_t ncl = 0;   // clamped path-steps of this thread's valid paths
   for (uint64_t base = (uint64_t)blockIdx.x * chunk; base < N; base += (uint64_t)gridDim.x * chunk) {
     float Y[P], zn[P][4];
     bool ok[P];
@@ -650,7 +661,9 @@ __global__ void __launch_bounds__(256, 2) cdc_pred_fused_kernel(const __grid_con
 #pragma unroll
         for (int u = 0; u < P; ++u) {
           const float Z = (r == 0) ? zn[u][0] : (r == 1) ? zn[u][1] : (r == 2) ? zn[u][2] : zn[u][3];
-          Y[u] = cdc_pred_path_step<MR, FAST>(p, T, Cr, zr, vr, sinv, Y[u], Z);
+          uint32_t c = 0;
+          Y[u] = cdc_pred_path_step<MR, FAST>(p, T, Cr, zr, vr, sinv, Y[u], Z, c);
+          ncl += ok[u] ? c : 0u;
           if (full && ok[u]) out[(uint64_t)(i + 1) * N + base + (uint64_t)u * blockDim.x + threadIdx.x] = Y[u];
         }
       }
@@ -663,7 +676,10 @@ __global__ void __launch_bounds__(256, 2) cdc_pred_fused_kernel(const __grid_con
       if (p.has_stats) stat_add(acc, p, Y[u], 0.0, hist);
     }
   }
-  if (p.has_stats) stat_flush(acc, p, hist, red);
+  if (p.has_stats) {
+    acc.e1 += (double)ncl;   // E1 of a CDC_PRED run: clamped path-steps (no strong-error reference, include/sl7.h)
+    stat_flush(acc, p, hist, red);
+  }
 }
 
 __global__ void fill_kernel(float* y, uint64_t n, float v) {

@@ -128,6 +128,16 @@ def test_cdc_pred_cir_terminal_moments_identical_paths(gpu_lib, name):
                                                           abs(YT.var() / Yo.var() - 1)))
     assert abs(YT.mean() - Yo.mean()) <= 1e-4 * abs(Yo.mean())
     assert abs(YT.var() - Yo.var()) <= 1e-4 * Yo.var()
+    # the clamp count (stats E1 of a CDC_PRED run) against the oracle's count on the same paths: fp32 and
+    # fp64 states can fall on different sides of a hull edge, hence the small allowance
+    st = torch.zeros(sl7.stats_elems(0), dtype=torch.float64, device="cuda")
+    os_ = sl7.make_opts(colloc=code, scheme=sl7.SCHEME_CDC_PRED, shift=0.1)
+    ctx.simulate(w.y0, w.dt, w.n_steps, th, n, w.seed, sl7.OUT_STATS, os_, stats=st)
+    torch.cuda.synchronize()
+    nd, no = st[6].item(), O.cdc_pred_clamped(spec, Y)
+    print("%s CDC_PRED clamped path-steps: device %d oracle %d" % (name, nd, no))
+    assert no > 0 and abs(nd - no) <= 0.005 * no + 10
+    assert sl7.stats_summary(st.cpu().numpy(), os_)["clamped_steps"] == nd
 
 
 @pytest.mark.parametrize("name", ["cfg2_cir", "cfg4"])

@@ -118,3 +118,16 @@ def test_golden_blobs_carry_their_fitted_box():
         assert np.all(lo <= hi)
         if w.process == "cir":
             assert lo[1] <= w.dt and (w.n_steps - 1) * w.dt <= hi[1] and lo[0] <= w.y0 <= hi[0]
+
+
+def test_cdc_pred_clamped_counts_states_outside_the_hull():
+    # by hand: 3 steps of exact OU from Y0 = 1; step 0 has every path at Y0 (repeated z: nearest row, no
+    # clamp); the states of steps 1 and 2 are placed inside, below and above the predicted hull
+    spec = O.Spec(5, "ou", (0.0, 1.0, 0.5), 1.0, 0.25, 3)
+    z1, z2 = O.cdc_pred_marginals(spec, 1), O.cdc_pred_marginals(spec, 2)
+    Y = np.empty((4, 4))
+    Y[0] = 1.0
+    Y[1] = [z1[0] - 1e-3, 0.5 * (z1[0] + z1[-1]), z1[-1] + 1.0, np.nan]
+    Y[2] = [z2[0], z2[-1], z2[-1] + 1e-9, z2[0] - 5.0]
+    Y[3] = 123.0                                   # the terminal row is never read by a table
+    assert O.cdc_pred_clamped(spec, Y) == 2 + 2
