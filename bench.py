@@ -363,6 +363,15 @@ def main():
         line["cpu_baseline"] = {"value": rates[0], "unit": UNIT, "cores": cores, "kind": "oracle",
                                 "sample": "%d paths x 32 steps of cfg4 (%.1f s), float64 numpy oracle, "
                                           "multiprocessing pool" % (sample, els[0])}
+        # also a 1-core number (one chunk of the same oracle in this process, one BLAS thread)
+        from threadpoolctl import threadpool_limits
+        n1 = 65536
+        with threadpool_limits(1):
+            t0 = time.perf_counter()
+            done = _oracle_chunk(("cfg4", 0, n1))
+            el1 = time.perf_counter() - t0
+        line["cpu_baseline"]["value_1core"] = done / el1
+        line["cpu_baseline"]["sample_1core"] = "%d paths x 32 steps of cfg4 on one core (%.1f s)" % (n1, el1)
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

@@ -384,6 +384,47 @@ def test_exact_flags_teacher_forced(gpu_lib, colloc, m, theta, n_steps, dt, flag
     print("flags=%d worst |err|/kappa = %.3g" % (flags, worst))
 
 
+@pytest.mark.parametrize("m,theta,n_steps,dt", [(5, (0.05, 0.2), 64, 1 / 64), (7, (0.05, 0.2), 6, 0.5),
+                                                (6, (0.1, 0.5), 9, 0.25)])
+def test_exact_full4_teacher_forced(gpu_lib, m, theta, n_steps, dt):
+    """cfg3's FULL kernel (four paths per thread, 16-byte row stores, normals in units of sqrt(2 ln 2), Horner
+    coefficients scaled by s^j; it runs when n_paths % 4 == 0): teacher-forced against the float64 oracle on
+    the device's fast normals at 1e-5 * kappa, incl. m = 6 (padded Horner) and a 9-step tail of one block."""
+    sl7 = gpu_lib
+    torch = _torch()
+    n_paths = 30_000
+    ctx = sl7.Context(m)
+    opts = sl7.make_opts(colloc=sl7.COLLOC_EXACT_GBM, flags=sl7.FLAG_FAST_NORMALS | sl7.FLAG_SPECIALIZED)
+    out, _ = ctx.simulate(1.0, dt, n_steps, theta, n_paths, 78, sl7.OUT_FULL, opts)
+    z = torch.empty(n_steps * n_paths, dtype=torch.float32, device="cuda")
+    sl7.normals(78, 0, n_paths, n_steps, z, flags=sl7.FLAG_FAST_NORMALS)
+    torch.cuda.synchronize()
+    Yd = out.double().cpu().numpy().reshape(n_steps + 1, n_paths)
+    Z = z.double().cpu().numpy().reshape(n_steps, n_paths)
+    worst = _teacher_forced(O.Spec(m, "gbm", theta, 1.0, dt, n_steps), Yd, Z)
+    print("full4 m=%d worst |err|/kappa = %.3g" % (m, worst))
+
+
+def test_exact_full4_stats_and_reference(gpu_lib):
+    """The FULL kernel's REF_ON form (FULL output + fused statistics + strong error against exact GBM on the
+    same normals, which it rebuilds as -s W'): moments equal the oracle's statistics of the last row, the strong
+    error stays at rounding level."""
+    sl7 = gpu_lib
+    torch = _torch()
+    n_paths, n_steps, dt, theta = 40_000, 16, 1 / 16, (0.05, 0.2)
+    ctx = sl7.Context(7)
+    opts = sl7.make_opts(colloc=sl7.COLLOC_EXACT_GBM, flags=sl7.FLAG_FAST_NORMALS | sl7.FLAG_SPECIALIZED,
+                         n_bins=256, hist_lo=0.0, hist_hi=3.0, shift=1.0, ref=sl7.REF_GBM, ref_theta=theta + (0,))
+    st = torch.zeros(sl7.stats_elems(256), dtype=torch.float64, device="cuda")
+    out, _ = ctx.simulate(1.0, dt, n_steps, theta, n_paths, 79, sl7.OUT_FULL, opts, stats=st)
+    torch.cuda.synchronize()
+    YT = out.double().cpu().numpy()[-n_paths:]
+    v, s = O.stats_vector(YT, 1.0, 0.0, 3.0, 256), st.cpu().numpy()
+    np.testing.assert_allclose(s[2:6], v[2:6], rtol=1e-12, atol=1e-9)
+    assert s[8:].sum() == v[8:].sum() and np.abs(s[8:] - v[8:]).sum() <= 4   # T-5: edge ties only
+    assert s[0] == n_paths and 0 < s[6] / s[0] < 2e-6
+
+
 def test_fast_normals_vs_oracle(gpu_lib):
     """The SL7_FLAG_FAST_NORMALS Box-Muller (MUFU lg2 + series near u -> 1, MUFU sin/cos on the exactly
     reduced angle) stays within 2e-6 (1 + |Z|) of the float64 normals (measured 1.1e-6), including the
