@@ -282,6 +282,9 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
   // epilogue in quarters of 16 columns (paired softplus, NMASK bit 9); the A columns of a quarter that is
   // not stored keep the layer-1 values (all such columns are zero padding: the same on every layer)
   constexpr bool QUARTERS = (ACT == kActSoftplusPair) && (NMASK & 0x200u) && !TF32;
+  // NMASK bit 10 (with QUARTERS): software-pipelined quarters -- the TMEM load of quarter q+1 is issued before
+  // quarter q's activations are computed, so its latency hides behind them (two 16-value buffers live)
+  constexpr bool QPIPE = QUARTERS && (NMASK & 0x400u);
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint64_t mbar[NG];   // per group: MMA completion (tcgen05.commit)
   __shared__ uint32_t tmem_base_sh;
@@ -292,9 +295,11 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
   const int wq = warp & 3;                 // warp within the group -> TMEM lanes [32 wq, 32 wq + 32)
   const int tid_g = threadIdx.x & (kGroupThreads - 1);
   static_assert(!TF32 || NP == 1, "TF32 has one operand part");
-  static_assert(!AS || (NP == 1 && !TF32), "A in shared memory: the bf16 kernel");
-  // acc fp32 [0,64) + A (NP 16-bit parts | tf32) in TMEM, or the accumulator alone when A lives in shared memory
-  constexpr uint32_t kCols = AS ? 64u : kAccCol + 64u + (TF32 ? 64u : 32u * NP);
+  static_assert(!AS || !TF32, "A in shared memory: the 16-bit kernels");
+  // acc fp32 [0,64) + A (NP 16-bit parts | tf32) in TMEM.  AS: the LAST 16-bit part lives in shared memory (BF16:
+  // the only part, TMEM holds the accumulator alone; SPLIT: part 0 stays in TMEM, part 1 moves out -> 96 columns)
+  constexpr int NPT = AS ? NP - 1 : NP;   // operand parts in TMEM
+  constexpr uint32_t kCols = kAccCol + 64u + (TF32 ? 64u : 32u * NPT);
   constexpr uint32_t kTileB = TF32 ? 2u * kTcTileBytes : (uint32_t)kTcTileBytes;   // bytes per weight tile part
   constexpr uint32_t kOutB = TF32 ? 2u * kTcOutBytes : (uint32_t)kTcOutBytes;
   constexpr uint32_t kTmemCols = NG * kCols <= 256 ? 256u : 512u;
@@ -393,17 +398,14 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
           uint32_t pk[NP][16];
 #pragma unroll
           for (int k = 0; k < 16; ++k) split_pack<NP>(h[2 * k], h[2 * k + 1], pk, k);
-          if constexpr (AS) {
-            st_a_row<16>(a_row, a_r7, 4 * half, pk[0]);
-          } else {
 #pragma unroll
-            for (int part = 0; part < NP; ++part)
-              tc::tmem_st_32x32b_x16(a_t + 32u * part + lane_off + 16u * half, pk[part]);
-          }
+          for (int part = 0; part < NPT; ++part)
+            tc::tmem_st_32x32b_x16(a_t + 32u * part + lane_off + 16u * half, pk[part]);
+          if constexpr (AS) st_a_row<16>(a_row, a_r7, 4 * half, pk[NP - 1]);
         }
       }
       if constexpr (AS) tc::fence_proxy_async_smem();
-      else tc::wait_st();
+      if constexpr (NPT > 0 || TF32) tc::wait_st();
       // ---- layers 2..L+1 on the tensor cores; the Lagrange basis at Z (independent of the MLP)
       //      is computed while the first MMA runs
       float lb[MR], den = 1.0f, y[MR];
@@ -421,13 +423,26 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
           } else if (TF32) {
             if (last) issue_layer_tf32(acc_t, a_t, sbase + (uint32_t)(nL * kTileB), kTcNOut, idesc_o);
             else issue_layer_tf32(acc_t, a_t, sbase + (uint32_t)(l * kTileB), kTcN, idesc_h);
-          } else if (AS) {
+          } else if (AS && NP == 1) {
             const uint64_t adesc = tc::smem_desc_sw128(a_s);
             const uint64_t bdesc = tc::smem_desc_sw128(sbase + (uint32_t)((last ? nL : l) * kTcTileBytes));
             const uint32_t idesc = last ? idesc_o : idesc_h;
 #pragma unroll
             for (int k = 0; k < kTcN / 16; ++k)
               tc::mma_bf16_ss(acc_t, adesc + 2u * k, bdesc + 2u * k, idesc, k > 0 ? 1u : 0u);
+          } else if (AS) {
+            // SPLIT: h0 W0 + h0 W1 from the TMEM part, h1 W0 from the shared-memory part
+            const uint32_t b0 = sbase + (uint32_t)(NP * (last ? nL : l) * kTcTileBytes);
+            const uint32_t pb = last ? (uint32_t)kTcOutBytes : (uint32_t)kTcTileBytes;
+            const uint32_t idesc = last ? idesc_o : idesc_h;
+            const uint64_t bd0 = tc::smem_desc_sw128(b0), bd1 = tc::smem_desc_sw128(b0 + pb);
+            const uint64_t ad1 = tc::smem_desc_sw128(a_s);
+#pragma unroll
+            for (int k = 0; k < kTcN / 16; ++k) tc::mma_bf16_ts(acc_t, a_t + 8u * k, bd0 + 2u * k, idesc, k > 0 ? 1u : 0u);
+#pragma unroll
+            for (int k = 0; k < kTcN / 16; ++k) tc::mma_bf16_ts(acc_t, a_t + 8u * k, bd1 + 2u * k, idesc, 1u);
+#pragma unroll
+            for (int k = 0; k < kTcN / 16; ++k) tc::mma_bf16_ss(acc_t, ad1 + 2u * k, bd0 + 2u * k, idesc, 1u);
           } else if (last) {
             issue_layer<NP>(acc_t, a_t, sbase + (uint32_t)(NP * nL * kTcTileBytes), kTcOutBytes, idesc_o);
           } else {
@@ -440,7 +455,25 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
         phase ^= 1u;
         tc::fence_after();
         if (!last) {
-          if constexpr (QUARTERS) {
+          if constexpr (QPIPE) {
+            constexpr int NQ = ((FOLD ? H + 3 : H) + 15) / 16;   // quarters holding live columns
+            uint32_t va[16], vb[16];
+            tc::tmem_ld_32x32b_x16(acc_t + lane_off, va);
+            tc::wait_ld();
+#pragma unroll
+            for (int qt = 0; qt < NQ; ++qt) {
+              uint32_t (&cur)[16] = (qt & 1) ? vb : va;
+              uint32_t (&nxt)[16] = (qt & 1) ? va : vb;
+              if (qt + 1 < NQ) tc::tmem_ld_32x32b_x16(acc_t + lane_off + 16u * (qt + 1), nxt);
+              uint32_t pk[NP][8];
+              act_pack_32<ACT, H, NMASK, FOLD, NP, 16>(cur, 16 * qt, t.lscale[l], t.bias[l], pk);
+#pragma unroll
+              for (int part = 0; part < NPT; ++part)
+                tc::tmem_st_32x32b_x8(a_t + 32u * part + lane_off + 8u * qt, pk[part]);
+              if constexpr (AS) st_a_row<8>(a_row, a_r7, 2 * qt, pk[NP - 1]);
+              if (qt + 1 < NQ) tc::wait_ld();
+            }
+          } else if constexpr (QUARTERS) {
             // 16 columns at a time (fewer live registers: more pairs of the epilogue in flight); the
             // quarters past the last unit (and its 3 bias columns) are not loaded
 #pragma unroll
@@ -451,13 +484,10 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
                 tc::wait_ld();
                 uint32_t pk[NP][8];
                 act_pack_32<ACT, H, NMASK, FOLD, NP, 16>(v, 16 * qt, t.lscale[l], t.bias[l], pk);
-                if constexpr (AS) {
-                  st_a_row<8>(a_row, a_r7, 2 * qt, pk[0]);
-                } else {
 #pragma unroll
-                  for (int part = 0; part < NP; ++part)
-                    tc::tmem_st_32x32b_x8(a_t + 32u * part + lane_off + 8u * qt, pk[part]);
-                }
+                for (int part = 0; part < NPT; ++part)
+                  tc::tmem_st_32x32b_x8(a_t + 32u * part + lane_off + 8u * qt, pk[part]);
+                if constexpr (AS) st_a_row<8>(a_row, a_r7, 2 * qt, pk[NP - 1]);
               }
             }
           } else {
@@ -473,18 +503,15 @@ __global__ void __launch_bounds__(NG * kGroupThreads, 1)
             } else {
               uint32_t pk[NP][16];
               act_pack_32<ACT, H, NMASK, FOLD, NP>(v, 32 * half, t.lscale[l], t.bias[l], pk);
-              if constexpr (AS) {
-                st_a_row<16>(a_row, a_r7, 4 * half, pk[0]);
-              } else {
 #pragma unroll
-                for (int part = 0; part < NP; ++part)
-                  tc::tmem_st_32x32b_x16(a_t + 32u * part + lane_off + 16u * half, pk[part]);
-              }
+              for (int part = 0; part < NPT; ++part)
+                tc::tmem_st_32x32b_x16(a_t + 32u * part + lane_off + 16u * half, pk[part]);
+              if constexpr (AS) st_a_row<16>(a_row, a_r7, 4 * half, pk[NP - 1]);
             }
           }
           }
           if constexpr (AS) tc::fence_proxy_async_smem();
-          else tc::wait_st();
+          if constexpr (NPT > 0 || TF32) tc::wait_st();
         } else {
           uint32_t v[16];
           tc::tmem_ld_32x32b_x16(acc_t + lane_off, v);
@@ -599,6 +626,10 @@ cudaError_t launch_softplus_bf16(const RunParams& p, const TcParams& t, cudaStre
     case 37: return launch_tc_t<kTcGroupsSoftplus, 50, 7, false, kActSoftplusPair, 0x15Fu, 1, true>(p, t, st, num_sms);
     case 38: return launch_tc_t<4, 50, 7, false, kActSoftplusPair, 0x15Fu>(p, t, st, num_sms);
     // A operand in shared memory: 64 TMEM columns per tile, 6 / 7 tile groups per SM
+    case 48: return launch_sp_pair<0x75Fu>(p, t, st, num_sms);   // pipelined quarters
+    case 49: return launch_sp_pair<0x777u>(p, t, st, num_sms);
+    case 50: return launch_sp_pair<0x77Fu>(p, t, st, num_sms);
+    case 51: return launch_sp_pair<0x71Fu>(p, t, st, num_sms);
     case 39: return launch_tc_t<6, 50, 7, false, kActSoftplusPair, 0x15Fu, 1, false, false, true>(p, t, st, num_sms);
     case 44: return launch_tc_t<7, 50, 7, false, kActSoftplusPair, 0x15Fu, 1, false, false, true>(p, t, st, num_sms);
     case 45: return launch_tc_t<5, 50, 7, false, kActSoftplusPair, 0x15Fu, 1, false, false, true>(p, t, st, num_sms);
@@ -635,6 +666,20 @@ cudaError_t launch_accurate(const RunParams& p, const TcParams& t, cudaStream_t 
                          : launch_pairs<NG, kActSoftplusPairS, 0xFFu, NP, TF32>(p, t, st, num_sms);
     case 43: return tanh ? launch_pairs<NG, kActTanhPair, 0x5Fu, NP, TF32>(p, t, st, num_sms)
                          : launch_pairs<NG, kActSoftplusPairS, 0x5Fu, NP, TF32>(p, t, st, num_sms);
+    case 55:   // SPLIT with the lo part in shared memory: 96 TMEM columns per group, 5 groups
+      if constexpr (NP == 2 && !TF32) {
+        if (p.width == 50 && p.m == 7)
+          return tanh ? launch_tc_t<5, 50, 7, false, kActTanhPair, kSplitTanhMask, 2, false, false, true>(p, t, st, num_sms)
+                      : launch_tc_t<5, 50, 7, false, kActSoftplusPairS, kSplitSoftplusMask, 2, false, false, true>(p, t, st, num_sms);
+      }
+      break;
+    case 56:   // the same with 4 groups (the cost of the shared-memory part alone)
+      if constexpr (NP == 2 && !TF32) {
+        if (p.width == 50 && p.m == 7)
+          return tanh ? launch_tc_t<4, 50, 7, false, kActTanhPair, kSplitTanhMask, 2, false, false, true>(p, t, st, num_sms)
+                      : launch_tc_t<4, 50, 7, false, kActSoftplusPairS, kSplitSoftplusMask, 2, false, false, true>(p, t, st, num_sms);
+      }
+      break;
     default: break;
   }
 #endif
