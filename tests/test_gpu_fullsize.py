@@ -142,3 +142,41 @@ def test_cfg1_strong_error_flat_in_steps(gpu_lib, prec, bound):
         err[n] = sl7.stats_summary(st.cpu().numpy(), opts)["strong_err"]
     print(prec, "strong error by n:", err)
     assert max(err.values()) < bound
+
+
+def test_cfg4_full_size(gpu_lib):
+    """cfg4 (the bench headline): all 4e9 paths in one STATS call, the launch bench.py times (BF16 tcgen05,
+    4096-bin histogram): every path counted and finite, terminal mean / variance within 0.5% / 2% of the CIR
+    law; then the top of the path range (the last 65,536 paths through path_offset, FULL output) teacher-forced
+    against O6 on sampled paths, so the paths the strong-scaling shards end on are checked too."""
+    sl7 = gpu_lib
+    torch = _torch()
+    w = workloads()["cfg4"]
+    N = w.n_paths
+    blob = load_golden_blob(w.blob)
+    ctx = sl7.Context(w.m, list(w.dims), w.act)
+    ctx.load_weights(blob)
+    st = torch.zeros(sl7.stats_elems(4096), dtype=torch.float64, device="cuda")
+    opts = sl7.make_opts(prec=sl7.PREC_BF16, colloc=sl7.COLLOC_ANN, n_bins=4096, hist_lo=0.0, hist_hi=0.8, shift=0.1)
+    ctx.simulate(w.y0, w.dt, w.n_steps, w.theta, N, w.seed, sl7.OUT_STATS, opts, stats=st)
+    torch.cuda.synchronize()
+    v = st.cpu().numpy()
+    assert v[0] == N and v[1] == 0
+    s = sl7.stats_summary(v, opts)
+    k, yb, sg = w.theta
+    e = np.exp(-k * w.T)
+    law_m = w.y0 * e + yb * (1 - e)
+    law_v = w.y0 * sg * sg / k * (e - e * e) + yb * sg * sg / (2 * k) * (1 - e) ** 2
+    print("cfg4 4e9 paths: mean %.6f (law %.6f) var %.6g (law %.6g)" % (s["mean"], law_m, s["var"], law_v))
+    assert abs(s["mean"] / law_m - 1) < 5e-3 and abs(s["var"] / law_v - 1) < 2e-2
+    n_top = 65536
+    off = N - n_top
+    o = sl7.make_opts(prec=sl7.PREC_BF16, colloc=sl7.COLLOC_ANN, path_offset=off)
+    full, _ = ctx.simulate(w.y0, w.dt, w.n_steps, w.theta, n_top, w.seed, sl7.OUT_FULL, o)
+    torch.cuda.synchronize()
+    ids = _sample_ids(n_top, 800)
+    rows = full.view(w.n_steps + 1, n_top)[:, torch.as_tensor(ids, device="cuda")].double().cpu().numpy()
+    spec = O.Spec(w.m, "ann", tuple(w.theta), w.y0, w.dt, w.n_steps, net=O.parse_blob(blob), quant="bf16")
+    Z = O.normals(w.seed, (off + ids).astype(np.uint64), w.n_steps)
+    worst = _teacher_forced_sample(spec, rows, off + ids, w.seed, 5e-3, Z=Z)
+    print("cfg4 top-of-range bf16 sampled worst |err|/kappa = %.3g" % worst)
