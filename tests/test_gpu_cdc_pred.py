@@ -214,3 +214,24 @@ def test_cdc_pred_host_entry_points_equal_simulate(gpu_lib, entry):
             ctx.simulate_host_async(y0, dt, ns, th, n, 5, sl7.OUT_FULL, o, h_out=h)
             ctx.sync()
         assert np.array_equal(h, want.cpu().numpy())
+
+
+@pytest.mark.parametrize("case", [CASES[0], CASES[2]], ids=["fused_m7", "per_step_m6"])
+def test_cdc_pred_clamp_count_both_launch_paths(gpu_lib, case):
+    # stats E1 of CDC_PRED = clamped path-steps, from the fused kernel (m = 7) and from the per-step launches
+    # (m = 6, counts added into the stats vector after every step) against the oracle's count
+    import torch
+    sl7 = gpu_lib
+    name, m, colloc, theta, y0, dt, n_steps = case
+    ctx, code, th, spec = _setup(sl7, name, m, colloc, theta, y0, dt, n_steps)
+    n = 20_000
+    out, _ = ctx.simulate(spec.y0, spec.dt, n_steps, th, n, 13, sl7.OUT_FULL,
+                          sl7.make_opts(colloc=code, scheme=sl7.SCHEME_CDC_PRED))
+    st = torch.zeros(sl7.stats_elems(0), dtype=torch.float64, device="cuda")
+    ctx.simulate(spec.y0, spec.dt, n_steps, th, n, 13, sl7.OUT_STATS,
+                 sl7.make_opts(colloc=code, scheme=sl7.SCHEME_CDC_PRED, shift=spec.y0), stats=st)
+    torch.cuda.synchronize()
+    Yd = out.double().cpu().numpy().reshape(n_steps + 1, n)
+    nd, no = st[6].item(), O.cdc_pred_clamped(spec, Yd)   # the oracle counts on the device's own states
+    print("%s clamped path-steps: device %d oracle %d" % (name, nd, no))
+    assert no > 0 and abs(nd - no) <= 2
