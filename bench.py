@@ -402,6 +402,12 @@ def ann_roofline(dims, prec, rate, sl7, peaks, n_sms, sm_max):
          "tensor": {"achieved": mma, "peak": tpk, "unit": "TFLOP/s", "frac": mma / tpk,
                     "basis": "%d MMA FLOP per path-step vs MEASURED_PEAKS.json bf16_tflops%s" % (
                         flops - 2 * dims[1], " x 1/2 (tf32:bf16 nominal ratio)" if prec == sl7.PREC_TF32 else "")}}
+    if prec in (sl7.PREC_TF32, sl7.PREC_SPLIT):
+        # the fp32-class modes need an activation accurate to ~1e-7, which one MUFU op does not give (MUFU.TANH:
+        # 1e-5): on the XU pipe alone that is two ops per unit (ex2 + rcp / ex2 + lg2), SURVEY §8(d)'s
+        # "accurate" XU bound; the kernels move part of the second op to the FMA pipe
+        r["accurate_activation_bound"] = {"ops_per_activation": 2, "peak_path_steps_per_s": pk * 1e12 / (2 * act),
+                                          "frac": 2 * ach / pk}
     return r
 
 
