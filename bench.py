@@ -503,6 +503,7 @@ def run_modes(sl7, torch, dev, stream, peaks, n_sms, sm_max):
         out["%s_cdc_pred" % key] = {"path_steps_per_s": rate, "ms": ms, "paths": N, "n_steps": w.n_steps,
                                     "scheme": "7L-CDC with predicted marginal points (DESIGN.md R-26)",
                                     "terminal": {"mean": s["mean"], "var": s["var"]},
+                                    "clamped_path_steps": s.get("clamped_steps"),
                                     "roofline": issue_roof(rate, cdc_pred_instr(w.m),
                                                            "Philox/4 + Box-Muller + table interpolation in the state "
                                                            "+ g_m"), "clocks": clk}
