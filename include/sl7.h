@@ -228,7 +228,13 @@ sl7_status sl7_simulate_host_async(sl7_ctx ctx, double Y0, double dt, int32_t n_
 sl7_status sl7_sync(sl7_ctx ctx);
 
 /* Moments, strong error and quantiles from a HOST copy of a stats vector (which the caller may
- * have all-reduced across ranks first).  opts supplies shift, hist_lo, hist_hi, n_bins.
+ * have all-reduced across ranks first).  Algorithm I step 7 collects the paths at each t_i into "a complete
+ * set"; the distribution of that set at T and its path-wise error against the exact solution
+ * on the same normals (Eq. 6.6, "used to compute the reference value to the path-wise error and the strong
+ * convergence") are what this summarises: population mean / variance / skew / excess
+ * kurtosis from the shifted power sums, strong error E1 / n and RMS sqrt(E2 / n), and quantiles by linear
+ * interpolation of the histogram CDF.  opts supplies shift, hist_lo, hist_hi, n_bins (and scheme: see
+ * SL7_SCHEME_CDC_PRED for the E1 slot of that scheme).
  * Returns SL7_ENONFINITE (after filling *out) if n_nonfinite > 0; SL7_EINVAL if n == 0. */
 sl7_status sl7_stats(const double* h_stats, const sl7_run_opts* opts, sl7_summary* out);
 
