@@ -2,11 +2,13 @@
 //
 // Algorithm I steps 3-8 for tiles of 128 paths, all n_steps inside one launch:
 //   layer 1 (rank 1 in Y after folding dt, theta)     : FFMA + activation, fp32, CUDA cores
-//   hidden layers 2..L and the output layer            : tcgen05.mma kind::f16, bf16 x bf16 -> fp32
-//                                                        [128 paths x 64] x [64 x 64] (output: x 16)
-//   bias + activation epilogue                         : tcgen05.ld -> MUFU.TANH (tanh) or ex2 + lg2
-//                                                        (softplus) -> bf16 -> tcgen05.st
-//   Philox/Box-Muller normal, barycentric g_m, store   : CUDA cores, as in the fp32 kernels
+//   hidden layers 2..L and the output layer            : tcgen05.mma kind::f16 (BF16: bf16 x bf16; SPLIT: three
+//                                                        fp16 products of two-part operands) or kind::tf32,
+//                                                        fp32 accumulate; [128 paths x 64] x [64 x 64] (output x 16)
+//   bias + activation epilogue                         : tcgen05.ld -> MUFU.TANH (BF16 tanh), softplus pairs on
+//                                                        MUFU ex2 + FFMA2 log1p polynomial / MUFU lg2, or the
+//                                                        accurate FFMA2 pairs (SPLIT, TF32) -> pack -> tcgen05.st
+//   Philox/Box-Muller normal, barycentric g_m, stats   : CUDA cores, as in the fp32 kernels
 //
 // CTA = NG independent "tile groups" of 4 warps (128 threads).  Thread t of a group owns path t of
 // the group's current tile AND TMEM lane t: the MMA's M dimension is the path index, so every
@@ -16,9 +18,11 @@
 // signalled by tcgen05.commit), the other groups run their MUFU-bound epilogues, which is where the
 // time goes (the XU pipe binds, the tensor pipe has >= 5x slack).
 //
-// TMEM per group (128 columns): [0,64) hidden accumulator fp32, [64,80) output accumulator fp32,
-// [96,128) A operand (64 bf16 packed two per 32-bit column).  Shared memory: bf16 weight tiles in the
-// SWIZZLE_128B K-major layout (staged once per CTA), the histogram, barriers.
+// TMEM per group: [0,64) hidden accumulator fp32 (the [128 x 16] output accumulator reuses [0,16)), then the
+// A operand: BF16 [64,96) (64 bf16 packed two per 32-bit column) -> 96 columns, 5 groups per SM; SPLIT two
+// fp16 parts [64,128) and TF32 64 columns -> 128 columns, 4 groups.  Shared memory: the weight tiles in the
+// SWIZZLE_128B K-major layout (staged once per CTA), the histogram, the per-thread statistics, barriers.
+// (Experiment builds also hold the AS variants: the A operand, or SPLIT's lo part, in shared memory.)
 #include <cuda_runtime.h>
 
 #include "sl7_device.cuh"
