@@ -67,6 +67,15 @@ def exact_special_instr():
 
 
 def cdc_pred_instr(m):
+    # the 7L-CDC step with predicted marginal points as ONE bivariate polynomial of degree m-1 in the clamped,
+    # normalised state and in X (the same interpolant as the table-then-g_m form, R-26): m(m-1) + (m-1)
+    # FMA, the clamp (2) and the state normalisation (1)
+    return PHILOX_PER_NORMAL + BOX_MULLER_PER_NORMAL + m * (m - 1) + (m - 1) + 3
+
+
+def cdc_pred_instr_lagrange(m):
+    # the same step in the Lagrange forms of PAPER.md:106 / R-19: the basis in the state, the m x m contraction,
+    # g_m at X
     return PHILOX_PER_NORMAL + BOX_MULLER_PER_NORMAL + gm_instr(m) + m * m + gm_instr(m) + 2
 
 
@@ -505,8 +514,10 @@ def run_modes(sl7, torch, dev, stream, peaks, n_sms, sm_max):
                                     "terminal": {"mean": s["mean"], "var": s["var"]},
                                     "clamped_path_steps": s.get("clamped_steps"),
                                     "roofline": issue_roof(rate, cdc_pred_instr(w.m),
-                                                           "Philox/4 + Box-Muller + table interpolation in the state "
-                                                           "+ g_m"), "clocks": clk}
+                                                           "Philox/4 + Box-Muller + clamp + the step as one bivariate "
+                                                           "polynomial in (state, X)"),
+                                    "frac_vs_lagrange_form_budget": rate * cdc_pred_instr_lagrange(w.m) / issue_peak,
+                                    "clocks": clk}
         if w.process == "ou":
             exo = sl7.Context(w.m, device=dev.index)
             o = sl7.make_opts(prec=sl7.PREC_FP32, colloc=sl7.COLLOC_EXACT_OU, stream=stream, n_bins=N_BINS,

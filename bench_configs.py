@@ -278,7 +278,7 @@ def main():
                         "quantiles_1_50_99": s["quantiles"], "clocks": clk.summary()}
                 if flags == -3:
                     # fused CDC_PRED kernel: issue-bound; algorithmic budget (bench.cdc_pred_instr): Philox/4 +
-                    # Box-Muller + the table basis at the state + the m x m contraction + g_m at X_hat + clamp
+                    # Box-Muller + clamp + the step as one bivariate polynomial (m(m-1) + m-1 FMA)
                     instr = cdc_pred_instr(w.m)
                     ach = rate * instr
                     line["roofline"] = {"bound": "alu", "pipe": "issue", "achieved": ach / 1e12,

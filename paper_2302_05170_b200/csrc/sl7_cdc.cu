@@ -16,6 +16,7 @@
 // + 1 write of 4 bytes.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "sl7_device.cuh"
@@ -40,11 +41,19 @@ struct CdcScratch {
 };
 
 // One step's CDC_PRED table (the fused kernel stages all steps' tables; same fields as CdcScratch's).
+// kCdcBiv: the fused CDC_PRED kernel evaluates a step as ONE bivariate polynomial (m <= kCdcBiv)
+constexpr int kCdcBiv = 8;
 struct CdcTable {
   float z[kMaxM], zlo[kMaxM], v[kMaxM], C[kMaxM][kMaxM];
   float sinv;
   int degenerate;
   double zd[kMaxM];
+  // Y' = sum_j l_j(X) sum_k L_k(Yb) C[k][j] (g_m of the table interpolated at the clamped state, R-19/R-26) is a
+  // polynomial of degree m-1 in each of s = (Yb - c) / h (c, h: centre and half-width of the hull) and X:
+  // Y' = sum_a sum_b D[a][b] s^a X^b with D = A^T C B, A / B the monomial coefficients of the Lagrange bases
+  // on the s-nodes of the z_k and on the Gauss-Hermite nodes (built in double by the table kernel)
+  float D[kCdcBiv][kCdcBiv];
+  float shinv, sc;   // s = Yb * shinv + sc
 };
 
 // From the double marginal points s->zd[0..m): the fp32 hi/lo split, the scaled barycentric weights and
@@ -362,6 +371,52 @@ __global__ void __launch_bounds__(256) cdc_table_mlp_kernel(const __grid_constan
 // SL7_SCHEME_CDC_PRED (reading R-26): the marginal collocation points of Y(t_i) are the predictor's at
 // (Y0, t_i = i dt, theta) -- the horizon's folded constants hz -- instead of quantiles of the paths
 // (t_0: every path at Y0, a degenerate table); then the table rows as above.  One block.
+// Monomial coefficients of the Lagrange basis on n[0..m): A[k][a] = coefficient of t^a in
+// prod_{k' != k} (t - n_k') / (n_k - n_k'), in double (one thread).
+__device__ void lagrange_monomial(const double* n, int m, double (*A)[kCdcBiv]) {
+  for (int k = 0; k < m; ++k) {
+    double q[kCdcBiv] = {1.0};
+    double den = 1.0;
+    int deg = 0;
+    for (int k2 = 0; k2 < m; ++k2) {
+      if (k2 == k) continue;
+      for (int a = deg + 1; a >= 0; --a) q[a] = (a > 0 ? q[a - 1] : 0.0) - n[k2] * (a <= deg ? q[a] : 0.0);
+      ++deg;
+      den *= n[k] - n[k2];
+    }
+    for (int a = 0; a < m; ++a) A[k][a] = q[a] / den;
+  }
+}
+
+// D = A^T C B of the step's table (CdcTable::D); skipped for repeated / unordered points (nearest-row rule)
+__device__ void cdc_bivariate(const RunParams& p, CdcTable* s, int m) {
+  if (s->degenerate) return;
+  const double c = 0.5 * (s->zd[0] + s->zd[m - 1]), h = 0.5 * (s->zd[m - 1] - s->zd[0]);
+  double sn[kCdcBiv], xn[kCdcBiv], A[kCdcBiv][kCdcBiv], B[kCdcBiv][kCdcBiv];
+  for (int k = 0; k < m; ++k) {
+    sn[k] = (s->zd[k] - c) / h;
+    xn[k] = (double)p.xhi[k] + (double)p.xlo[k];
+  }
+  lagrange_monomial(sn, m, A);
+  lagrange_monomial(xn, m, B);
+  double CB[kCdcBiv][kCdcBiv];
+  for (int k = 0; k < m; ++k)
+    for (int b = 0; b < m; ++b) {
+      double a = 0.0;
+      for (int j = 0; j < m; ++j) a += (double)s->C[k][j] * B[j][b];
+      CB[k][b] = a;
+    }
+  for (int a = 0; a < kCdcBiv; ++a)
+    for (int b = 0; b < kCdcBiv; ++b) {
+      double v = 0.0;
+      if (a < m && b < m)
+        for (int k = 0; k < m; ++k) v += A[k][a] * CB[k][b];
+      s->D[a][b] = (float)v;
+    }
+  s->shinv = (float)(1.0 / h);
+  s->sc = (float)(-c / h);
+}
+
 template <int ACT, class T>
 __device__ void cdc_pred_table_body(const RunParams& p, const CdcHorizon& hz, T* s, int step) {
   __shared__ float zr[1][kMaxM];
@@ -391,6 +446,10 @@ __device__ void cdc_pred_table_body(const RunParams& p, const CdcHorizon& hz, T*
       const float zk = s->z[k];
       s->C[k][j] = (p.colloc == kExactGbm) ? zk * p.c[j] : fmaf(p.ou_a, zk, p.ou_b) + p.c[j];
     }
+  }
+  if constexpr (sizeof(T) == sizeof(CdcTable)) {
+    __syncthreads();
+    if (threadIdx.x == 0 && m <= kCdcBiv) cdc_bivariate(p, s, m);
   }
 }
 
@@ -540,8 +599,9 @@ __global__ void __launch_bounds__(256) cdc_step_kernel(const __grid_constant__ R
 template <int MR>
 struct CdcSTab {
   float C[MR][MR];
+  float D[MR][MR];   // the step as a bivariate polynomial (CdcTable::D)
   float z[MR], v[MR];
-  float sinv;
+  float sinv, shinv, sc;
   int deg;
 };
 constexpr int kCdcFusedP = 4;
@@ -590,7 +650,7 @@ __device__ __forceinline__ float cdc_pred_path_step(const RunParams& p, const Cd
   return gm_eval<MR, false>(p, Z, y);
 }
 
-template <int MR, bool FAST>
+template <int MR, bool FAST, bool BIV = true>
 __global__ void __launch_bounds__(256, 2) cdc_pred_fused_kernel(const __grid_constant__ RunParams p,
                                                              const CdcTable* __restrict__ tabs, float* __restrict__ out) {
   constexpr int P = kCdcFusedP;
@@ -602,6 +662,7 @@ __global__ void __launch_bounds__(256, 2) cdc_pred_fused_kernel(const __grid_con
   for (int i = threadIdx.x; i < n * MR * MR; i += blockDim.x) {
     const int t = i / (MR * MR), r = i % (MR * MR);
     st[t].C[r / MR][r % MR] = tabs[t].C[r / MR][r % MR];
+    st[t].D[r / MR][r % MR] = tabs[t].D[r / MR][r % MR];
   }
   for (int i = threadIdx.x; i < n * MR; i += blockDim.x) {
     const int t = i / MR, k = i % MR;
@@ -610,6 +671,8 @@ __global__ void __launch_bounds__(256, 2) cdc_pred_fused_kernel(const __grid_con
   }
   for (int t = threadIdx.x; t < n; t += blockDim.x) {
     st[t].sinv = tabs[t].sinv;
+    st[t].shinv = tabs[t].shinv;
+    st[t].sc = tabs[t].sc;
     st[t].deg = tabs[t].degenerate;
   }
   hist_init(p, hist);
@@ -649,6 +712,35 @@ __global__ void __launch_bounds__(256, 2) cdc_pred_fused_kernel(const __grid_con
         const int i = i0 + r;
         if (i >= n) break;
         const CdcSTab<MR>& T = st[i];
+        if (BIV && !T.deg) {
+          // Y' = sum_b X^b P_b(s), P_b(s) = sum_a D[a][b] s^a: two paths per FFMA2 with D broadcast
+          const float zlo = T.z[0], zhi = T.z[MR - 1], shinv = T.shinv, sc = T.sc;
+#pragma unroll
+          for (int u = 0; u < P; u += 2) {
+            float Zp[2], Sp[2];
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const float Yv = Y[u + v];
+              Zp[v] = (r == 0) ? zn[u + v][0] : (r == 1) ? zn[u + v][1] : (r == 2) ? zn[u + v][2] : zn[u + v][3];
+              const float Yb = (Yv < zlo) ? zlo : (Yv > zhi) ? zhi : Yv;   // hull clamp (R-26); NaN stays
+              ncl += (ok[u + v] && (Yv < zlo || Yv > zhi)) ? 1u : 0u;
+              Sp[v] = fmaf(Yb, shinv, sc);
+            }
+            const uint64_t S = pk2(Sp[0], Sp[1]), X = pk2(Zp[0], Zp[1]);
+            uint64_t acc = 0;
+#pragma unroll
+            for (int b = MR - 1; b >= 0; --b) {
+              uint64_t q = pk2(T.D[MR - 1][b], T.D[MR - 1][b]);
+#pragma unroll
+              for (int a = MR - 2; a >= 0; --a) q = fma2(q, S, pk2(T.D[a][b], T.D[a][b]));
+              acc = (b == MR - 1) ? q : fma2(acc, X, q);
+            }
+            up2(acc, Y[u], Y[u + 1]);
+#pragma unroll
+            for (int v = 0; v < 2; ++v)
+              if (full && ok[u + v]) out[(uint64_t)(i + 1) * N + base + (uint64_t)(u + v) * blockDim.x + threadIdx.x] = Y[u + v];
+          }
+        } else {
         float Cr[MR][MR], zr[MR], vr[MR];
 #pragma unroll
         for (int k = 0; k < MR; ++k) {
@@ -665,6 +757,7 @@ __global__ void __launch_bounds__(256, 2) cdc_pred_fused_kernel(const __grid_con
           Y[u] = cdc_pred_path_step<MR, FAST>(p, T, Cr, zr, vr, sinv, Y[u], Z, c);
           ncl += ok[u] ? c : 0u;
           if (full && ok[u]) out[(uint64_t)(i + 1) * N + base + (uint64_t)u * blockDim.x + threadIdx.x] = Y[u];
+        }
         }
       }
     }
@@ -808,6 +901,12 @@ int launch_cdc_pred(const RunParams& p, const CdcHorizon* hz, void* scratch, flo
     const bool fast = p.flags & SL7_FLAG_FAST_NORMALS;
     auto k = (p.m == 5) ? (fast ? cdc_pred_fused_kernel<5, true> : cdc_pred_fused_kernel<5, false>)
                         : (fast ? cdc_pred_fused_kernel<7, true> : cdc_pred_fused_kernel<7, false>);
+#ifdef SL7_AB_HOOKS
+    if (const char* v = std::getenv("SL7_TC_VARIANT"))
+      if (std::atoi(v) == 70)   // the r01/r02 step: conditional points by Lagrange in the state, then g_m
+        k = (p.m == 5) ? (fast ? cdc_pred_fused_kernel<5, true, false> : cdc_pred_fused_kernel<5, false, false>)
+                       : (fast ? cdc_pred_fused_kernel<7, true, false> : cdc_pred_fused_kernel<7, false, false>);
+#endif
     const size_t tab = (p.m == 5 ? sizeof(CdcSTab<5>) : sizeof(CdcSTab<7>)) * (size_t)p.n_steps;
     const size_t smem = tab + ((p.has_stats && p.n_bins > 0) ? sizeof(uint32_t) * (size_t)(p.n_bins + 2) : 0);
     const cudaError_t ce = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -138,7 +138,7 @@ struct CdcHorizon {
 int launch_cdc_pred(const RunParams& p, const CdcHorizon* hz, void* scratch, float* const* rows, int nrows,
                     void* stream, int num_sms, void* tables);
 size_t cdc_table_bytes();
-constexpr int kCdcFusedMaxSteps = 256;
+constexpr int kCdcFusedMaxSteps = 160;   // 160 x 464 B of step tables + the histogram: 2 CTAs per SM
 size_t cdc_scratch_bytes();
 int cdc_init_scratch(void* scratch, void* stream);
 // rows: nrows == 1 -> one in-place state buffer; nrows == n_steps + 1 -> FULL output rows.
