@@ -25,7 +25,7 @@ opts = sl7.make_opts(prec=sl7.PREC_FP32, colloc=sl7.COLLOC_ANN, scheme=scheme, n
                      hist_hi=3.0, shift=w.y0)
 ctx.simulate(w.y0, w.dt, w.n_steps, w.theta, N, w.seed, sl7.OUT_STATS, opts, stats=st)
 torch.cuda.synchronize()
-reps = int(os.environ.get("CDC_PROBE_REPS", "0"))   # > 0: also time that many launches (CUDA events)
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else int(os.environ.get("CDC_PROBE_REPS", "0"))   # > 0: time them
 ms = []
 for _ in range(reps):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -1,6 +1,6 @@
 #!/bin/bash
 # GPU-box driver for the round-2 ncu captures of the current kernels (one process, one GPU each):
-#   bash profiles/gpu_prof.sh TAG [which...]   which: cfg4 split fp32 cfg3 tf32 (default: all)
+#   bash profiles/gpu_prof.sh TAG [which...]   which: cfg4 split fp32 cfg3 tf32 cdcpred (default: cfg4 split fp32 cfg3 tf32)
 # Writes gpurun_out/TAG_<which>.ncu-rep plus the raw and source pages as CSV (read here with summarize.py).
 T=${1:-prof}; shift
 W=${@:-cfg4 split fp32 cfg3 tf32}
@@ -14,6 +14,7 @@ for w in $W; do
     tf32)  K=regex:ann_tc_step_kernel;  CMD="python profiles/ann_probe.py cfg1 tf32 10000000 1" ;;
     fp32)  K=regex:ann_f32; CMD="python profiles/ann_probe.py cfg1 fp32 4000000 1" ;;
     cfg3)  K=regex:exact_full4_kernel;  CMD="python profiles/exact_probe.py 50000000 1" ;;
+    cdcpred) K=regex:cdc_pred_fused;    CMD="python profiles/cdc_probe.py 20000000 pred 1" ;;
   esac
   timeout 600 $NCU -k $K -s 1 -c 1 -o $O/${T}_$w -f $CMD > $O/${T}_$w.log 2>&1
   echo "$w ncu rc=$?"
