@@ -650,7 +650,7 @@ __device__ __forceinline__ float cdc_pred_path_step(const RunParams& p, const Cd
   return gm_eval<MR, false>(p, Z, y);
 }
 
-template <int MR, bool FAST, bool BIV = true>
+template <int MR, bool FAST, bool BIV = true, bool ESTRIN = false>
 __global__ void __launch_bounds__(256, 2) cdc_pred_fused_kernel(const __grid_constant__ RunParams p,
                                                              const CdcTable* __restrict__ tabs, float* __restrict__ out) {
   constexpr int P = kCdcFusedP;
@@ -728,12 +728,38 @@ __global__ void __launch_bounds__(256, 2) cdc_pred_fused_kernel(const __grid_con
             }
             const uint64_t S = pk2(Sp[0], Sp[1]), X = pk2(Zp[0], Zp[1]);
             uint64_t acc = 0;
+            if constexpr (ESTRIN) {
+              // the same polynomial in Estrin's order (pairs (c_2i + c_2i+1 t), then powers t^2, t^4): the same
+              // FMA count as Horner, a dependence chain of ~log2(m) + 1 instead of m - 1
+              const uint64_t z0 = pk2(0.0f, 0.0f);
+              const uint64_t S2 = fma2(S, S, z0), X2 = fma2(X, X, z0);
+              uint64_t P[MR];
+#pragma unroll
+              for (int b = 0; b < MR; ++b) {
+                uint64_t e[(MR + 1) / 2];
+#pragma unroll
+                for (int i = 0; i < (MR + 1) / 2; ++i)
+                  e[i] = (2 * i + 1 < MR) ? fma2(S, pk2(T.D[2 * i + 1][b], T.D[2 * i + 1][b]), pk2(T.D[2 * i][b], T.D[2 * i][b]))
+                                          : pk2(T.D[2 * i][b], T.D[2 * i][b]);
+                uint64_t q = e[(MR + 1) / 2 - 1];
+#pragma unroll
+                for (int i = (MR + 1) / 2 - 2; i >= 0; --i) q = fma2(q, S2, e[i]);
+                P[b] = q;
+              }
+              uint64_t f[(MR + 1) / 2];
+#pragma unroll
+              for (int i = 0; i < (MR + 1) / 2; ++i) f[i] = (2 * i + 1 < MR) ? fma2(X, P[2 * i + 1], P[2 * i]) : P[2 * i];
+              acc = f[(MR + 1) / 2 - 1];
+#pragma unroll
+              for (int i = (MR + 1) / 2 - 2; i >= 0; --i) acc = fma2(acc, X2, f[i]);
+            } else {
 #pragma unroll
             for (int b = MR - 1; b >= 0; --b) {
               uint64_t q = pk2(T.D[MR - 1][b], T.D[MR - 1][b]);
 #pragma unroll
               for (int a = MR - 2; a >= 0; --a) q = fma2(q, S, pk2(T.D[a][b], T.D[a][b]));
               acc = (b == MR - 1) ? q : fma2(acc, X, q);
+            }
             }
             up2(acc, Y[u], Y[u + 1]);
 #pragma unroll
@@ -906,6 +932,9 @@ int launch_cdc_pred(const RunParams& p, const CdcHorizon* hz, void* scratch, flo
       if (std::atoi(v) == 70)   // the r01/r02 step: conditional points by Lagrange in the state, then g_m
         k = (p.m == 5) ? (fast ? cdc_pred_fused_kernel<5, true, false> : cdc_pred_fused_kernel<5, false, false>)
                        : (fast ? cdc_pred_fused_kernel<7, true, false> : cdc_pred_fused_kernel<7, false, false>);
+      else if (std::atoi(v) == 71)   // Estrin order
+        k = (p.m == 5) ? (fast ? cdc_pred_fused_kernel<5, true, true, true> : cdc_pred_fused_kernel<5, false, true, true>)
+                       : (fast ? cdc_pred_fused_kernel<7, true, true, true> : cdc_pred_fused_kernel<7, false, true, true>);
 #endif
     const size_t tab = (p.m == 5 ? sizeof(CdcSTab<5>) : sizeof(CdcSTab<7>)) * (size_t)p.n_steps;
     const size_t smem = tab + ((p.has_stats && p.n_bins > 0) ? sizeof(uint32_t) * (size_t)(p.n_bins + 2) : 0);
