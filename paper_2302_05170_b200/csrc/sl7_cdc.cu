@@ -18,6 +18,7 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "sl7_device.cuh"
 
@@ -447,7 +448,7 @@ __device__ void cdc_pred_table_body(const RunParams& p, const CdcHorizon& hz, T*
       s->C[k][j] = (p.colloc == kExactGbm) ? zk * p.c[j] : fmaf(p.ou_a, zk, p.ou_b) + p.c[j];
     }
   }
-  if constexpr (sizeof(T) == sizeof(CdcTable)) {
+  if constexpr (std::is_same<T, CdcTable>::value) {   // the fused kernel's tables (not the per-step scratch)
     __syncthreads();
     if (threadIdx.x == 0 && m <= kCdcBiv) cdc_bivariate(p, s, m);
   }
