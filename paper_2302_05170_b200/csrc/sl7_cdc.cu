@@ -25,6 +25,9 @@
 namespace sl7 {
 
 // Device-side scratch of the CDC pipeline (context-owned).
+// kCdcBiv: tables of m <= kCdcBiv also carry the step as ONE bivariate polynomial (CdcTable::D below)
+constexpr int kCdcBiv = 8;
+
 struct CdcScratch {
   unsigned long long hist[kCdcMaxT][256];   // per-slot digit histograms of the current pass
   unsigned long long rank[kCdcMaxT];        // residual rank of each target within its prefix
@@ -39,11 +42,11 @@ struct CdcScratch {
   float sinv;   // 1 / half-range of the z_k: the interpolation works on (Y - z_k) * sinv (no fp32 under/overflow)
   int degenerate;
   double zd[kMaxM];
+  float D[kCdcBiv][kCdcBiv];   // the step as a bivariate polynomial, as CdcTable::D
+  float shinv, sc;
 };
 
 // One step's CDC_PRED table (the fused kernel stages all steps' tables; same fields as CdcScratch's).
-// kCdcBiv: the fused CDC_PRED kernel evaluates a step as ONE bivariate polynomial (m <= kCdcBiv)
-constexpr int kCdcBiv = 8;
 struct CdcTable {
   float z[kMaxM], zlo[kMaxM], v[kMaxM], C[kMaxM][kMaxM];
   float sinv;
@@ -312,12 +315,62 @@ __global__ void __launch_bounds__(1024) cdc_scan_kernel(int pass, int m, CdcScra
   }
 }
 
+// Monomial coefficients of the Lagrange basis on n[0..m): A[k][a] = coefficient of t^a in
+// prod_{k' != k} (t - n_k') / (n_k - n_k'), in double (one thread).
+__device__ void lagrange_monomial(const double* n, int m, double (*A)[kCdcBiv]) {
+  for (int k = 0; k < m; ++k) {
+    double q[kCdcBiv] = {1.0};
+    double den = 1.0;
+    int deg = 0;
+    for (int k2 = 0; k2 < m; ++k2) {
+      if (k2 == k) continue;
+      for (int a = deg + 1; a >= 0; --a) q[a] = (a > 0 ? q[a - 1] : 0.0) - n[k2] * (a <= deg ? q[a] : 0.0);
+      ++deg;
+      den *= n[k] - n[k2];
+    }
+    for (int a = 0; a < m; ++a) A[k][a] = q[a] / den;
+  }
+}
+
+// D = A^T C B of the step's table (CdcTable::D); skipped for repeated / unordered points (nearest-row rule)
+template <class T>
+__device__ void cdc_bivariate(const RunParams& p, T* s, int m) {
+  if (s->degenerate) return;
+  const double c = 0.5 * (s->zd[0] + s->zd[m - 1]), h = 0.5 * (s->zd[m - 1] - s->zd[0]);
+  double sn[kCdcBiv], xn[kCdcBiv], A[kCdcBiv][kCdcBiv], B[kCdcBiv][kCdcBiv];
+  for (int k = 0; k < m; ++k) {
+    sn[k] = (s->zd[k] - c) / h;
+    xn[k] = (double)p.xhi[k] + (double)p.xlo[k];
+  }
+  lagrange_monomial(sn, m, A);
+  lagrange_monomial(xn, m, B);
+  double CB[kCdcBiv][kCdcBiv];
+  for (int k = 0; k < m; ++k)
+    for (int b = 0; b < m; ++b) {
+      double a = 0.0;
+      for (int j = 0; j < m; ++j) a += (double)s->C[k][j] * B[j][b];
+      CB[k][b] = a;
+    }
+  for (int a = 0; a < kCdcBiv; ++a)
+    for (int b = 0; b < kCdcBiv; ++b) {
+      double v = 0.0;
+      if (a < m && b < m)
+        for (int k = 0; k < m; ++k) v += A[k][a] * CB[k][b];
+      s->D[a][b] = (float)v;
+    }
+  s->shinv = (float)(1.0 / h);
+  s->sc = (float)(-c / h);
+}
+
 // ---- table rows C[k][.] = H(z_k)
 __global__ void cdc_table_exact_kernel(const __grid_constant__ RunParams p, CdcScratch* s) {
   const int k = threadIdx.x / kMaxM, j = threadIdx.x % kMaxM;
-  if (k >= p.m || j >= p.m) return;
-  const float zk = s->z[k];
-  s->C[k][j] = (p.colloc == kExactGbm) ? zk * p.c[j] : fmaf(p.ou_a, zk, p.ou_b) + p.c[j];
+  if (k < p.m && j < p.m) {
+    const float zk = s->z[k];
+    s->C[k][j] = (p.colloc == kExactGbm) ? zk * p.c[j] : fmaf(p.ou_a, zk, p.ou_b) + p.c[j];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && p.m <= kCdcBiv) cdc_bivariate(p, s, p.m);
 }
 
 // MLP on `rows` states zin[0..rows), fp32 with the accurate activations of the FP32 kernel, layer 1 folded
@@ -366,57 +419,13 @@ __device__ void cdc_mlp_rows(const RunParams& p, const float* l1b, const float* 
 // table rows C[k][.] = H(z_k) with the network (the run's dt)
 template <int ACT>
 __global__ void __launch_bounds__(256) cdc_table_mlp_kernel(const __grid_constant__ RunParams p, CdcScratch* s) {
-  cdc_mlp_rows<ACT>(p, p.l1b, p.out_scale, p.out_shift, s->z, p.m, s->C);
+  cdc_mlp_rows<ACT>(p, p.l1b, p.out_scale, p.out_shift, s->z, p.m, s->C);   // ends with a block barrier
+  if (threadIdx.x == 0 && p.m <= kCdcBiv) cdc_bivariate(p, s, p.m);
 }
 
 // SL7_SCHEME_CDC_PRED (reading R-26): the marginal collocation points of Y(t_i) are the predictor's at
 // (Y0, t_i = i dt, theta) -- the horizon's folded constants hz -- instead of quantiles of the paths
 // (t_0: every path at Y0, a degenerate table); then the table rows as above.  One block.
-// Monomial coefficients of the Lagrange basis on n[0..m): A[k][a] = coefficient of t^a in
-// prod_{k' != k} (t - n_k') / (n_k - n_k'), in double (one thread).
-__device__ void lagrange_monomial(const double* n, int m, double (*A)[kCdcBiv]) {
-  for (int k = 0; k < m; ++k) {
-    double q[kCdcBiv] = {1.0};
-    double den = 1.0;
-    int deg = 0;
-    for (int k2 = 0; k2 < m; ++k2) {
-      if (k2 == k) continue;
-      for (int a = deg + 1; a >= 0; --a) q[a] = (a > 0 ? q[a - 1] : 0.0) - n[k2] * (a <= deg ? q[a] : 0.0);
-      ++deg;
-      den *= n[k] - n[k2];
-    }
-    for (int a = 0; a < m; ++a) A[k][a] = q[a] / den;
-  }
-}
-
-// D = A^T C B of the step's table (CdcTable::D); skipped for repeated / unordered points (nearest-row rule)
-__device__ void cdc_bivariate(const RunParams& p, CdcTable* s, int m) {
-  if (s->degenerate) return;
-  const double c = 0.5 * (s->zd[0] + s->zd[m - 1]), h = 0.5 * (s->zd[m - 1] - s->zd[0]);
-  double sn[kCdcBiv], xn[kCdcBiv], A[kCdcBiv][kCdcBiv], B[kCdcBiv][kCdcBiv];
-  for (int k = 0; k < m; ++k) {
-    sn[k] = (s->zd[k] - c) / h;
-    xn[k] = (double)p.xhi[k] + (double)p.xlo[k];
-  }
-  lagrange_monomial(sn, m, A);
-  lagrange_monomial(xn, m, B);
-  double CB[kCdcBiv][kCdcBiv];
-  for (int k = 0; k < m; ++k)
-    for (int b = 0; b < m; ++b) {
-      double a = 0.0;
-      for (int j = 0; j < m; ++j) a += (double)s->C[k][j] * B[j][b];
-      CB[k][b] = a;
-    }
-  for (int a = 0; a < kCdcBiv; ++a)
-    for (int b = 0; b < kCdcBiv; ++b) {
-      double v = 0.0;
-      if (a < m && b < m)
-        for (int k = 0; k < m; ++k) v += A[k][a] * CB[k][b];
-      s->D[a][b] = (float)v;
-    }
-  s->shinv = (float)(1.0 / h);
-  s->sc = (float)(-c / h);
-}
 
 template <int ACT, class T>
 __device__ void cdc_pred_table_body(const RunParams& p, const CdcHorizon& hz, T* s, int step) {
@@ -448,10 +457,8 @@ __device__ void cdc_pred_table_body(const RunParams& p, const CdcHorizon& hz, T*
       s->C[k][j] = (p.colloc == kExactGbm) ? zk * p.c[j] : fmaf(p.ou_a, zk, p.ou_b) + p.c[j];
     }
   }
-  if constexpr (std::is_same<T, CdcTable>::value) {   // the fused kernel's tables (not the per-step scratch)
-    __syncthreads();
-    if (threadIdx.x == 0 && m <= kCdcBiv) cdc_bivariate(p, s, m);
-  }
+  __syncthreads();
+  if (threadIdx.x == 0 && m <= kCdcBiv) cdc_bivariate(p, s, m);
 }
 
 template <int ACT, class T>
@@ -482,6 +489,10 @@ __global__ void __launch_bounds__(256) cdc_step_kernel(const __grid_constant__ R
   __shared__ double red[8];
   __shared__ float sz[kMaxM], szlo[kMaxM], sv[kMaxM], sC[kMaxM][kMaxM], ssinv;
   __shared__ int sdeg;
+  // m <= kCdcBiv at compile time: the non-degenerate step is ONE bivariate polynomial in s = Y shinv + sc and X
+  // (CdcScratch::D, built by the table kernel) instead of the basis in the state, the contraction and g_m
+  constexpr bool BIV = !RT_M && MR <= kCdcBiv;
+  __shared__ float sD[kCdcBiv][kCdcBiv], sshinv, ssc;
   __shared__ uint32_t nh[256];   // pass-0 digit histogram of the new states (next step's selection)
   if (next_hist)
     for (int i = threadIdx.x; i < 256; i += blockDim.x) nh[i] = 0u;
@@ -496,18 +507,33 @@ __global__ void __launch_bounds__(256) cdc_step_kernel(const __grid_constant__ R
     if (threadIdx.x == 0) ssinv = s->sinv;
   }
   if (threadIdx.x == 0) sdeg = s->degenerate;
+  if (BIV) {
+    for (int i = threadIdx.x; i < kCdcBiv * kCdcBiv; i += blockDim.x) sD[i / kCdcBiv][i % kCdcBiv] = s->D[i / kCdcBiv][i % kCdcBiv];
+    if (threadIdx.x == 0) {
+      sshinv = s->shinv;
+      ssc = s->sc;
+    }
+  }
   if (last) hist_init(p, hist);
   __syncthreads();
   const int m = p.m;
   // the m x m table in registers when m is a compile-time constant (49 for m = 7): it is the same for every
   // path, and reading it from shared memory cost one LDS per FFMA of the contraction below
-  float Cr[RT_M ? 1 : MR][RT_M ? 1 : MR];
-  if constexpr (!RT_M) {
+  float Cr[RT_M || BIV ? 1 : MR][RT_M || BIV ? 1 : MR];
+  if constexpr (!RT_M && !BIV) {
 #pragma unroll
     for (int k = 0; k < MR; ++k)
 #pragma unroll
       for (int j = 0; j < MR; ++j) Cr[k][j] = sC[k][j];
   }
+  float Dr[BIV ? MR : 1][BIV ? MR : 1];
+  if constexpr (BIV) {
+#pragma unroll
+    for (int a = 0; a < MR; ++a)
+#pragma unroll
+      for (int b = 0; b < MR; ++b) Dr[a][b] = sD[a][b];
+  }
+  const float shinv = sshinv, sc = ssc;
   StatAcc acc;
   uint32_t ncl = 0;   // CDC_PRED: clamped path-steps of this step (stats E1)
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -523,7 +549,7 @@ __global__ void __launch_bounds__(256) cdc_step_kernel(const __grid_constant__ R
     if (q + stride < p.n_paths) Ynext = yin[q + stride];   // yin may alias yout: a different path's slot
     int nbin = -1;
     if (q < p.n_paths) {
-    float y[MR];
+    float y[MR], sst = 0.0f;
     if (sdeg) {
       int kb = 0;
       float db = fabsf(Y - sz[0]);
@@ -541,6 +567,9 @@ __global__ void __launch_bounds__(256) cdc_step_kernel(const __grid_constant__ R
       // CDC_PRED (R-26): the state clamped to the marginal hull (zlo = 0 there: the points are fp32); NaN stays
       const float Yb = !clamp_hull ? Y : (Y < sz[0]) ? sz[0] : (Y > sz[m - 1]) ? sz[m - 1] : Y;
       ncl += (clamp_hull && (Y < sz[0] || Y > sz[m - 1])) ? 1u : 0u;
+      if constexpr (BIV) {
+        sst = fmaf(Yb, shinv, sc);
+      } else {
       for (int k = 0; k < MR; ++k) d[k] = (RT_M && k >= m) ? 1.0f : ((Yb - sz[k]) - szlo[k]) * ssinv;
       pre[0] = 1.0f;
 #pragma unroll
@@ -563,6 +592,7 @@ __global__ void __launch_bounds__(256) cdc_step_kernel(const __grid_constant__ R
         }
         y[j] = a * rden;
       }
+      }
     }
     // X_hat for (path, step): the Philox block of the step, then only the Box-Muller pair that holds it
     const uint64_t gp = p.path_offset + q;
@@ -572,7 +602,20 @@ __global__ void __launch_bounds__(256) cdc_step_kernel(const __grid_constant__ R
     if constexpr (FAST) box_muller_fast((r < 2) ? rr.x : rr.z, (r < 2) ? rr.y : rr.w, za, zb);
     else box_muller((r < 2) ? rr.x : rr.z, (r < 2) ? rr.y : rr.w, za, zb);
     const float Z = (r & 1) ? zb : za;
-    const float Yn = gm_eval<MR, RT_M>(p, Z, y);
+    float Yn;
+    if (BIV && !sdeg) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int b = MR - 1; b >= 0; --b) {
+        float qv = Dr[MR - 1][b];
+#pragma unroll
+        for (int a = MR - 2; a >= 0; --a) qv = fmaf(qv, sst, Dr[a][b]);
+        acc = (b == MR - 1) ? qv : fmaf(acc, Z, qv);
+      }
+      Yn = acc;
+    } else {
+      Yn = gm_eval<MR, RT_M>(p, Z, y);
+    }
     yout[q] = Yn;
     if (last && p.has_stats) stat_add(acc, p, Yn, 0.0, hist);
     nbin = isfinite(Yn) ? (int)(f2key(Yn) >> 24) : -1;
