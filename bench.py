@@ -98,6 +98,7 @@ class ClockSampler(threading.Thread):
         super().__init__(daemon=True)
         self.index = index
         self.samples, self.reasons = [], set()
+        self.reason_counts = {}   # samples per reason (GpuIdle can appear in the gaps between timed launches)
         self.max_mhz = None
         self._halt = threading.Event()
         self.ok = True
@@ -115,7 +116,9 @@ class ClockSampler(threading.Thread):
                 r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
                 for bit, name in names.items():
                     if bit and bit != 0xFFFFFFFFFFFFFFFF and (r & bit) == bit and "All" not in name and "None" not in name:
-                        self.reasons.add(name.replace("nvmlClocksThrottleReason", ""))
+                        nm = name.replace("nvmlClocksThrottleReason", "")
+                        self.reasons.add(nm)
+                        self.reason_counts[nm] = self.reason_counts.get(nm, 0) + 1
                 time.sleep(0.1)
         except Exception as e:  # NVML missing: report, do not fake
             self.ok = False
@@ -127,7 +130,8 @@ class ClockSampler(threading.Thread):
 
     def summary(self):
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+                "reasons": sorted(self.reasons), "reason_samples": dict(sorted(self.reason_counts.items())),
+                "samples": len(self.samples)}
 
 
 def measured_peaks():
