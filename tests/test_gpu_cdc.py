@@ -91,3 +91,29 @@ def test_cdc_rejects_reference_and_tc(gpu_lib):
     o = sl7.make_opts(colloc=sl7.COLLOC_EXACT_GBM, scheme=sl7.SCHEME_CDC, ref=sl7.REF_GBM, ref_theta=(0.05, 0.2, 0))
     with pytest.raises(sl7.Sl7Error, match="EUNSUPPORTED"):
         ctx.simulate(1.0, 0.5, 2, (0.05, 0.2), 100, 1, sl7.OUT_TERMINAL, o)
+
+
+@pytest.mark.parametrize("name", ["ou_exact", "cfg2_ou_ann"])
+def test_cdc_terminal_moments_identical_paths(gpu_lib, name):
+    """T-4 for the quantile-marginal 7L-CDC: the device runs the 2e4 paths of one call free from Y0 (their own
+    empirical quantiles each step), the oracle runs the same path set with its float64 quantiles; terminal mean
+    and variance within 1e-4 relative (cfg2's OU network over its 16 steps, and exact OU collocation)."""
+    import torch
+    sl7 = gpu_lib
+    case = {c[0]: c for c in CASES}[name]
+    _, m, colloc, theta, y0, dt, _ = case
+    ctx, code, th, spec = _setup(sl7, name, m, colloc, theta, y0, dt, 16)
+    n = 20_000
+    opts = sl7.make_opts(prec=sl7.PREC_FP32, colloc=code, scheme=sl7.SCHEME_CDC)
+    out, _ = ctx.simulate(spec.y0, spec.dt, 16, th, n, 11, sl7.OUT_TERMINAL, opts)
+    torch.cuda.synchronize()
+    YT = out.double().cpu().numpy()
+    with np.errstate(all="ignore"):
+        Y, _ = O.simulate_cdc(spec, 11, np.arange(n, dtype=np.uint64))
+    Yo = Y[-1]
+    assert np.all(np.isfinite(YT)) and np.all(np.isfinite(Yo))
+    mo, vo = Yo.mean(), Yo.var()
+    scale = abs(mo) if abs(mo) >= 1e-3 * np.sqrt(vo) else np.sqrt(vo)
+    print("%s CDC: dmean/scale %.2g dvar/var %.2g" % (name, abs(YT.mean() - mo) / scale, abs(YT.var() - vo) / vo))
+    assert abs(YT.mean() - mo) <= 1e-4 * scale
+    assert abs(YT.var() - vo) <= 1e-4 * vo
