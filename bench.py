@@ -16,6 +16,7 @@ At N=1 the line also carries "modes": the other BASELINE configs, each timed on 
 (L2 flushed, CUDA events, NVML clocks) with its own algorithmic roofline:
   cfg3  exact-collocation GBM, FULL step-major [65][2e8] fp32 path tensor (52 GB): HBM-store-bound;
   cfg2  OU and CIR (the paper's process, PAPER.md:83) in BF16 / TF32 / SPLIT / FP32, exact OU, CDC_PRED;
+  cfg4  the headline workload in TF32 / SPLIT / FP32 (1e8 paths; FP32 2.5e7) and with CDC_PRED;
   cfg1  the GBM dt sweep n = 1..64 (1e7 paths) in BF16 / TF32 / SPLIT / FP32 and exact GBM.
 
 python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--prec bf16|tf32|split|fp32]
@@ -534,6 +535,36 @@ def run_modes(sl7, torch, dev, stream, peaks, n_sms, sm_max):
                                     "terminal": {"mean": s["mean"], "var": s["var"], "strong_err": s["strong_err"]},
                                     "roofline": issue_roof(rate, exact_instr(w.m), "Philox/4 + Box-Muller + g_m + "
                                                            "the Eq. 6.6 reference"), "clocks": clk}
+
+    # ---- cfg4's workload (the headline's) in the other precisions and with CDC_PRED: 1e8 paths (FP32 2.5e7),
+    # the same 32 steps to T = 4, terminal moments against the CIR law
+    w = Wl["cfg4"]
+    ctx = sl7.Context(w.m, list(w.dims), w.act, device=dev.index)
+    ctx.load_weights(load_golden_blob(w.blob))
+    lo, hi = HIST[w.process]
+    for pn, pc in P[1:]:
+        n_p = 100_000_000 if pc != sl7.PREC_FP32 else 25_000_000
+        o = sl7.make_opts(prec=pc, colloc=sl7.COLLOC_ANN, stream=stream, n_bins=N_BINS, hist_lo=lo, hist_hi=hi,
+                          shift=w.y0)
+        ms, clk = timed(lambda o=o, n_p=n_p: ctx.simulate(w.y0, w.dt, w.n_steps, w.theta, n_p, w.seed,
+                                                             sl7.OUT_STATS, o, stats=stats))
+        rate = n_p * w.n_steps / (ms * 1e-3)
+        s = sl7.stats_summary(stats.cpu().numpy(), o)
+        out["cfg4_%s" % pn] = {"path_steps_per_s": rate, "ms": ms, "paths": n_p, "n_steps": w.n_steps,
+                               "terminal": {"mean": s["mean"], "var": s["var"]},
+                               "roofline": ann_roofline(w.dims, pc, rate, sl7, peaks, n_sms, sm_max), "clocks": clk}
+    o = sl7.make_opts(prec=sl7.PREC_FP32, colloc=sl7.COLLOC_ANN, scheme=sl7.SCHEME_CDC_PRED, stream=stream,
+                      n_bins=N_BINS, hist_lo=lo, hist_hi=hi, shift=w.y0)
+    ms, clk = timed(lambda o=o: ctx.simulate(w.y0, w.dt, w.n_steps, w.theta, 100_000_000, w.seed, sl7.OUT_STATS, o,
+                                             stats=stats))
+    rate = 100_000_000 * w.n_steps / (ms * 1e-3)
+    s = sl7.stats_summary(stats.cpu().numpy(), o)
+    out["cfg4_cdc_pred"] = {"path_steps_per_s": rate, "ms": ms, "paths": 100_000_000, "n_steps": w.n_steps,
+                            "scheme": "7L-CDC with predicted marginal points (DESIGN.md R-26)",
+                            "terminal": {"mean": s["mean"], "var": s["var"]}, "clamped_path_steps": s.get("clamped_steps"),
+                            "roofline": issue_roof(rate, cdc_pred_instr(w.m), "Philox/4 + Box-Muller + clamp + the "
+                                                   "step as one bivariate polynomial in (state, X)"), "clocks": clk}
+    ctx.close()
 
     # ---- cfg1: the GBM dt sweep n = 1..64 at 1e7 paths (127 path-steps per path)
     w = Wl["cfg1"]
