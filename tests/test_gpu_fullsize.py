@@ -180,3 +180,25 @@ def test_cfg4_full_size(gpu_lib):
     Z = O.normals(w.seed, (off + ids).astype(np.uint64), w.n_steps)
     worst = _teacher_forced_sample(spec, rows, off + ids, w.seed, 5e-3, Z=Z)
     print("cfg4 top-of-range bf16 sampled worst |err|/kappa = %.3g" % worst)
+
+
+def test_cfg4_paths_across_2_pow_32(gpu_lib):
+    """64-bit global path ids in the headline kernel: 65,536 paths starting 32,768 below 2^32 (the Philox
+    counter's high path word turns over in the middle of a tile group), FULL output, teacher-forced against O6
+    on sampled paths on both sides of the boundary."""
+    sl7 = gpu_lib
+    torch = _torch()
+    w = workloads()["cfg4"]
+    blob = load_golden_blob(w.blob)
+    ctx = sl7.Context(w.m, list(w.dims), w.act)
+    ctx.load_weights(blob)
+    n, off = 65536, (1 << 32) - 32768
+    o = sl7.make_opts(prec=sl7.PREC_BF16, colloc=sl7.COLLOC_ANN, path_offset=off)
+    full, _ = ctx.simulate(w.y0, w.dt, w.n_steps, w.theta, n, w.seed, sl7.OUT_FULL, o)
+    torch.cuda.synchronize()
+    ids = np.unique(np.concatenate([_sample_ids(n, 400), np.arange(32768 - 64, 32768 + 64)]))
+    rows = full.view(w.n_steps + 1, n)[:, torch.as_tensor(ids, device="cuda")].double().cpu().numpy()
+    spec = O.Spec(w.m, "ann", tuple(w.theta), w.y0, w.dt, w.n_steps, net=O.parse_blob(blob), quant="bf16")
+    Z = O.normals(w.seed, (off + ids).astype(np.uint64), w.n_steps)
+    worst = _teacher_forced_sample(spec, rows, off + ids, w.seed, 5e-3, Z=Z)
+    print("cfg4 paths across 2^32: worst |err|/kappa = %.3g" % worst)
