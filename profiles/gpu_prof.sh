@@ -16,6 +16,7 @@ for w in $W; do
     cfg3)  K=regex:exact_full4_kernel;  CMD="python profiles/exact_probe.py 50000000 1" ;;
     cdcpred) K=regex:cdc_pred_fused;    CMD="python profiles/cdc_probe.py 20000000 pred 1" ;;
     cdcstep) K=regex:cdc_step_kernel;   CMD="python profiles/cdc_probe.py 20000000 quantile" ;;
+    cdchist) K=regex:cdc_hist_kernel;   CMD="python profiles/cdc_probe.py 100000000 quantile" ;;
   esac
   timeout 600 $NCU -k $K -s 1 -c 1 -o $O/${T}_$w -f $CMD > $O/${T}_$w.log 2>&1
   echo "$w ncu rc=$?"
