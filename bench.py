@@ -15,7 +15,8 @@ inside the timed region; the step time is the max over ranks.
 At N=1 the line also carries "modes": the other BASELINE configs, each timed on the device the same way
 (L2 flushed, CUDA events, NVML clocks) with its own algorithmic roofline:
   cfg3  exact-collocation GBM, FULL step-major [65][2e8] fp32 path tensor (52 GB): HBM-store-bound;
-  cfg2  OU and CIR (the paper's process, PAPER.md:83) in BF16 / TF32 / SPLIT / FP32, exact OU, CDC_PRED;
+  cfg2  OU and CIR (the paper's process) in BF16 / TF32 / SPLIT / FP32, exact OU, CDC_PRED (OU also
+        with fast normals) and the quantile-marginal 7L-CDC (OU);
   cfg4  the headline workload in TF32 / SPLIT / FP32 (1e8 paths; FP32 2.5e7) and with CDC_PRED;
   cfg1  the GBM dt sweep n = 1..64 (1e7 paths) in BF16 / TF32 / SPLIT / FP32 and exact GBM.
 
@@ -524,6 +525,25 @@ def run_modes(sl7, torch, dev, stream, peaks, n_sms, sm_max):
                                     "frac_vs_lagrange_form_budget": rate * cdc_pred_instr_lagrange(w.m) / issue_peak,
                                     "clocks": clk}
         if w.process == "ou":
+            # the same with the fast Box-Muller (SL7_FLAG_FAST_NORMALS, |dX| <= 2e-6 (1 + |X|)), and the quantile-
+            # marginal 7L-CDC (R-18: the paper's CDC with the marginal points from all paths' states each step)
+            for label, sch, fl in (("cdc_pred_fast_normals", sl7.SCHEME_CDC_PRED, sl7.FLAG_FAST_NORMALS),
+                                   ("cdc_quantile", sl7.SCHEME_CDC, 0)):
+                o = sl7.make_opts(prec=sl7.PREC_FP32, colloc=sl7.COLLOC_ANN, scheme=sch, stream=stream, flags=fl,
+                                  n_bins=N_BINS, hist_lo=lo, hist_hi=hi, shift=w.y0)
+                ms, clk = timed(lambda o=o: ctx.simulate(w.y0, w.dt, w.n_steps, w.theta, N, w.seed, sl7.OUT_STATS, o,
+                                                         stats=stats))
+                rate = N * w.n_steps / (ms * 1e-3)
+                s = sl7.stats_summary(stats.cpu().numpy(), o)
+                line = {"path_steps_per_s": rate, "ms": ms, "paths": N, "n_steps": w.n_steps,
+                        "terminal": {"mean": s["mean"], "var": s["var"]}, "clocks": clk}
+                if sch == sl7.SCHEME_CDC_PRED:
+                    line["roofline"] = issue_roof(rate, cdc_pred_instr(w.m), "Philox/4 + fast Box-Muller + clamp + "
+                                                  "the step as one bivariate polynomial in (state, X)")
+                else:
+                    line["scheme"] = ("per step: marginal points = exact quantiles of all paths (3 radix-select passes "
+                                      "over the states + the pass fused into the step kernel), the m-row table, the step")
+                out["%s_%s" % (key, label)] = line
             exo = sl7.Context(w.m, device=dev.index)
             o = sl7.make_opts(prec=sl7.PREC_FP32, colloc=sl7.COLLOC_EXACT_OU, stream=stream, n_bins=N_BINS,
                               hist_lo=lo, hist_hi=hi, shift=w.y0, ref=sl7.REF_OU, ref_theta=w.theta)
