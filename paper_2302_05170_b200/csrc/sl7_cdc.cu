@@ -335,8 +335,9 @@ __device__ void lagrange_monomial(const double* n, int m, double (*A)[kCdcBiv]) 
 // D = A^T C B of the step's table (CdcTable::D); skipped for repeated / unordered points (nearest-row rule)
 template <class T>
 __device__ void cdc_bivariate(const RunParams& p, T* s, int m) {
-  if (s->degenerate) return;
+  if (s->degenerate || m < 2) return;
   const double c = 0.5 * (s->zd[0] + s->zd[m - 1]), h = 0.5 * (s->zd[m - 1] - s->zd[0]);
+  if (!(h > 0.0) || !isfinite(h)) return;   // (the step kernels only read D for ordered, finite points)
   double sn[kCdcBiv], xn[kCdcBiv], A[kCdcBiv][kCdcBiv], B[kCdcBiv][kCdcBiv];
   for (int k = 0; k < m; ++k) {
     sn[k] = (s->zd[k] - c) / h;
