@@ -15,6 +15,7 @@
 // sequence of launches on the caller's stream; HBM traffic per path-step: 4 selection reads + 1 read
 // + 1 write of 4 bytes.
 #include <cuda_runtime.h>
+#include <math_constants.h>
 
 #include <cstdlib>
 #include <cstring>
@@ -337,7 +338,13 @@ template <class T>
 __device__ void cdc_bivariate(const RunParams& p, T* s, int m) {
   if (s->degenerate || m < 2) return;
   const double c = 0.5 * (s->zd[0] + s->zd[m - 1]), h = 0.5 * (s->zd[m - 1] - s->zd[0]);
-  if (!(h > 0.0) || !isfinite(h)) return;   // (the step kernels only read D for ordered, finite points)
+  if (!(h > 0.0) || !isfinite(h)) {   // marginal points at +-inf (a diverged run): the step yields NaN, as the
+    for (int a = 0; a < kCdcBiv; ++a)   // Lagrange form would, and the paths are counted as non-finite
+      for (int b = 0; b < kCdcBiv; ++b) s->D[a][b] = CUDART_NAN_F;
+    s->shinv = 0.0f;
+    s->sc = CUDART_NAN_F;
+    return;
+  }
   double sn[kCdcBiv], xn[kCdcBiv], A[kCdcBiv][kCdcBiv], B[kCdcBiv][kCdcBiv];
   for (int k = 0; k < m; ++k) {
     sn[k] = (s->zd[k] - c) / h;
