@@ -131,3 +131,33 @@ def test_cdc_pred_clamped_counts_states_outside_the_hull():
     Y[2] = [z2[0], z2[-1], z2[-1] + 1e-9, z2[0] - 5.0]
     Y[3] = 123.0                                   # the terminal row is never read by a table
     assert O.cdc_pred_clamped(spec, Y) == 2 + 2
+
+
+@pytest.mark.parametrize("m", [5, 7])
+def test_bivariate_form_of_the_cdc_step_is_the_same_polynomial(m):
+    # the device evaluates the CDC(_PRED) step as ONE bivariate polynomial Y' = sum_a sum_b D[a][b] s^a X^b,
+    # D = A^T C B (A, B: monomial coefficients of the Lagrange bases on the hull-normalised marginal points and on
+    # the Gauss-Hermite nodes).  Mathematically it is the oracle's two-stage Lagrange step: checked
+    # here in float64 on a random table, inside and outside the hull, with numpy's polynomial routines building A, B
+    rng = np.random.default_rng(m)
+    x = O.gauss_hermite_nodes(m)
+    z = np.sort(rng.uniform(-1.0, 2.0, m))
+    C = rng.normal(size=(m, m))
+    c, h = 0.5 * (z[0] + z[-1]), 0.5 * (z[-1] - z[0])
+    sn = (z - c) / h
+
+    def mono(nodes):   # A[k][a] = coefficient of t^a in the k-th Lagrange basis polynomial
+        A = np.zeros((len(nodes), len(nodes)))
+        for k in range(len(nodes)):
+            others = np.delete(nodes, k)
+            poly = np.polynomial.polynomial.polyfromroots(others) / np.prod(nodes[k] - others)
+            A[k] = poly
+        return A
+
+    D = mono(sn).T @ C @ mono(x)
+    Y = rng.uniform(z[0] - 0.3, z[-1] + 0.3, 500)
+    X = rng.normal(size=500) * 2
+    s = (Y - c) / h
+    biv = np.einsum("pa,ab,pb->p", np.vander(s, m, increasing=True), D, np.vander(X, m, increasing=True))
+    ref = O.lagrange_eval(X, x, O.lagrange_basis(Y, z) @ C)
+    np.testing.assert_allclose(biv, ref, rtol=1e-9, atol=1e-9 * np.abs(ref).max())
