@@ -106,14 +106,15 @@ def test_cdc_pred_stats_match_full(gpu_lib):
     np.testing.assert_allclose(s[2:6], v[2:6], rtol=1e-12, atol=1e-9)
 
 
-@pytest.mark.parametrize("name", ["cfg2_cir", "cfg4"])
+@pytest.mark.parametrize("name", ["cfg2_cir", "cfg4", "cfg2_ou"])
 def test_cdc_pred_cir_terminal_moments_identical_paths(gpu_lib, name):
     # T-4 on the identical path set: the device's CDC_PRED run of paths 0..2e4-1 against the oracle's
     # free run of the same paths (fp32 table; O3), terminal mean and variance within 1e-4 relative
     import torch
     sl7 = gpu_lib
     w = workloads()[name]
-    ctx, code, th, spec = _setup(sl7, "cfg2_cir_ann", 7, "ann", None, None, None, w.n_steps)
+    ctx, code, th, spec = _setup(sl7, "cfg2_ou_ann" if name == "cfg2_ou" else "cfg2_cir_ann", 7, "ann", None, None,
+                                 None, w.n_steps)
     spec = O.Spec(w.m, "ann", th, w.y0, w.dt, w.n_steps, net=spec.net)
     n = 20_000
     o = sl7.make_opts(colloc=code, scheme=sl7.SCHEME_CDC_PRED)
